@@ -1,0 +1,147 @@
+/*
+ * cbie.h — C-ABI of libcbie.so, the B200 (sm_100a) implementation of the
+ * CBIE fill -> ACA -> H-LU hot path of the chebscat reference
+ * (arXiv 2408.17116; reference sources /root/reference/pkg/src/chebscat/).
+ *
+ * Plain C types only: pointers + sizes, no torch / numpy types.  Host arrays
+ * belong to the caller and are read/written during the call only.  Device
+ * memory belongs to the handles.  Every call is synchronous on return.
+ * Return value: 0 on success, else one of the CBIE_E* codes below (the
+ * Python shim maps them onto the reference exception hierarchy,
+ * errors.py:1-73).  cbie_last_error() gives the message.
+ *
+ * Index conventions (identical to the reference):
+ *   points are patch-major, node flat index k*nu + l (u fastest)   geometry.py:145-155
+ *   dof = point*C + component (components interleaved)               assembly.py:41-58
+ *   dense outputs are row-major (numpy C order)
+ */
+#ifndef CBIE_H
+#define CBIE_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct cbie_ctx cbie_ctx;
+typedef struct cbie_hmat cbie_hmat;
+typedef struct cbie_hlu cbie_hlu;
+typedef struct { double re, im; } cbie_c128;   /* == numpy complex128 */
+
+enum {
+  CBIE_OK = 0,
+  CBIE_ESINGULAR_DIAGONAL = 1,   /* errors.py:40  SingularDiagonal  */
+  CBIE_EDEGENERATE_PATCH = 2,    /* errors.py:8   DegeneratePatch   */
+  CBIE_ESINGULAR_POINT = 3,      /* errors.py:28  SingularPoint     */
+  CBIE_ECAP_EXCEEDED = 4,        /* errors.py:44  CapExceeded       */
+  CBIE_ERANK_OVERFLOW = 5,       /* errors.py:36  RankOverflow      */
+  CBIE_ECUDA = 10,
+  CBIE_EOOM = 12,
+  CBIE_EINVALID = 13,
+  CBIE_ESTATE = 14               /* call made before its prerequisites */
+};
+
+enum { CBIE_CHART_SAMPLES = 0, CBIE_CHART_CUBE_SPHERE = 1, CBIE_CHART_STAR = 2 };
+enum { CBIE_MFIE_PEC = 0, CBIE_MULLER = 1 };
+enum { CBIE_FAR = 0, CBIE_NEAR = 1, CBIE_SELF = 2 };
+
+/* Context on one CUDA device (one process per GPU).
+ * Replaces the construction of EntryGenerator (assembly.py:68-95). */
+int cbie_create(int device, cbie_ctx** out);
+void cbie_destroy(cbie_ctx* ctx);
+const char* cbie_last_error(const cbie_ctx* ctx);
+
+/* Patch geometry, uniform order nu x nv for all patches.
+ *   samples      [npatch][nu][nv][3]   == Patch.samples[l, k, :]   (geometry.py:100-117)
+ *   chart_kind   [npatch]              CBIE_CHART_*
+ *   chart_params [npatch][8]           cube sphere: radius, face, u_lo, u_hi, v_lo, v_hi
+ *                                      (geometry.py:63-68); star: radius, face, u_lo..v_hi
+ *   star_coef    [25] real Y_lm coefficients (l<=4) for CBIE_CHART_STAR, else NULL
+ *   cheb_coef    [npatch][6][3][nu][nv] Chebyshev coefficient tensors of the samples
+ *                (position, d/du, d/dv, d2/du2, d2/dudv, d2/dv2; Patch.position_coeffs +
+ *                deriv_coeffs, geometry.py:137-143, 228-238) or NULL to compute them
+ *                natively.  Passing the host's numpy tensors makes interpolated
+ *                positions bit-identical to the reference's.
+ * Replaces Patch/CubeSphereFace/eval_frames (geometry.py:48-220). */
+int cbie_set_geometry(cbie_ctx* ctx, int npatch, int nu, int nv, const double* samples,
+                      const int* chart_kind, const double* chart_params, const double* star_coef,
+                      const double* cheb_coef);
+
+/* Node frames computed on the device: pos/a_u/a_v [npts][3], sqrt_g [npts]
+ * (Patch.node_frames, geometry.py:157-163).  Any pointer may be NULL. */
+int cbie_node_frames(cbie_ctx* ctx, double* pos, double* a_u, double* a_v, double* sqrt_g);
+
+/* Formulation and quadrature parameters (kernels.py:31-100, quadrature.py:26-56,
+ * solver.py:102-117).  k1/k2 are Medium.k of outer/inner media (k2 ignored for
+ * MFIE); row/col scales are the per-component equilibration factors
+ * (length C = 2 or 4). */
+int cbie_set_formulation(cbie_ctx* ctx, int kind, double omega, cbie_c128 k1, cbie_c128 k2,
+                         cbie_c128 eps1, cbie_c128 mu1, cbie_c128 eps2, cbie_c128 mu2,
+                         double tau, int grading, int oversample,
+                         const cbie_c128* row_scale_c, const cbie_c128* col_scale_c);
+
+/* FAR/NEAR/SELF classification of every (point, patch) pair plus the near
+ * pair-block table.  Replaces EntryGenerator._classify_patch_column
+ * (assembly.py:106-143) + quadrature.closest_points (quadrature.py:87-140)
+ * + the NEAR/SELF branch of _pair_block_compute (assembly.py:191-213). */
+int cbie_classify(cbie_ctx* ctx, int64_t* n_near, int64_t* n_self, int64_t* n_fallback);
+
+/* Export of the non-FAR classification records, sorted by (point, patch). */
+int cbie_export_classification(cbie_ctx* ctx, int64_t cap, int32_t* point, int32_t* patch,
+                               int8_t* tag, double* u, double* v, int8_t* newton_ok);
+
+/* One canonical pair block (C x nu*nv*C, row-major), EntryGenerator.pair_block
+ * (assembly.py:146-213). */
+int cbie_pair_block(cbie_ctx* ctx, int64_t point, int patch, cbie_c128* out);
+
+/* Sub-block rows x cols (original dof ids) -> out[m][n] row-major.
+ * scaled != 0 applies the equilibration (solver.py:127-129).
+ * Replaces EntryGenerator.block / row_segment / col_segment / entry
+ * (assembly.py:229-271) and EquilibratedGenerator (solver.py:119-129). */
+int cbie_fill_block(cbie_ctx* ctx, const int64_t* rows, int64_t m, const int64_t* cols,
+                    int64_t n, int scaled, cbie_c128* out);
+
+/* Dense matrix (unscaled), assemble_dense (assembly.py:438-460); CBIE_ECAP_EXCEEDED
+ * if N > cap.  out: N x N row-major host buffer. */
+int cbie_fill_dense(cbie_ctx* ctx, int64_t cap, cbie_c128* out);
+
+/* H-matrix of the equilibrated system: cluster tree, block tree, dense leaves,
+ * batched ACA + recompression, demotion.  Replaces build_hmatrix
+ * (solver.py:132-145): build_cluster_tree (hmatrix.py:82), build_block_tree
+ * (hmatrix.py:344), HMatrix.fill (hmatrix.py:207-264), aca (352-409),
+ * truncate_lowrank (412-426). */
+int cbie_hmatrix_build(cbie_ctx* ctx, int n_leaf, double eta, double aca_tol, cbie_hmat** out);
+void cbie_hmatrix_destroy(cbie_hmat* h);
+
+/* Tree export: dof_perm[N] (new -> original, ClusterTree.dof_perm), leaves
+ * [nleaf][6] = r_lo, r_hi, c_lo, c_hi (point units, permuted order), kind
+ * (0 dense, 1 low rank), rank. Pass NULL to query *nleaf only. */
+int cbie_hmatrix_tree(cbie_hmat* h, int64_t* dof_perm, int64_t* leaves, int64_t* nleaf);
+
+/* One leaf in permuted local order (row-major): dense -> D[m][n];
+ * low rank -> U[m][rank], V[rank][n].  hmatrix.py:96-143 */
+int cbie_hmatrix_leaf(cbie_hmat* h, int64_t leaf, int* kind, int* rank, cbie_c128* D_or_U,
+                      cbie_c128* V);
+
+/* y = H x for nrhs column vectors in ORIGINAL dof order, x/y [N][nrhs] row-major.
+ * HMatrix.matvec (hmatrix.py:267-274). */
+int cbie_hmatvec(cbie_hmat* h, const cbie_c128* x, cbie_c128* y, int nrhs);
+
+/* H-LU of the H-matrix (copy; h unchanged).  hlu_factor (hmatrix.py:827-858). */
+int cbie_hlu_factor(cbie_hmat* h, double trunc_tol, cbie_hlu** out);
+void cbie_hlu_destroy(cbie_hlu* f);
+
+/* x = (LU)^{-1} b, original dof order, [N][nrhs] row-major.
+ * HLUFactors.solve (hmatrix.py:807-816). */
+int cbie_hlu_solve(cbie_hlu* f, const cbie_c128* b, cbie_c128* x, int nrhs);
+
+/* Timings (CUDA events), counts, flops, bytes as one JSON object.
+ * which: 0 = context, 1 = hmatrix, 2 = hlu. */
+int cbie_stats_json(const void* handle, int which, char* buf, size_t cap);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CBIE_H */

@@ -1,0 +1,174 @@
+// common.cuh — shared types for libcbie (sm_100a): complex128 helpers, device
+// tables, physics parameters, error handling, device buffers.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/cbie.h"
+
+// ---------------------------------------------------------------------------
+// complex128 on double2 (16-byte aligned, == numpy complex128 == cbie_c128)
+// ---------------------------------------------------------------------------
+typedef double2 zc;
+
+__host__ __device__ __forceinline__ zc zmk(double a, double b) { return make_double2(a, b); }
+__host__ __device__ __forceinline__ zc zadd(zc a, zc b) { return zmk(a.x + b.x, a.y + b.y); }
+__host__ __device__ __forceinline__ zc zsub(zc a, zc b) { return zmk(a.x - b.x, a.y - b.y); }
+__host__ __device__ __forceinline__ zc zmul(zc a, zc b) {
+  return zmk(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+__host__ __device__ __forceinline__ zc zscale(zc a, double s) { return zmk(a.x * s, a.y * s); }
+__host__ __device__ __forceinline__ zc zconj(zc a) { return zmk(a.x, -a.y); }
+__host__ __device__ __forceinline__ double zabs2(zc a) { return a.x * a.x + a.y * a.y; }
+// a * conj(b)
+__host__ __device__ __forceinline__ zc zmulc(zc a, zc b) {
+  return zmk(a.x * b.x + a.y * b.y, a.y * b.x - a.x * b.y);
+}
+// conj(a) * b
+__host__ __device__ __forceinline__ zc zcmul(zc a, zc b) {
+  return zmk(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+__host__ __device__ __forceinline__ zc zdiv(zc a, zc b) {
+  double d = b.x * b.x + b.y * b.y;
+  return zmk((a.x * b.x + a.y * b.y) / d, (a.y * b.x - a.x * b.y) / d);
+}
+// acc += a * b
+__host__ __device__ __forceinline__ void zfma(zc& acc, zc a, zc b) {
+  acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
+  acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
+}
+// e^{-j k R} for complex k (Im k <= 0 for physical media)
+__device__ __forceinline__ zc zexp_mjkR(zc k, double R) {
+  double s, c;
+  sincos(k.x * R, &s, &c);
+  double m = (k.y == 0.0) ? 1.0 : exp(k.y * R);
+  return zmk(m * c, -m * s);
+}
+
+// ---------------------------------------------------------------------------
+// Tables shared by every kernel (passed by value as __grid_constant__).
+// ---------------------------------------------------------------------------
+#define CBIE_MAXO 16      // max patch order per direction
+#define CBIE_MAXS 32      // max oversampled singular-rule order
+
+struct Tables {
+  int nu, nv, np, ns;          // patch orders, nodes per patch, rule order
+  int npatch, npts, C;
+  double xu[CBIE_MAXO], xv[CBIE_MAXO];          // Fejer-1 nodes (descending)
+  double wu[CBIE_MAXO], wv[CBIE_MAXO];          // Fejer-1 weights
+  double Au[CBIE_MAXO * CBIE_MAXO];             // analysis [m][l]: coeff m from value l
+  double Av[CBIE_MAXO * CBIE_MAXO];
+  double Du[CBIE_MAXO * CBIE_MAXO];             // node differentiation [l][m]
+  double Dv[CBIE_MAXO * CBIE_MAXO];
+  double rs[CBIE_MAXS], rw[CBIE_MAXS];          // graded rule: s = sigma^p, w_s
+};
+
+struct Phys {
+  int kind, C;
+  double omega, tau;
+  zc k1, k2, eps1, mu1, eps2, mu2;
+  zc jump[16];                 // C x C jump matrix (kernels.py:85-100)
+  zc rsc[4], csc[4];           // per-component equilibration (solver.py:107-117)
+};
+
+// Device-side geometry pointers (all device memory owned by the ctx).
+struct Geom {
+  const int* kind;             // [npatch] chart kind
+  const double* cpar;          // [npatch][8]
+  const double* coef;          // [npatch][6][3][nu*nv]; tensors pos,du,dv,duu,duv,dvv; c[n*nv+m]
+  const double* star;          // [25] star-body Y_lm coefficients (or null)
+  const double* pos;           // node frames [npts][3]
+  const double* au;
+  const double* av;
+  const double* sg;            // [npts]
+  const double* wg;            // [npts] Fejer weight * sqrt_g
+  const double* bbox;          // [npatch][6]
+  const double* diam;          // [npatch]
+};
+
+// Near-field table (classification output).
+struct NearTab {
+  const int32_t* idx;          // [npts][npatch] -> record or -1 (FAR)
+  const zc* blk;               // [n_near][C][np*C]
+};
+
+// ---------------------------------------------------------------------------
+// Host-side errors and buffers
+// ---------------------------------------------------------------------------
+struct cbie_error : std::runtime_error {
+  int code;
+  cbie_error(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+
+#define CK(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      throw cbie_error(e_ == cudaErrorMemoryAllocation ? CBIE_EOOM : CBIE_ECUDA,          \
+                       std::string(#call) + ": " + cudaGetErrorString(e_) + " @" +         \
+                           __FILE__ + ":" + std::to_string(__LINE__));                    \
+  } while (0)
+
+#define CKL() CK(cudaGetLastError())
+
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  ~DBuf() { release(); }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  void alloc(size_t count) {
+    if (count == n && p) return;
+    release();
+    if (count == 0) return;
+    CK(cudaMalloc(&p, count * sizeof(T)));
+    n = count;
+  }
+  void upload(const T* h, size_t count, cudaStream_t s) {
+    alloc(count);
+    if (count) CK(cudaMemcpyAsync(p, h, count * sizeof(T), cudaMemcpyHostToDevice, s));
+  }
+  void upload(const std::vector<T>& h, cudaStream_t s) { upload(h.data(), h.size(), s); }
+  std::vector<T> download(cudaStream_t s) const {
+    std::vector<T> h(n);
+    if (n) CK(cudaMemcpyAsync(h.data(), p, n * sizeof(T), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    return h;
+  }
+};
+
+// Elapsed-time helper on one stream (CUDA events).
+struct EvTimer {
+  cudaEvent_t a = nullptr, b = nullptr;
+  EvTimer() {
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+  }
+  ~EvTimer() {
+    cudaEventDestroy(a);
+    cudaEventDestroy(b);
+  }
+  void start(cudaStream_t s) { cudaEventRecord(a, s); }
+  double stop_ms(cudaStream_t s) {
+    cudaEventRecord(b, s);
+    cudaEventSynchronize(b);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, a, b);
+    return ms;
+  }
+};
+
+static inline int ceil_div(int64_t a, int64_t b) { return (int)((a + b - 1) / b); }
