@@ -1,0 +1,80 @@
+// hmatrix.h — host-side H-matrix structure (cluster tree, block tree, leaf
+// storage descriptors) and the device-resident leaf data.
+//
+// Restates hmatrix.py:31-89 (ClusterTree, admissible), 96-204 (block kinds,
+// block tree) with flat arrays so the device kernels can address leaves by index.
+#pragma once
+#include <vector>
+
+#include "context.h"
+
+struct Cluster {
+  int lo = 0, hi = 0;          // point range in permuted order
+  double blo[3], bhi[3];       // bounding box of the cluster's points
+  int kid[2] = {-1, -1};
+  int nkid = 0;
+  int level = 0;
+};
+
+enum { BLK_H = 0, BLK_DENSE = 1, BLK_LR = 2 };
+
+struct BNode {                 // block-tree node (hmatrix.py:146-162)
+  int r = -1, c = -1;          // cluster ids
+  int kind = BLK_H;
+  int nr = 0, nc = 0;          // children grid nr x nc
+  int kid[4] = {-1, -1, -1, -1};
+  int leaf = -1;               // leaf index for DENSE / LR
+};
+
+struct LeafInfo {
+  int node = -1;
+  int r = -1, c = -1;          // clusters
+  int m = 0, n = 0;            // rows / cols in dofs
+  int kind = BLK_DENSE;        // BLK_DENSE or BLK_LR
+  int cap = 0;                 // rank capacity (LR)
+  int64_t off_d = -1;          // dense: column-major m x n at arena + off_d
+  int64_t off_u = -1;          // LR: U m x cap col-major
+  int64_t off_v = -1;          // LR: Vt n x cap col-major (Vt[l*n + j] = V[l][j])
+};
+
+struct Tree {
+  int C = 2;
+  std::vector<Cluster> cl;
+  std::vector<int32_t> pperm;  // new -> old point index
+  std::vector<BNode> nodes;
+  std::vector<LeafInfo> leaves;
+  int root_cl = 0, root_node = 0;
+  void build_clusters(const double* pts, int npts, int C, int n_leaf);
+  void build_blocks(double eta);
+  int dofs(int cl_id) const { return (cl[cl_id].hi - cl[cl_id].lo) * C; }
+};
+
+struct cbie_hmat {
+  cbie_ctx* ctx = nullptr;
+  Tree tree;
+  double eta = 1.0, tol = 1e-4;
+  int64_t N = 0;
+  DBuf<zc> arena;              // all leaf data
+  DBuf<int> rank;              // [nleaf] device ranks (LR)
+  std::vector<int> h_rank;     // host copy after fill
+  DBuf<int32_t> d_pperm;
+  int demoted = 0;
+  int64_t overflow = 0;        // truncations clipped at capacity
+  std::map<std::string, double> stat;
+};
+
+// lowrank.cu: batched truncation  (hmatrix.py:412-426, 605-609)
+// inputs are col-major U (m x k) and Vt (n x k) = V^T; they are used as workspace.
+// in_v < 0 means V = identity (n x n, k = n): truncated SVD of the dense U (m x n).
+struct TruncDesc {
+  int64_t in_u, in_v;          // arena offsets of the inputs
+  int64_t out_u, out_v;        // arena offsets of the outputs (m x cap, n x cap)
+  int m, n;
+  int k;                       // static rank if k_slot < 0
+  int k_slot;                  // >= 0: k = ranks[k_slot] (device-resident)
+  int cap;                     // output capacity (columns)
+  int out_slot;                // ranks[out_slot] <- r
+};
+// kmax >= every min(m,k), min(n,k) (dense mode: min(m,n) and n) in the batch
+void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
+                     unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s);

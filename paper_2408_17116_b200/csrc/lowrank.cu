@@ -1,0 +1,125 @@
+// lowrank.cu — K6: batched low-rank recompression, one CTA per problem.
+//
+// truncate_lowrank (hmatrix.py:412-426): QR(U), QR(V^T), SVD(R_u R_v^T), keep
+// singular values s > tol * s_0 (at least 1), U' = Q_u W_r s_r, V' = Z_r Q_v^T.
+// With in_v < 0 the input is a dense m x n block P and V = I (the full-SVD
+// truncation of add_dense / _overwrite_block, hmatrix.py:605-609, 776-783).
+// Ranks are device-resident: k is read from ranks[k_slot], r is written to
+// ranks[out_slot]; the host never synchronises on them.
+#include "hmatrix.h"
+#include "lowrank.cuh"
+
+namespace {
+
+__global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
+                                                    const TruncDesc* __restrict__ descs,
+                                                    zc* scratch, int64_t scratch_per, int KS,
+                                                    double tol, unsigned long long* overflow) {
+  const TruncDesc d = descs[blockIdx.x];
+  __shared__ double red[LR_NW];
+  __shared__ int flag;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  zc* rd1 = reinterpret_cast<zc*>(smem_raw);
+  zc* rd2 = rd1 + KS;
+  double* kap1 = reinterpret_cast<double*>(rd2 + KS);
+  double* kap2 = kap1 + KS;
+  double* sig = kap2 + KS;
+  int* order = reinterpret_cast<int*>(sig + KS);
+
+  const int m = d.m, n = d.n;
+  const int k = d.k_slot >= 0 ? ranks[d.k_slot] : d.k;
+  const bool ident = d.in_v < 0;
+  if (k <= 0 || m == 0 || n == 0) {
+    if (threadIdx.x == 0) ranks[d.out_slot] = 0;
+    return;
+  }
+  zc* U = arena + d.in_u;
+  zc* Vt = ident ? nullptr : arena + d.in_v;
+  const int kk1 = min(m, k);
+  const int kk2 = ident ? n : min(n, k);
+  zc* M = scratch + (int64_t)blockIdx.x * scratch_per;   // kk1 x kk2, ld kk1
+  zc* W = M + (int64_t)kk1 * kk2;                         // kk2 x kk2
+
+  cta_qr(U, m, k, m, rd1, kap1, red);
+  if (!ident) cta_qr(Vt, n, k, n, rd2, kap2, red);
+  // M = R1 R2^T (R2 = I for the dense mode)
+  for (int e = threadIdx.x; e < kk1 * kk2; e += LR_NT) {
+    const int a = e % kk1, b = e / kk1;
+    zc s = zmk(0.0, 0.0);
+    if (ident) {
+      s = b == a ? rd1[a] : (b > a ? U[(int64_t)b * m + a] : zmk(0.0, 0.0));
+    } else {
+      for (int c = max(a, b); c < k; ++c) {
+        const zc r1 = c == a ? rd1[a] : U[(int64_t)c * m + a];
+        const zc r2 = c == b ? rd2[b] : Vt[(int64_t)c * n + b];
+        s = zadd(s, zmul(r1, r2));
+      }
+    }
+    M[(int64_t)b * kk1 + a] = s;
+  }
+  __syncthreads();
+  cta_jacobi(M, kk1, kk2, kk1, W, kk2, &flag);
+  // singular values and descending order (stable)
+  for (int c = threadIdx.x; c < kk2; c += LR_NT) {
+    double s = 0.0;
+    for (int i = 0; i < kk1; ++i) s += zabs2(M[(int64_t)c * kk1 + i]);
+    sig[c] = sqrt(s);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < kk2; c += LR_NT) {
+    int pos = 0;
+    for (int o = 0; o < kk2; ++o)
+      if (sig[o] > sig[c] || (sig[o] == sig[c] && o < c)) ++pos;
+    order[pos] = c;
+  }
+  __syncthreads();
+  const double s0 = sig[order[0]];
+  int r = 0;
+  if (s0 > 0.0) {
+    for (int c = 0; c < kk2; ++c)
+      if (sig[c] > tol * s0) ++r;
+    r = max(r, 1);
+  }
+  if (r > d.cap) {
+    if (threadIdx.x == 0) atomicAdd(overflow, 1ull);
+    r = d.cap;
+  }
+  // U' = Q1 [ (M W)[:, order[:r]] ; 0 ]
+  zc* Uo = arena + d.out_u;
+  zc* Vo = arena + d.out_v;
+  for (int e = threadIdx.x; e < m * r; e += LR_NT) {
+    const int i = e % m, l = e / m;
+    Uo[(int64_t)l * m + i] = i < kk1 ? M[(int64_t)order[l] * kk1 + i] : zmk(0.0, 0.0);
+  }
+  // Vt' = Q2 [ conj(W[:, order[:r]]) ; 0 ]
+  for (int e = threadIdx.x; e < n * r; e += LR_NT) {
+    const int j = e % n, l = e / n;
+    Vo[(int64_t)l * n + j] = j < kk2 ? zconj(W[(int64_t)order[l] * kk2 + j]) : zmk(0.0, 0.0);
+  }
+  __syncthreads();
+  cta_apply_q(U, m, kk1, m, kap1, Uo, r, m);
+  if (!ident) cta_apply_q(Vt, n, kk2, n, kap2, Vo, r, n);
+  if (threadIdx.x == 0) ranks[d.out_slot] = r;
+}
+
+}  // namespace
+
+void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
+                     unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s) {
+  if (nd == 0) return;
+  kmax = std::max(kmax, 1);
+  const int64_t per = (int64_t)kmax * kmax * 2;
+  // waves keep the Jacobi scratch bounded (<= 1 GiB); the buffer is reused across calls
+  const int wave = (int)std::max<int64_t>(1, ((int64_t)1 << 30) / (per * (int64_t)sizeof(zc)));
+  const size_t need = (size_t)std::min(wave, nd) * per;
+  if (scratch.n < need) scratch.alloc(need);
+  const size_t smem = (size_t)kmax * (2 * sizeof(zc) + 3 * sizeof(double) + sizeof(int));
+  if (smem > 200 * 1024) throw cbie_error(CBIE_EINVALID, "truncation dimension too large");
+  CK(cudaFuncSetAttribute(k_truncate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  for (int b0 = 0; b0 < nd; b0 += wave) {
+    int nb = std::min(wave, nd - b0);
+    k_truncate<<<nb, LR_NT, smem, s>>>(arena, ranks, d_desc + b0, scratch.p, per, kmax, tol,
+                                       overflow);
+    CKL();
+  }
+}

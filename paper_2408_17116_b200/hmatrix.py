@@ -1,0 +1,153 @@
+"""Device-resident H-matrix and H-LU factors (drop-in for chebscat.hmatrix's
+HMatrix / hlu_factor / HLUFactors, hmatrix.py:179-308, 798-858).
+
+The cluster tree, block tree, dense-leaf fill, batched ACA, recompression,
+H-LU and solves all run in libcbie.so; these classes hold the handles.
+"""
+
+from __future__ import annotations
+
+import ctypes as ct
+
+import numpy as np
+
+from . import _ffi
+
+
+class HMatrix:
+    """H-matrix of the equilibrated system D_r A D_c (solver.py:132-145)."""
+
+    def __init__(self, gen, n_leaf: int, eta: float, aca_tol: float):
+        self.gen = gen                     # keeps the device context alive
+        self.dev = gen.dev
+        self.C = gen.C
+        self.N = gen.n_dofs
+        self.eta = eta
+        self.aca_tol = aca_tol
+        h = ct.c_void_p()
+        self.dev.check(self.dev.lib.cbie_hmatrix_build(self.dev.h, int(n_leaf), float(eta),
+                                                       float(aca_tol), ct.byref(h)))
+        self.h = h
+        self._stats = _ffi.stats(h, 1)
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            self.dev.lib.cbie_hmatrix_destroy(h)
+            self.h = None
+
+    # -- structure -------------------------------------------------------------------
+    def tree(self):
+        n = ct.c_int64()
+        self.dev.check(self.dev.lib.cbie_hmatrix_tree(self.h, None, None, ct.byref(n)))
+        perm = np.empty(self.N, np.int64)
+        lv = np.empty((n.value, 6), np.int64)
+        self.dev.check(self.dev.lib.cbie_hmatrix_tree(self.h, _ffi.ptr(perm), _ffi.ptr(lv),
+                                                      ct.byref(n)))
+        return perm, lv
+
+    @property
+    def dof_perm(self):
+        return self.tree()[0]
+
+    def leaf(self, i: int):
+        """('dense', D) or ('lowrank', U, V) in permuted local order."""
+        perm, lv = self.tree()
+        m = int(lv[i, 1] - lv[i, 0]) * self.C
+        n = int(lv[i, 3] - lv[i, 2]) * self.C
+        kind, rank = ct.c_int(), ct.c_int()
+        self.dev.check(self.dev.lib.cbie_hmatrix_leaf(self.h, int(i), ct.byref(kind),
+                                                      ct.byref(rank), None, None))
+        if kind.value == 0:
+            D = np.empty((m, n), complex)
+            self.dev.check(self.dev.lib.cbie_hmatrix_leaf(self.h, int(i), ct.byref(kind),
+                                                          ct.byref(rank), _ffi.ptr(D), None))
+            return ("dense", D)
+        r = rank.value
+        U = np.empty((m, r), complex)
+        V = np.empty((r, n), complex)
+        self.dev.check(self.dev.lib.cbie_hmatrix_leaf(self.h, int(i), ct.byref(kind),
+                                                      ct.byref(rank), _ffi.ptr(U), _ffi.ptr(V)))
+        return ("lowrank", U, V)
+
+    def to_dense(self) -> np.ndarray:
+        """Dense reconstruction in ORIGINAL dof order (tests / diagnostics)."""
+        perm, lv = self.tree()
+        C = self.C
+        A = np.zeros((self.N, self.N), complex)
+        for i, row in enumerate(lv):
+            lf = self.leaf(i)
+            M = lf[1] if lf[0] == "dense" else lf[1] @ lf[2]
+            A[row[0] * C:row[1] * C, row[2] * C:row[3] * C] = M
+        out = np.empty_like(A)
+        out[np.ix_(perm, perm)] = A
+        return out
+
+    # -- application / accounting ----------------------------------------------------------
+    def matvec(self, x: np.ndarray) -> np.ndarray:
+        x = np.asarray(x, complex)
+        one = x.ndim == 1
+        X = np.ascontiguousarray(x.reshape(-1, 1) if one else x)
+        Y = np.empty_like(X)
+        self.dev.check(self.dev.lib.cbie_hmatvec(self.h, _ffi.ptr(X), _ffi.ptr(Y), X.shape[1]))
+        return Y[:, 0] if one else Y
+
+    def stats(self) -> dict:
+        return dict(self._stats)
+
+    @property
+    def demoted(self) -> int:
+        return int(self._stats.get("demoted", 0))
+
+    def stored_scalars(self) -> int:
+        return int(self._stats["stored_scalars"])
+
+    def memory_bytes(self) -> int:
+        return self.stored_scalars() * 16
+
+    def compression_rate(self) -> float:
+        return 1.0 - self.stored_scalars() / float(self.N) ** 2
+
+    def diagnostics(self) -> dict:
+        perm, lv = self.tree()
+        ranks: dict[str, int] = {}
+        for row in lv:
+            if row[4] == 1:
+                ranks[str(int(row[5]))] = ranks.get(str(int(row[5])), 0) + 1
+        return {"rank_histogram": dict(sorted(ranks.items(), key=lambda t: int(t[0]))),
+                "compression_rate": self.compression_rate(),
+                "demoted_blocks": self.demoted,
+                "n_leaves": int(lv.shape[0])}
+
+
+class HLUFactors:
+    """H-LU factors on the device (HLUFactors, hmatrix.py:798-824)."""
+
+    def __init__(self, H: HMatrix, tol: float):
+        self.H = H
+        self.dev = H.dev
+        h = ct.c_void_p()
+        self.dev.check(self.dev.lib.cbie_hlu_factor(H.h, float(tol), ct.byref(h)))
+        self.h = h
+        self._stats = _ffi.stats(h, 2)
+
+    def __del__(self):
+        h = getattr(self, "h", None)
+        if h:
+            self.dev.lib.cbie_hlu_destroy(h)
+            self.h = None
+
+    def solve(self, b: np.ndarray) -> np.ndarray:
+        b = np.asarray(b, complex)
+        one = b.ndim == 1
+        B = np.ascontiguousarray(b.reshape(-1, 1) if one else b)
+        X = np.empty_like(B)
+        self.dev.check(self.dev.lib.cbie_hlu_solve(self.h, _ffi.ptr(B), _ffi.ptr(X), B.shape[1]))
+        return X[:, 0] if one else X
+
+    def stats(self) -> dict:
+        return dict(self._stats)
+
+
+def hlu_factor(H: HMatrix, tol: float) -> HLUFactors:
+    return HLUFactors(H, tol)

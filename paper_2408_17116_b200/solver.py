@@ -1,0 +1,134 @@
+"""End-to-end pipelines (drop-in for chebscat.solver: Problem, build_hmatrix,
+solve_direct, solve_dense; solver.py:30-203).  Same Problem fields and the
+same SolveResult metric keys, plus device timings from CUDA events."""
+
+from __future__ import annotations
+
+import resource
+import time
+from dataclasses import dataclass, field
+from typing import Optional
+
+import numpy as np
+
+from . import assembly as asm
+from . import hmatrix as hm
+from .kernels import FormulationSpec, PlaneWave
+
+
+@dataclass
+class Problem:
+    patches: list
+    spec: FormulationSpec
+    excitation: PlaneWave
+    aca_tol: float = 1e-4
+    trunc_tol: Optional[float] = None
+    gmres_tol: float = 1e-4
+    eta: float = 2.0
+    n_leaf: int = 64
+    tau: float = 1.0
+    grading: int = 3
+    oversample: Optional[int] = None
+    dense_cap: int = asm.DENSE_CAP_DEFAULT
+    workers: int = 1          # no meaning on the GPU path
+    device: int = 0
+
+    def __post_init__(self):
+        for name in ("aca_tol", "gmres_tol"):
+            v = getattr(self, name)
+            if not (0.0 < v < 1.0):
+                raise ValueError(f"{name} must lie in (0, 1), got {v}")
+        if self.trunc_tol is not None and not (0.0 < self.trunc_tol < 1.0):
+            raise ValueError("trunc_tol must lie in (0, 1)")
+
+    @property
+    def effective_trunc_tol(self) -> float:
+        return self.aca_tol if self.trunc_tol is None else self.trunc_tol
+
+    def generator(self) -> asm.GpuGenerator:
+        return asm.GpuGenerator(self.patches, self.spec, tau=self.tau,
+                                oversample=self.oversample, grading=self.grading,
+                                device=self.device)
+
+    @property
+    def n_dofs(self) -> int:
+        return sum(p.n_nodes for p in self.patches) * self.spec.n_components
+
+
+@dataclass
+class SolveResult:
+    solution: np.ndarray
+    residual: float
+    metrics: dict = field(default_factory=dict)
+    iterations: int = 0
+    converged: bool = True
+
+
+def _peak_rss_bytes() -> int:
+    return resource.getrusage(resource.RUSAGE_SELF).ru_maxrss * 1024
+
+
+def build_hmatrix(problem: Problem, gen: Optional[asm.GpuGenerator] = None):
+    """Classification + near field + H-matrix fill of the scaled system."""
+    t0 = time.perf_counter()
+    gen = gen or problem.generator()
+    t1 = time.perf_counter()
+    H = hm.HMatrix(gen, problem.n_leaf, problem.eta, problem.aca_tol)
+    t2 = time.perf_counter()
+    st = H.stats()
+    gs = gen.stats()
+    times = {"setup_s": t1 - t0, "fill_s": t2 - t1, "tree_s": st.get("tree_ms", 0) / 1e3,
+             "device_fill_s": (gs.get("classify_ms", 0) + gs.get("near_fill_ms", 0)
+                               + st.get("fill_ms", 0)) / 1e3}
+    return H, gen, asm.ScaledView(gen), times
+
+
+def solve_direct(problem: Problem) -> SolveResult:
+    """H-matrix fill, H-LU, forward/backward substitution (solver.py:148-175)."""
+    H, gen, scaled, times = build_hmatrix(problem)
+    b = gen.rhs(problem.excitation)
+    b_scaled = b * scaled.row_scale
+    t0 = time.perf_counter()
+    F = hm.hlu_factor(H, problem.effective_trunc_tol)
+    t_factor = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    x = F.solve(b_scaled) * scaled.col_scale
+    t_solve = time.perf_counter() - t0
+    bnorm = np.linalg.norm(b_scaled)
+    residual = float(np.linalg.norm(H.matvec(x / scaled.col_scale) - b_scaled) / bnorm) \
+        if bnorm else 0.0
+    metrics = {
+        **times,
+        "factor_s": t_factor,
+        "solve_s": t_solve,
+        "n_dofs": problem.n_dofs,
+        "hmatrix_bytes": H.memory_bytes(),
+        "compression_rate": H.compression_rate(),
+        "peak_rss_bytes": _peak_rss_bytes(),
+        "memory_method": "ru_maxrss sampling + logical leaf accounting",
+        "hmatrix_diagnostics": H.diagnostics(),
+        "newton_fallbacks": gen.newton_fallbacks,
+        "device": {"generator": gen.stats(), "hmatrix": H.stats(), "hlu": F.stats()},
+    }
+    return SolveResult(x, residual, metrics)
+
+
+def solve_dense(problem: Problem) -> SolveResult:
+    """Dense GPU fill + LU of the unscaled system (solver.py:178-203).  The fill
+    is the product path; the LU here is scipy on the host (reference oracle
+    path, not the north-star hot path)."""
+    import scipy.linalg as sla
+    gen = problem.generator()
+    t0 = time.perf_counter()
+    A = asm.assemble_dense(gen, cap=problem.dense_cap)
+    t_fill = time.perf_counter() - t0
+    b = gen.rhs(problem.excitation)
+    t0 = time.perf_counter()
+    lu = sla.lu_factor(A)
+    t_factor = time.perf_counter() - t0
+    x = sla.lu_solve(lu, b)
+    bnorm = np.linalg.norm(b)
+    residual = float(np.linalg.norm(A @ x - b) / bnorm) if bnorm else 0.0
+    return SolveResult(x, residual, {"fill_s": t_fill, "factor_s": t_factor,
+                                     "n_dofs": problem.n_dofs,
+                                     "newton_fallbacks": gen.newton_fallbacks})
