@@ -394,6 +394,9 @@ static void hmatrix_build(cbie_hmat* H, int n_leaf) {
     TruncDesc d;
     d.in_u = aca[a].off_u;
     d.in_v = aca[a].off_v;
+    d.ldu = L.m;
+    d.ldv = L.n;
+    d.skip_slot = -1;
     d.out_u = L.off_u;
     d.out_v = L.off_v;
     d.m = L.m;

@@ -417,3 +417,16 @@ std::string stats_to_json(const std::map<std::string, double>& m) {
   o << "}";
   return o.str();
 }
+
+std::string hmat_stats(const cbie_hmat* h);
+std::string hlu_stats(const cbie_hlu* f);
+
+extern "C" int cbie_stats_json(const void* h, int which, char* buf, size_t cap) {
+  if (!h || !buf || cap == 0) return CBIE_EINVALID;
+  std::string s = which == 0   ? stats_to_json(((const cbie_ctx*)h)->stat)
+                  : which == 1 ? hmat_stats((const cbie_hmat*)h)
+                               : hlu_stats((const cbie_hlu*)h);
+  if (s.size() + 1 > cap) return CBIE_EINVALID;
+  std::memcpy(buf, s.c_str(), s.size() + 1);
+  return CBIE_OK;
+}

@@ -1,0 +1,1055 @@
+// hlu.cu — H-LU factorisation and solve on the device.
+//
+// The host walks the block tree exactly like the reference recursion
+// (hmatrix.py:433-858: _factor, rsolve_block, lsolve_block, mult_add,
+// add_lowrank, add_dense, _mult_to_lowrank, apply_right/left, to_dense,
+// _overwrite_block, lsolve/usolve/rsolve_upper_dense) but RECORDS every
+// numerical step as a task on a tape instead of executing it.  Ranks stay on
+// the device (the recorded shapes are capacities), so recording never waits
+// on the GPU.  A dependency analysis over buffers assigns every task a level;
+// tasks of one level and kind run as ONE batched kernel launch.  Temporaries
+// come from a size-class pool whose chunks keep their identity, so reuse is
+// ordered by the same dependency analysis.
+#include <algorithm>
+#include <chrono>
+#include <cstring>
+#include <map>
+
+#include "hlu_kernels.cuh"
+#include "hmatrix.h"
+
+std::string stats_to_json(const std::map<std::string, double>& m);
+void hmat_apply(cbie_hmat* H, const zc* d_xp, zc* d_yp, int nrhs, cudaStream_t s);
+
+namespace {
+
+// ---------------------------------------------------------------------------
+// host matrix views
+// ---------------------------------------------------------------------------
+struct Mat {
+  int64_t off = 0;
+  int ld = 0, tr = 0;
+  int rows = 0, cols = 0;      // capacities / static sizes
+  int rslot = -1, cslot = -1;  // dynamic dims
+  int buf = -1;                // dependency buffer id
+  View view() const { return View{off, ld, tr}; }
+  DimR R() const { return DimR{rows, rslot}; }
+  DimR Cc() const { return DimR{cols, cslot}; }
+  Mat sub(int r0, int nr, int c0, int nc) const {
+    Mat s = *this;
+    s.off = tr ? off + (int64_t)r0 * ld + c0 : off + (int64_t)c0 * ld + r0;
+    if (!(r0 == 0 && nr == rows)) s.rslot = -1;
+    if (!(c0 == 0 && nc == cols)) s.cslot = -1;
+    s.rows = nr;
+    s.cols = nc;
+    return s;
+  }
+  Mat T() const {
+    Mat s = *this;
+    s.tr = !tr;
+    std::swap(s.rows, s.cols);
+    std::swap(s.rslot, s.cslot);
+    return s;
+  }
+};
+
+// low-rank factor pair U (m x r), Vt (n x r) with a shared dynamic rank
+struct LR {
+  Mat U, Vt;
+  int cap = 0, slot = -1, buf = -1;
+  Mat V() const { return Vt.T(); }
+};
+
+enum OpKind { OP_GEMM, OP_EW, OP_CONCAT, OP_TRSM, OP_GETRF, OP_TRUNC, OP_NKIND };
+
+struct Task {
+  int kind, idx, level;
+};
+
+struct Recorder {
+  // storage
+  int64_t leaf_end = 0;          // arena offset where temporaries start
+  int64_t pool_top = 0;          // temp high-water mark (relative)
+  int64_t pool_budget = 0;
+  int nbuf = 0;
+  // free lists per size class: (offset, buffer id)
+  std::map<int, std::vector<std::pair<int64_t, int>>> freel;
+  std::vector<int> init_ranks;   // initial values of every rank slot
+  // dependency state per buffer
+  std::vector<int> last_w, max_r;
+  // tapes
+  std::vector<GemmD> gemm;
+  std::vector<EwD> ew;
+  std::vector<ConcatD> cat;
+  std::vector<TrsmD> trsm;
+  std::vector<GetrfD> getrf;
+  std::vector<TruncDesc> trunc;
+  std::vector<int> trunc_kmax;
+  std::vector<Task> tasks;
+  double flops = 0.0;
+  int64_t trunc_count = 0, gemm_count = 0, trsm_count = 0, getrf_count = 0;
+
+  int new_buf() {
+    last_w.push_back(0);
+    max_r.push_back(0);
+    return nbuf++;
+  }
+  int new_slot(int v0) {
+    init_ranks.push_back(v0);
+    return (int)init_ranks.size() - 1;
+  }
+  void add(int kind, int idx, std::initializer_list<int> rd, std::initializer_list<int> wr) {
+    int lvl = 0;
+    for (int b : rd)
+      if (b >= 0) lvl = std::max(lvl, last_w[b]);
+    for (int b : wr)
+      if (b >= 0) lvl = std::max(lvl, std::max(last_w[b], max_r[b]));
+    ++lvl;
+    for (int b : rd)
+      if (b >= 0) max_r[b] = std::max(max_r[b], lvl);
+    for (int b : wr)
+      if (b >= 0) {
+        last_w[b] = lvl;
+        max_r[b] = lvl;
+      }
+    tasks.push_back(Task{kind, idx, lvl});
+  }
+
+  // temporaries ----------------------------------------------------------------
+  struct Tmp {
+    int64_t off;
+    int cls;
+    int buf;
+  };
+  Tmp alloc(int64_t elems) {
+    int cls = 10;
+    while (((int64_t)1 << cls) < elems) ++cls;
+    auto& fl = freel[cls];
+    const int64_t sz = (int64_t)1 << cls;
+    if (!fl.empty() && pool_top + sz > pool_budget) {
+      auto pr = fl.front();   // oldest freed chunk first
+      fl.erase(fl.begin());
+      return Tmp{pr.first, cls, pr.second};
+    }
+    Tmp t{leaf_end + pool_top, cls, new_buf()};
+    pool_top += sz;
+    return t;
+  }
+  void release(const Tmp& t) { freel[t.cls].push_back({t.off, t.buf}); }
+
+  Mat tmp_mat(int rows, int cols, int rslot, int cslot, std::vector<Tmp>& owned) {
+    Tmp t = alloc(std::max<int64_t>((int64_t)rows * cols, 1));
+    owned.push_back(t);
+    Mat m;
+    m.off = t.off;
+    m.ld = std::max(rows, 1);
+    m.rows = rows;
+    m.cols = cols;
+    m.rslot = rslot;
+    m.cslot = cslot;
+    m.buf = t.buf;
+    return m;
+  }
+  LR tmp_lr(int m, int n, int cap, std::vector<Tmp>& owned) {
+    LR r;
+    Tmp t = alloc(std::max<int64_t>((int64_t)(m + n) * cap, 1));
+    owned.push_back(t);
+    r.cap = cap;
+    r.slot = new_slot(0);
+    r.buf = t.buf;
+    r.U.off = t.off;
+    r.U.ld = m;
+    r.U.rows = m;
+    r.U.cols = cap;
+    r.U.cslot = r.slot;
+    r.U.buf = t.buf;
+    r.Vt.off = t.off + (int64_t)m * cap;
+    r.Vt.ld = n;
+    r.Vt.rows = n;
+    r.Vt.cols = cap;
+    r.Vt.cslot = r.slot;
+    r.Vt.buf = t.buf;
+    return r;
+  }
+
+  // primitive ops ------------------------------------------------------------------
+  // C = alpha A B + beta C
+  void op_gemm(const Mat& A, const Mat& B, const Mat& C, zc alpha, zc beta) {
+    if (A.rows == 0 || B.cols == 0 || A.cols == 0) {
+      if (beta.x == 0.0 && beta.y == 0.0) op_ew(nullptr, C, zmk(0, 0), zmk(0, 0));
+      return;
+    }
+    GemmD d{A.view(), B.view(), C.view(), A.R(), B.Cc(), A.Cc(), alpha, beta};
+    gemm.push_back(d);
+    flops += 8.0 * A.rows * A.cols * B.cols;
+    ++gemm_count;
+    if (beta.x != 0.0 || beta.y != 0.0)
+      add(OP_GEMM, (int)gemm.size() - 1, {A.buf, B.buf, C.buf}, {C.buf});
+    else
+      add(OP_GEMM, (int)gemm.size() - 1, {A.buf, B.buf}, {C.buf});
+  }
+  // Y = a X + b Y
+  void op_ew(const Mat* X, const Mat& Y, zc a, zc b) {
+    if (Y.rows == 0 || Y.cols == 0) return;
+    EwD d;
+    d.Y = Y.view();
+    d.X = X ? X->view() : View{0, 1, 0};
+    d.m = Y.R();
+    d.n = Y.Cc();
+    d.a = a;
+    d.b = b;
+    d.hasX = X != nullptr;
+    ew.push_back(d);
+    const bool readsY = b.x != 0.0 || b.y != 0.0;
+    add(OP_EW, (int)ew.size() - 1, {X ? X->buf : -1, readsY ? Y.buf : -1}, {Y.buf});
+  }
+  void op_trsm(const Mat& T, int64_t pivoff, int variant, const Mat& Y) {
+    if (Y.cols == 0) return;
+    TrsmD d{T.off, pivoff, T.rows, variant, Y.view(), Y.Cc()};
+    trsm.push_back(d);
+    flops += 4.0 * T.rows * T.rows * Y.cols;
+    ++trsm_count;
+    add(OP_TRSM, (int)trsm.size() - 1, {T.buf, Y.buf}, {Y.buf});
+  }
+  void op_getrf(const Mat& A, int64_t pivoff, int leaf) {
+    getrf.push_back(GetrfD{A.off, pivoff, A.rows, leaf});
+    flops += 8.0 * A.rows * (double)A.rows * A.rows / 3.0;
+    ++getrf_count;
+    add(OP_GETRF, (int)getrf.size() - 1, {A.buf}, {A.buf});
+  }
+  // dst (rows x cap) <- concat(pieces)
+  void op_concat(int64_t dst, int rows, int out_slot, int dstbuf, const std::vector<Piece>& ps,
+                 const std::vector<int>& srcbufs) {
+    ConcatD d;
+    d.dst = dst;
+    d.rows = rows;
+    d.out_slot = out_slot;
+    d.np = (int)ps.size();
+    for (int i = 0; i < d.np; ++i) d.p[i] = ps[i];
+    cat.push_back(d);
+    int b[4] = {-1, -1, -1, -1};
+    for (size_t i = 0; i < srcbufs.size(); ++i) b[i] = srcbufs[i];
+    add(OP_CONCAT, (int)cat.size() - 1, {b[0], b[1], b[2], b[3]}, {dstbuf});
+  }
+  void op_trunc(const TruncDesc& d, int kmax, int rdbuf, int rdbuf2, int wrbuf) {
+    trunc.push_back(d);
+    trunc_kmax.push_back(kmax);
+    ++trunc_count;
+    add(OP_TRUNC, (int)trunc.size() - 1, {rdbuf, rdbuf2, wrbuf}, {rdbuf, wrbuf});
+  }
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------------------
+// H-LU handle
+// ---------------------------------------------------------------------------
+struct cbie_hlu {
+  cbie_hmat* H = nullptr;
+  double tol = 1e-4;
+  Tree tree;                       // copy (kinds after demotion)
+  std::vector<int64_t> pivoff;     // per leaf (diagonal dense leaves)
+  DBuf<zc> arena;
+  DBuf<int> ranks;
+  DBuf<int> piv;
+  DBuf<double> rcond;
+  int64_t leaf_end = 0;
+  int nslot_leaf = 0;
+  std::map<std::string, double> stat;
+};
+
+namespace {
+
+struct Builder {
+  Recorder& R;
+  cbie_hlu& F;
+  const Tree& T;
+  const int C;
+  Builder(Recorder& r, cbie_hlu& f) : R(r), F(f), T(f.tree), C(f.tree.C) {}
+
+  const BNode& nd(int id) const { return T.nodes[id]; }
+  int rows_of(int id) const { return T.dofs(nd(id).r); }
+  int cols_of(int id) const { return T.dofs(nd(id).c); }
+  int kid(int id, int a, int b) const { return nd(id).kid[a * nd(id).nc + b]; }
+  // dof offset of child cluster relative to parent cluster
+  int roff(int id, int a) const {
+    const BNode& b = nd(id);
+    const Cluster& P = T.cl[b.r];
+    int ck = P.nkid ? P.kid[a] : b.r;
+    return (T.cl[ck].lo - P.lo) * C;
+  }
+  int coff(int id, int a) const {
+    const BNode& b = nd(id);
+    const Cluster& P = T.cl[b.c];
+    int ck = P.nkid ? P.kid[a] : b.c;
+    return (T.cl[ck].lo - P.lo) * C;
+  }
+  int rsz(int id, int a) const {
+    const BNode& b = nd(id);
+    const Cluster& P = T.cl[b.r];
+    int ck = P.nkid ? P.kid[a] : b.r;
+    return T.dofs(ck);
+  }
+  int csz(int id, int a) const {
+    const BNode& b = nd(id);
+    const Cluster& P = T.cl[b.c];
+    int ck = P.nkid ? P.kid[a] : b.c;
+    return T.dofs(ck);
+  }
+  bool is_leaf(int id) const { return nd(id).kind != BLK_H; }
+  int kind(int id) const { return nd(id).kind; }
+  Mat D(int id) const {
+    const LeafInfo& L = T.leaves[nd(id).leaf];
+    Mat m;
+    m.off = L.off_d;
+    m.ld = L.m;
+    m.rows = L.m;
+    m.cols = L.n;
+    m.buf = nd(id).leaf;
+    return m;
+  }
+  LR lr(int id) const {
+    const int li = nd(id).leaf;
+    const LeafInfo& L = T.leaves[li];
+    LR r;
+    r.cap = L.cap;
+    r.slot = li;
+    r.buf = li;
+    r.U.off = L.off_u;
+    r.U.ld = L.m;
+    r.U.rows = L.m;
+    r.U.cols = L.cap;
+    r.U.cslot = li;
+    r.U.buf = li;
+    r.Vt.off = L.off_v;
+    r.Vt.ld = L.n;
+    r.Vt.rows = L.n;
+    r.Vt.cols = L.cap;
+    r.Vt.cslot = li;
+    r.Vt.buf = li;
+    return r;
+  }
+  int64_t piv(int id) const { return F.pivoff[nd(id).leaf]; }
+
+  // ---- products with blocks (hmatrix.py:433-472) --------------------------------
+  // OUT = alpha blk X + (acc ? OUT : 0)
+  void mul_right(int id, const Mat& X, const Mat& OUT, zc alpha, bool acc) {
+    const zc beta = acc ? zmk(1, 0) : zmk(0, 0);
+    if (kind(id) == BLK_DENSE) {
+      R.op_gemm(D(id), X, OUT, alpha, beta);
+    } else if (kind(id) == BLK_LR) {
+      LR l = lr(id);
+      std::vector<Recorder::Tmp> own;
+      Mat W = R.tmp_mat(l.cap, X.cols, l.slot, X.cslot, own);
+      R.op_gemm(l.V(), X, W, zmk(1, 0), zmk(0, 0));
+      R.op_gemm(l.U, W, OUT, alpha, beta);
+      for (auto& t : own) R.release(t);
+    } else {
+      if (!acc) R.op_ew(nullptr, OUT, zmk(0, 0), zmk(0, 0));
+      const BNode& b = nd(id);
+      for (int a = 0; a < b.nr; ++a)
+        for (int c = 0; c < b.nc; ++c)
+          mul_right(kid(id, a, c), X.sub(coff(id, c), csz(id, c), 0, X.cols),
+                    OUT.sub(roff(id, a), rsz(id, a), 0, OUT.cols), alpha, true);
+    }
+  }
+  // OUT = alpha X blk + (acc ? OUT : 0)
+  void mul_left(const Mat& X, int id, const Mat& OUT, zc alpha, bool acc) {
+    const zc beta = acc ? zmk(1, 0) : zmk(0, 0);
+    if (kind(id) == BLK_DENSE) {
+      R.op_gemm(X, D(id), OUT, alpha, beta);
+    } else if (kind(id) == BLK_LR) {
+      LR l = lr(id);
+      std::vector<Recorder::Tmp> own;
+      Mat W = R.tmp_mat(X.rows, l.cap, X.rslot, l.slot, own);
+      R.op_gemm(X, l.U, W, zmk(1, 0), zmk(0, 0));
+      R.op_gemm(W, l.V(), OUT, alpha, beta);
+      for (auto& t : own) R.release(t);
+    } else {
+      if (!acc) R.op_ew(nullptr, OUT, zmk(0, 0), zmk(0, 0));
+      const BNode& b = nd(id);
+      for (int a = 0; a < b.nr; ++a)
+        for (int c = 0; c < b.nc; ++c)
+          mul_left(X.sub(0, X.rows, roff(id, a), rsz(id, a)), kid(id, a, c),
+                   OUT.sub(0, OUT.rows, coff(id, c), csz(id, c)), alpha, true);
+    }
+  }
+  // OUT = dense copy of the block (hmatrix.py:475-499)
+  void densify(int id, const Mat& OUT) {
+    if (kind(id) == BLK_DENSE) {
+      Mat d = D(id);
+      R.op_ew(&d, OUT, zmk(1, 0), zmk(0, 0));
+    } else if (kind(id) == BLK_LR) {
+      LR l = lr(id);
+      R.op_gemm(l.U, l.V(), OUT, zmk(1, 0), zmk(0, 0));
+    } else {
+      const BNode& b = nd(id);
+      for (int a = 0; a < b.nr; ++a)
+        for (int c = 0; c < b.nc; ++c)
+          densify(kid(id, a, c), OUT.sub(roff(id, a), rsz(id, a), coff(id, c), csz(id, c)));
+    }
+  }
+
+  // ---- low-rank targets ----------------------------------------------------------------
+  // target = generic low-rank storage (leaf or temporary)
+  // T += sign U V^T-form (U m x r, Vt n x r) with truncation (hmatrix.py:535-554)
+  void add_lr_to(const LR& Tg, const Mat& U, const Mat& Vt, zc sign) {
+    const int m = Tg.U.rows, n = Tg.Vt.rows;
+    if (U.cols == 0) return;
+    std::vector<Recorder::Tmp> own;
+    const int kc = Tg.cap + U.cols;
+    Recorder::Tmp t = R.alloc((int64_t)(m + n) * kc);
+    own.push_back(t);
+    const int ks = R.new_slot(0);
+    std::vector<Piece> pu{Piece{Tg.U.view(), m, 0, Tg.U.Cc(), zmk(1, 0)},
+                          Piece{U.view(), U.rows, 0, U.Cc(), sign}};
+    std::vector<Piece> pv{Piece{Tg.Vt.view(), n, 0, Tg.Vt.Cc(), zmk(1, 0)},
+                          Piece{Vt.view(), Vt.rows, 0, Vt.Cc(), zmk(1, 0)}};
+    R.op_concat(t.off, m, ks, t.buf, pu, {Tg.buf, U.buf});
+    R.op_concat(t.off + (int64_t)m * kc, n, ks, t.buf, pv, {Tg.buf, Vt.buf});
+    TruncDesc d;
+    d.in_u = t.off;
+    d.in_v = t.off + (int64_t)m * kc;
+    d.ldu = m;
+    d.ldv = n;
+    d.out_u = Tg.U.off;
+    d.out_v = Tg.Vt.off;
+    d.m = m;
+    d.n = n;
+    d.k = kc;
+    d.k_slot = ks;
+    d.cap = Tg.cap;
+    d.out_slot = Tg.slot;
+    d.skip_slot = U.cslot;   // adding rank 0 leaves the target untouched (hmatrix.py:537-538)
+    R.op_trunc(d, std::min(kc, std::max(m, n)), t.buf, U.buf, Tg.buf);
+    R.flops += trunc_flops(m, n, kc);
+    for (auto& x : own) R.release(x);
+  }
+  static double trunc_flops(int m, int n, int k) {
+    auto qr = [](double a, double b) { return 16.0 * a * b * b - 16.0 * b * b * b / 3.0; };
+    double kk = std::min(std::min(m, n), k);
+    return qr(m, std::min(m, k)) + qr(n, std::min(n, k)) + 104.0 * kk * kk * kk + 8.0 * kk * kk * kk;
+  }
+  // dense P (m x n) -> truncated low rank temp (hmatrix.py:605-609)
+  LR dense_to_lr(const Mat& P, std::vector<Recorder::Tmp>& own) {
+    const int m = P.rows, n = P.cols;
+    LR o = R.tmp_lr(m, n, std::min(m, n), own);
+    TruncDesc d;
+    d.in_u = P.off;
+    d.in_v = -1;
+    d.ldu = P.ld;
+    d.ldv = n;
+    d.out_u = o.U.off;
+    d.out_v = o.Vt.off;
+    d.m = m;
+    d.n = n;
+    d.k = n;
+    d.k_slot = -1;
+    d.cap = o.cap;
+    d.out_slot = o.slot;
+    d.skip_slot = -1;
+    R.op_trunc(d, std::max(m, n), P.buf, -1, o.buf);
+    R.flops += 4.0 * (4.0 * std::max(m, n) * (double)std::min(m, n) * std::min(m, n) +
+                      22.0 * std::pow(std::min(m, n), 3));
+    return o;
+  }
+
+  // ---- formatted arithmetic on blocks ---------------------------------------------------
+  void add_lr(int id, const Mat& U, const Mat& Vt, zc sign) {
+    if (U.cols == 0) return;
+    if (kind(id) == BLK_DENSE) {
+      R.op_gemm(U, Vt.T(), D(id), sign, zmk(1, 0));
+    } else if (kind(id) == BLK_LR) {
+      add_lr_to(lr(id), U, Vt, sign);
+    } else {
+      const BNode& b = nd(id);
+      for (int a = 0; a < b.nr; ++a)
+        for (int c = 0; c < b.nc; ++c)
+          add_lr(kid(id, a, c), U.sub(roff(id, a), rsz(id, a), 0, U.cols),
+                 Vt.sub(coff(id, c), csz(id, c), 0, Vt.cols), sign);
+    }
+  }
+  void add_full(int id, const Mat& P) {
+    if (kind(id) == BLK_DENSE) {
+      Mat d = D(id);
+      R.op_ew(&P, d, zmk(1, 0), zmk(1, 0));
+    } else if (kind(id) == BLK_LR) {
+      std::vector<Recorder::Tmp> own;
+      LR o = dense_to_lr(P, own);
+      add_lr_to(lr(id), o.U, o.Vt, zmk(1, 0));
+      for (auto& t : own) R.release(t);
+    } else {
+      const BNode& b = nd(id);
+      for (int a = 0; a < b.nr; ++a)
+        for (int c = 0; c < b.nc; ++c)
+          add_full(kid(id, a, c), P.sub(roff(id, a), rsz(id, a), coff(id, c), csz(id, c)));
+    }
+  }
+  // generic target for mult_add: a node or a temporary low-rank block
+  struct Tgt {
+    int id = -1;     // node id, or -1 for a temp LR
+    LR tl;
+    int rows = 0, cols = 0;
+  };
+  void tgt_add_lr(const Tgt& t, const Mat& U, const Mat& Vt, zc sign) {
+    if (t.id >= 0) add_lr(t.id, U, Vt, sign);
+    else add_lr_to(t.tl, U, Vt, sign);
+  }
+  void tgt_add_full(const Tgt& t, const Mat& P) {
+    if (t.id >= 0) {
+      add_full(t.id, P);
+    } else {
+      std::vector<Recorder::Tmp> own;
+      LR o = dense_to_lr(P, own);
+      add_lr_to(t.tl, o.U, o.Vt, zmk(1, 0));
+      for (auto& x : own) R.release(x);
+    }
+  }
+  // t += sign A B   (hmatrix.py:557-596)
+  void gemm_h(const Tgt& t, int A, int B, zc sign) {
+    std::vector<Recorder::Tmp> own;
+    const int m = rows_of(A), n = cols_of(B);
+    if (kind(A) == BLK_LR) {
+      LR a = lr(A);
+      Mat Wt = R.tmp_mat(n, a.cap, -1, a.slot, own);      // (A.V B)^T
+      mul_left(a.V(), B, Wt.T(), zmk(1, 0), false);
+      tgt_add_lr(t, a.U, Wt, sign);
+    } else if (kind(B) == BLK_LR) {
+      LR b = lr(B);
+      Mat W = R.tmp_mat(m, b.cap, -1, b.slot, own);
+      mul_right(A, b.U, W, zmk(1, 0), false);
+      tgt_add_lr(t, W, b.Vt, sign);
+    } else if (kind(A) == BLK_DENSE && kind(B) == BLK_DENSE) {
+      Mat P = R.tmp_mat(m, n, -1, -1, own);
+      R.op_gemm(D(A), D(B), P, sign, zmk(0, 0));
+      tgt_add_full(t, P);
+    } else if (kind(A) == BLK_DENSE) {
+      Mat P = R.tmp_mat(m, n, -1, -1, own);
+      mul_left(D(A), B, P, sign, false);
+      tgt_add_full(t, P);
+    } else if (kind(B) == BLK_DENSE) {
+      Mat P = R.tmp_mat(m, n, -1, -1, own);
+      mul_right(A, D(B), P, sign, false);
+      tgt_add_full(t, P);
+    } else if (t.id >= 0 && kind(t.id) == BLK_H) {
+      const BNode& tb = nd(t.id);
+      for (int a = 0; a < tb.nr; ++a)
+        for (int b = 0; b < tb.nc; ++b)
+          for (int k = 0; k < nd(A).nc; ++k) {
+            Tgt s;
+            s.id = kid(t.id, a, b);
+            gemm_h(s, kid(A, a, k), kid(B, k, b), sign);
+          }
+    } else {
+      LR p = prod_lowrank(A, B, own);
+      tgt_add_lr(t, p.U, p.Vt, sign);
+    }
+    for (auto& x : own) R.release(x);
+  }
+  void gemm_node(int tid, int A, int B, zc sign) {
+    Tgt t;
+    t.id = tid;
+    gemm_h(t, A, B, sign);
+  }
+  // agglomerated low-rank form of A B, both subdivided (hmatrix.py:620-642)
+  LR prod_lowrank(int A, int B, std::vector<Recorder::Tmp>& own) {
+    const int m = rows_of(A), n = cols_of(B);
+    const BNode &a_ = nd(A), &b_ = nd(B);
+    std::vector<LR> parts;
+    std::vector<int> pr, pc;
+    std::vector<Recorder::Tmp> own2;
+    for (int a = 0; a < a_.nr; ++a)
+      for (int b = 0; b < b_.nc; ++b) {
+        const int ma = rsz(A, a), nb = csz(B, b);
+        Tgt t;
+        t.id = -1;
+        t.tl = R.tmp_lr(ma, nb, std::min(ma, nb), own2);
+        for (int k = 0; k < a_.nc; ++k) gemm_h(t, kid(A, a, k), kid(B, k, b), zmk(1, 0));
+        parts.push_back(t.tl);
+        pr.push_back(roff(A, a));
+        pc.push_back(coff(B, b));
+      }
+    int kc = 0;
+    for (auto& p : parts) kc += p.cap;
+    Recorder::Tmp t = R.alloc((int64_t)(m + n) * kc);
+    own2.push_back(t);
+    const int ks = R.new_slot(0);
+    std::vector<Piece> pu, pv;
+    std::vector<int> bu;
+    for (size_t i = 0; i < parts.size(); ++i) {
+      pu.push_back(Piece{parts[i].U.view(), parts[i].U.rows, pr[i], parts[i].U.Cc(), zmk(1, 0)});
+      pv.push_back(Piece{parts[i].Vt.view(), parts[i].Vt.rows, pc[i], parts[i].Vt.Cc(), zmk(1, 0)});
+      bu.push_back(parts[i].buf);
+    }
+    if (parts.size() > 4) throw cbie_error(CBIE_EINVALID, "more than 4 product parts");
+    R.op_concat(t.off, m, ks, t.buf, pu, bu);
+    R.op_concat(t.off + (int64_t)m * kc, n, ks, t.buf, pv, bu);
+    LR o = R.tmp_lr(m, n, std::min(m, n), own);
+    TruncDesc d;
+    d.in_u = t.off;
+    d.in_v = t.off + (int64_t)m * kc;
+    d.ldu = m;
+    d.ldv = n;
+    d.out_u = o.U.off;
+    d.out_v = o.Vt.off;
+    d.m = m;
+    d.n = n;
+    d.k = kc;
+    d.k_slot = ks;
+    d.cap = o.cap;
+    d.out_slot = o.slot;
+    d.skip_slot = -1;
+    R.op_trunc(d, std::min(kc, std::max(m, n)), t.buf, -1, o.buf);
+    R.flops += trunc_flops(m, n, kc);
+    for (auto& x : own2) R.release(x);
+    return o;
+  }
+
+  // ---- triangular solves with factored H blocks (hmatrix.py:649-767) ----------------------
+  void lsolve(int L, const Mat& X) {
+    if (kind(L) == BLK_DENSE) {
+      R.op_trsm(D(L), piv(L), 0, X);
+      return;
+    }
+    const BNode& b = nd(L);
+    for (int k = 0; k < b.nr; ++k) {
+      Mat Xk = X.sub(roff(L, k), rsz(L, k), 0, X.cols);
+      lsolve(kid(L, k, k), Xk);
+      for (int i = k + 1; i < b.nr; ++i)
+        mul_right(kid(L, i, k), Xk, X.sub(roff(L, i), rsz(L, i), 0, X.cols), zmk(-1, 0), true);
+    }
+  }
+  void usolve(int U, const Mat& X) {
+    if (kind(U) == BLK_DENSE) {
+      R.op_trsm(D(U), -1, 1, X);
+      return;
+    }
+    const BNode& b = nd(U);
+    for (int k = b.nr - 1; k >= 0; --k) {
+      Mat Xk = X.sub(roff(U, k), rsz(U, k), 0, X.cols);
+      for (int i = k + 1; i < b.nr; ++i)
+        mul_right(kid(U, k, i), X.sub(roff(U, i), rsz(U, i), 0, X.cols), Xk, zmk(-1, 0), true);
+      usolve(kid(U, k, k), Xk);
+    }
+  }
+  void rsolve(const Mat& X, int U) {   // X := X U^{-1}
+    if (kind(U) == BLK_DENSE) {
+      R.op_trsm(D(U), -1, 2, X.T());
+      return;
+    }
+    const BNode& b = nd(U);
+    for (int k = 0; k < b.nc; ++k) {
+      Mat Xk = X.sub(0, X.rows, coff(U, k), csz(U, k));
+      for (int l = 0; l < k; ++l)
+        mul_left(X.sub(0, X.rows, coff(U, l), csz(U, l)), kid(U, l, k), Xk, zmk(-1, 0), true);
+      rsolve(Xk, kid(U, k, k));
+    }
+  }
+  void overwrite(int id, const Mat& X) {   // (hmatrix.py:770-791)
+    if (kind(id) == BLK_DENSE) {
+      Mat d = D(id);
+      R.op_ew(&X, d, zmk(1, 0), zmk(0, 0));
+    } else if (kind(id) == BLK_LR) {
+      LR l = lr(id);
+      TruncDesc dd;
+      dd.in_u = X.off;
+      dd.in_v = -1;
+      dd.ldu = X.ld;
+      dd.ldv = X.cols;
+      dd.out_u = l.U.off;
+      dd.out_v = l.Vt.off;
+      dd.m = X.rows;
+      dd.n = X.cols;
+      dd.k = X.cols;
+      dd.k_slot = -1;
+      dd.cap = l.cap;
+      dd.out_slot = l.slot;
+      dd.skip_slot = -1;
+      R.op_trunc(dd, std::max(X.rows, X.cols), X.buf, -1, l.buf);
+    } else {
+      const BNode& b = nd(id);
+      for (int a = 0; a < b.nr; ++a)
+        for (int c = 0; c < b.nc; ++c)
+          overwrite(kid(id, a, c), X.sub(roff(id, a), rsz(id, a), coff(id, c), csz(id, c)));
+    }
+  }
+  void lsolve_blk(int L, int B) {   // (hmatrix.py:713-740)
+    if (kind(B) == BLK_LR) {
+      lsolve(L, lr(B).U);
+    } else if (kind(B) == BLK_DENSE) {
+      lsolve(L, D(B));
+    } else if (kind(L) == BLK_DENSE) {
+      for (int c = 0; c < nd(B).nc; ++c) lsolve_blk(L, kid(B, 0, c));
+    } else if (nd(B).nr == 1) {
+      std::vector<Recorder::Tmp> own;
+      Mat X = R.tmp_mat(rows_of(B), cols_of(B), -1, -1, own);
+      densify(B, X);
+      lsolve(L, X);
+      overwrite(B, X);
+      for (auto& t : own) R.release(t);
+    } else {
+      const int s = nd(L).nr;
+      for (int k = 0; k < s; ++k) {
+        for (int c = 0; c < nd(B).nc; ++c) lsolve_blk(kid(L, k, k), kid(B, k, c));
+        for (int i = k + 1; i < s; ++i)
+          for (int c = 0; c < nd(B).nc; ++c) gemm_node(kid(B, i, c), kid(L, i, k), kid(B, k, c), zmk(-1, 0));
+      }
+    }
+  }
+  void rsolve_blk(int B, int U) {   // (hmatrix.py:743-767)
+    if (kind(B) == BLK_LR) {
+      rsolve(lr(B).V(), U);
+    } else if (kind(B) == BLK_DENSE) {
+      rsolve(D(B), U);
+    } else if (kind(U) == BLK_DENSE) {
+      for (int a = 0; a < nd(B).nr; ++a) rsolve_blk(kid(B, a, 0), U);
+    } else if (nd(B).nc == 1) {
+      std::vector<Recorder::Tmp> own;
+      Mat X = R.tmp_mat(rows_of(B), cols_of(B), -1, -1, own);
+      densify(B, X);
+      rsolve(X, U);
+      overwrite(B, X);
+      for (auto& t : own) R.release(t);
+    } else {
+      const int s = nd(U).nc;
+      for (int k = 0; k < s; ++k) {
+        for (int l = 0; l < k; ++l)
+          for (int a = 0; a < nd(B).nr; ++a) gemm_node(kid(B, a, k), kid(B, a, l), kid(U, l, k), zmk(-1, 0));
+        for (int a = 0; a < nd(B).nr; ++a) rsolve_blk(kid(B, a, k), kid(U, k, k));
+      }
+    }
+  }
+  void factor(int id) {   // (hmatrix.py:834-858)
+    if (kind(id) == BLK_DENSE) {
+      R.op_getrf(D(id), piv(id), nd(id).leaf);
+      return;
+    }
+    if (kind(id) != BLK_H) throw cbie_error(CBIE_EINVALID, "diagonal block must be dense or subdivided");
+    const int s = nd(id).nr;
+    for (int k = 0; k < s; ++k) {
+      factor(kid(id, k, k));
+      for (int i = k + 1; i < s; ++i) rsolve_blk(kid(id, i, k), kid(id, k, k));
+      for (int j = k + 1; j < s; ++j) lsolve_blk(kid(id, k, k), kid(id, k, j));
+      for (int i = k + 1; i < s; ++i)
+        for (int j = k + 1; j < s; ++j) gemm_node(kid(id, i, j), kid(id, i, k), kid(id, k, j), zmk(-1, 0));
+    }
+  }
+};
+
+// ---------------------------------------------------------------------------
+// executor: group by (level, kind) -> batched launches
+// ---------------------------------------------------------------------------
+struct Exec {
+  int levels = 0, launches = 0;
+};
+
+Exec execute(Recorder& R, zc* arena, int* ranks, int* piv, double* rcond, int* flag,
+             unsigned long long* ovf, DBuf<zc>& trunc_scratch, double tol, cudaStream_t s) {
+  Exec ex;
+  std::vector<Task> ts = R.tasks;
+  std::stable_sort(ts.begin(), ts.end(), [](const Task& a, const Task& b) {
+    return a.level != b.level ? a.level < b.level : a.kind < b.kind;
+  });
+  // reorder descriptor arrays into launch order and upload once
+  std::vector<GemmD> g;
+  std::vector<EwD> e;
+  std::vector<ConcatD> c;
+  std::vector<TrsmD> t;
+  std::vector<GetrfD> f;
+  std::vector<TruncDesc> tr;
+  struct Grp {
+    int kind, start, count, level, kmax;
+  };
+  std::vector<Grp> groups;
+  for (size_t i = 0; i < ts.size();) {
+    size_t j = i;
+    const int kind = ts[i].kind, lvl = ts[i].level;
+    Grp gr{kind, 0, 0, lvl, 1};
+    switch (kind) {
+      case OP_GEMM: gr.start = (int)g.size(); break;
+      case OP_EW: gr.start = (int)e.size(); break;
+      case OP_CONCAT: gr.start = (int)c.size(); break;
+      case OP_TRSM: gr.start = (int)t.size(); break;
+      case OP_GETRF: gr.start = (int)f.size(); break;
+      default: gr.start = (int)tr.size(); break;
+    }
+    for (; j < ts.size() && ts[j].kind == kind && ts[j].level == lvl; ++j) {
+      const int id = ts[j].idx;
+      switch (kind) {
+        case OP_GEMM: g.push_back(R.gemm[id]); break;
+        case OP_EW: e.push_back(R.ew[id]); break;
+        case OP_CONCAT: c.push_back(R.cat[id]); break;
+        case OP_TRSM: t.push_back(R.trsm[id]); break;
+        case OP_GETRF: f.push_back(R.getrf[id]); break;
+        default:
+          tr.push_back(R.trunc[id]);
+          gr.kmax = std::max(gr.kmax, R.trunc_kmax[id]);
+          break;
+      }
+    }
+    gr.count = (int)(j - i);
+    groups.push_back(gr);
+    i = j;
+  }
+  DBuf<GemmD> dg;
+  DBuf<EwD> de;
+  DBuf<ConcatD> dc;
+  DBuf<TrsmD> dt;
+  DBuf<GetrfD> df;
+  DBuf<TruncDesc> dtr;
+  dg.upload(g, s);
+  de.upload(e, s);
+  dc.upload(c, s);
+  dt.upload(t, s);
+  df.upload(f, s);
+  dtr.upload(tr, s);
+  // launch geometry helpers
+  int gemm_tiles = 1;
+  for (auto& x : g) gemm_tiles = std::max(gemm_tiles, std::max(x.m.v, x.n.v));
+  int maxn_trsm = 1;
+  for (auto& x : t) maxn_trsm = std::max(maxn_trsm, x.n);
+  int maxn_getrf = 1;
+  for (auto& x : f) maxn_getrf = std::max(maxn_getrf, x.n);
+  const size_t trsm_smem = (size_t)maxn_trsm * TS_COLS * sizeof(zc);
+  CK(cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem));
+  const size_t getrf_smem = (size_t)maxn_getrf * sizeof(zc);
+  int lvl = -1;
+  for (auto& gr : groups) {
+    if (gr.level != lvl) {
+      ++ex.levels;
+      lvl = gr.level;
+    }
+    ++ex.launches;
+    switch (gr.kind) {
+      case OP_GEMM: {
+        int mt = 1, nt = 1;
+        for (int i = 0; i < gr.count; ++i) {
+          mt = std::max(mt, ceil_div(g[gr.start + i].m.v, GT));
+          nt = std::max(nt, ceil_div(g[gr.start + i].n.v, GT));
+        }
+        for (int b0 = 0; b0 < gr.count; b0 += 65535) {
+          int nb = std::min(65535, gr.count - b0);
+          k_gemm<<<dim3(mt, nt, nb), 256, 0, s>>>(arena, ranks, dg.p + gr.start + b0);
+        }
+        break;
+      }
+      case OP_EW: {
+        for (int b0 = 0; b0 < gr.count; b0 += 65535) {
+          int nb = std::min(65535, gr.count - b0);
+          k_ew<<<dim3(16, nb), 256, 0, s>>>(arena, ranks, de.p + gr.start + b0);
+        }
+        break;
+      }
+      case OP_CONCAT: {
+        for (int b0 = 0; b0 < gr.count; b0 += 65535) {
+          int nb = std::min(65535, gr.count - b0);
+          k_concat<<<dim3(8, nb), 256, 0, s>>>(arena, ranks, dc.p + gr.start + b0);
+        }
+        break;
+      }
+      case OP_TRSM: {
+        int cmax = 1;
+        for (int i = 0; i < gr.count; ++i) cmax = std::max(cmax, ceil_div(t[gr.start + i].p.v, TS_COLS));
+        for (int b0 = 0; b0 < gr.count; b0 += 65535) {
+          int nb = std::min(65535, gr.count - b0);
+          k_trsm<<<dim3(cmax, nb), 256, trsm_smem, s>>>(arena, ranks, piv, dt.p + gr.start + b0);
+        }
+        break;
+      }
+      case OP_GETRF:
+        k_getrf<<<gr.count, 256, getrf_smem, s>>>(arena, piv, df.p + gr.start, rcond, flag);
+        break;
+      default:
+        launch_truncate(arena, ranks, dtr.p + gr.start, gr.count, gr.kmax, tol, ovf, trunc_scratch, s);
+        break;
+    }
+    CKL();
+  }
+  (void)gemm_tiles;
+  CK(cudaStreamSynchronize(s));
+  return ex;
+}
+
+}  // namespace
+
+
+// ---------------------------------------------------------------------------
+// factor / solve drivers
+// ---------------------------------------------------------------------------
+static void hlu_factor_impl(cbie_hlu* F) {
+  cbie_hmat* H = F->H;
+  cbie_ctx* c = H->ctx;
+  cudaStream_t s = c->stream;
+  F->tree = H->tree;
+  Tree& T = F->tree;
+  const int nleaf = (int)T.leaves.size();
+  // leaf storage region of H (everything below the first ACA scratch offset)
+  int64_t leaf_end = 0;
+  for (auto& L : T.leaves) {
+    if (L.kind == BLK_DENSE) leaf_end = std::max(leaf_end, L.off_d + (int64_t)L.m * L.n);
+    else leaf_end = std::max(leaf_end, L.off_v + (int64_t)L.n * L.cap);
+  }
+  // pivots for dense diagonal leaves
+  F->pivoff.assign(nleaf, -1);
+  int64_t npiv = 0;
+  for (int li = 0; li < nleaf; ++li)
+    if (T.leaves[li].kind == BLK_DENSE && T.leaves[li].r == T.leaves[li].c) {
+      F->pivoff[li] = npiv;
+      npiv += T.leaves[li].m;
+    }
+  auto t0 = std::chrono::steady_clock::now();
+  Recorder R;
+  R.leaf_end = leaf_end;
+  R.pool_budget = (int64_t)8 << 30 >> 4;   // 8 GiB of temporaries before chunk reuse
+  for (int li = 0; li < nleaf; ++li) {
+    R.new_buf();
+    R.new_slot(0);
+  }
+  Builder B(R, *F);
+  B.factor(T.root_node);
+  auto t1 = std::chrono::steady_clock::now();
+  F->stat["record_ms"] = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  // device state: arena = copy of the leaf storage + temporaries
+  F->arena.alloc((size_t)(leaf_end + R.pool_top + 1));
+  CK(cudaMemcpyAsync(F->arena.p, H->arena.p, sizeof(zc) * leaf_end, cudaMemcpyDeviceToDevice, s));
+  std::vector<int> r0 = R.init_ranks;
+  for (int li = 0; li < nleaf; ++li) r0[li] = H->h_rank[li];
+  F->ranks.upload(r0, s);
+  F->piv.alloc(std::max<int64_t>(npiv, 1));
+  F->rcond.alloc(nleaf);
+  CK(cudaMemsetAsync(F->rcond.p, 0, sizeof(double) * nleaf, s));
+  DBuf<int> flag;
+  flag.alloc(1);
+  CK(cudaMemsetAsync(flag.p, 0, sizeof(int), s));
+  DBuf<unsigned long long> ovf;
+  ovf.alloc(1);
+  CK(cudaMemsetAsync(ovf.p, 0, 8, s));
+  DBuf<zc> scratch;
+  EvTimer tm;
+  tm.start(s);
+  Exec ex = execute(R, F->arena.p, F->ranks.p, F->piv.p, F->rcond.p, flag.p, ovf.p, scratch, F->tol, s);
+  F->stat["factor_device_ms"] = tm.stop_ms(s);
+  int hflag = 0;
+  unsigned long long hovf = 0;
+  CK(cudaMemcpy(&hflag, flag.p, sizeof(int), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(&hovf, ovf.p, 8, cudaMemcpyDeviceToHost));
+  F->leaf_end = leaf_end;
+  F->stat["levels"] = ex.levels;
+  F->stat["launches"] = ex.launches;
+  F->stat["tasks"] = (double)R.tasks.size();
+  F->stat["flops"] = R.flops;
+  F->stat["n_truncations"] = (double)R.trunc_count;
+  F->stat["n_gemm"] = (double)R.gemm_count;
+  F->stat["n_trsm"] = (double)R.trsm_count;
+  F->stat["n_getrf"] = (double)R.getrf_count;
+  F->stat["temp_bytes"] = (double)R.pool_top * sizeof(zc);
+  F->stat["trunc_overflow"] = (double)hovf;
+  if (hflag) {
+    std::vector<double> rc(nleaf);
+    CK(cudaMemcpy(rc.data(), F->rcond.p, sizeof(double) * nleaf, cudaMemcpyDeviceToHost));
+    double mn = 1e300;
+    for (int li = 0; li < nleaf; ++li)
+      if (F->pivoff[li] >= 0) mn = std::min(mn, rc[li]);
+    throw cbie_error(CBIE_ESINGULAR_DIAGONAL, "diagonal block rcond " + std::to_string(mn));
+  }
+}
+
+static void hlu_solve_impl(cbie_hlu* F, const zc* b, zc* x, int nrhs) {
+  cbie_hmat* H = F->H;
+  cudaStream_t s = H->ctx->stream;
+  const Tree& T = F->tree;
+  const int64_t N = H->N;
+  const int C = T.C;
+  // permuted right-hand sides, column-major N x nrhs
+  std::vector<zc> bp((size_t)N * nrhs);
+  for (size_t p = 0; p < T.pperm.size(); ++p)
+    for (int c = 0; c < C; ++c) {
+      const int64_t ni = (int64_t)p * C + c, oi = (int64_t)T.pperm[p] * C + c;
+      for (int r = 0; r < nrhs; ++r) bp[(size_t)r * N + ni] = b[(size_t)oi * nrhs + r];
+    }
+  Recorder R;
+  R.leaf_end = F->leaf_end;
+  R.pool_budget = (int64_t)1 << 40;
+  const int nleaf = (int)T.leaves.size();
+  for (int li = 0; li < nleaf; ++li) {
+    R.new_buf();
+    R.new_slot(0);
+  }
+  // the rank slots of the factors live in F->ranks (same leaf slot numbering)
+  std::vector<Recorder::Tmp> own;
+  Mat X = R.tmp_mat((int)N, nrhs, -1, -1, own);
+  Builder Bd(R, *F);
+  Bd.lsolve(T.root_node, X);
+  Bd.usolve(T.root_node, X);
+  // arena for the solve: factors (shared) + temps: allocate temps after the factor arena
+  const int64_t need = F->leaf_end + R.pool_top + 1;
+  if ((int64_t)F->arena.n < need) {
+    DBuf<zc> bigger;
+    bigger.alloc(need);
+    CK(cudaMemcpyAsync(bigger.p, F->arena.p, sizeof(zc) * F->leaf_end, cudaMemcpyDeviceToDevice, s));
+    std::swap(bigger.p, F->arena.p);
+    std::swap(bigger.n, F->arena.n);
+  }
+  CK(cudaMemcpyAsync(F->arena.p + X.off, bp.data(), sizeof(zc) * bp.size(), cudaMemcpyHostToDevice, s));
+  // slots: leaves keep their factor ranks; extra slots (none expected) appended
+  DBuf<int> ranks;
+  std::vector<int> r0 = R.init_ranks;
+  {
+    std::vector<int> fr(nleaf);
+    CK(cudaMemcpy(fr.data(), F->ranks.p, sizeof(int) * nleaf, cudaMemcpyDeviceToHost));
+    for (int li = 0; li < nleaf; ++li) r0[li] = fr[li];
+  }
+  ranks.upload(r0, s);
+  DBuf<int> flag;
+  flag.alloc(1);
+  DBuf<double> rc;
+  rc.alloc(1);
+  DBuf<unsigned long long> ovf;
+  ovf.alloc(1);
+  DBuf<zc> scratch;
+  execute(R, F->arena.p, ranks.p, F->piv.p, rc.p, flag.p, ovf.p, scratch, F->tol, s);
+  CK(cudaMemcpy(bp.data(), F->arena.p + X.off, sizeof(zc) * bp.size(), cudaMemcpyDeviceToHost));
+  for (size_t p = 0; p < T.pperm.size(); ++p)
+    for (int c = 0; c < C; ++c) {
+      const int64_t ni = (int64_t)p * C + c, oi = (int64_t)T.pperm[p] * C + c;
+      for (int r = 0; r < nrhs; ++r) x[(size_t)oi * nrhs + r] = bp[(size_t)r * N + ni];
+    }
+}
+
+extern "C" {
+
+int cbie_hlu_factor(cbie_hmat* h, double trunc_tol, cbie_hlu** out) {
+  cbie_hlu* F = nullptr;
+  try {
+    cudaSetDevice(h->ctx->device);
+    if (!(trunc_tol > 0.0 && trunc_tol < 1.0)) throw cbie_error(CBIE_EINVALID, "trunc_tol in (0,1)");
+    F = new cbie_hlu();
+    F->H = h;
+    F->tol = trunc_tol;
+    hlu_factor_impl(F);
+    *out = F;
+  } catch (const cbie_error& e) {
+    h->ctx->err = e.what();
+    delete F;
+    *out = nullptr;
+    return e.code;
+  }
+  return CBIE_OK;
+}
+
+void cbie_hlu_destroy(cbie_hlu* f) { delete f; }
+
+int cbie_hlu_solve(cbie_hlu* f, const cbie_c128* b, cbie_c128* x, int nrhs) {
+  try {
+    cudaSetDevice(f->H->ctx->device);
+    hlu_solve_impl(f, reinterpret_cast<const zc*>(b), reinterpret_cast<zc*>(x), nrhs);
+  } catch (const cbie_error& e) {
+    f->H->ctx->err = e.what();
+    return e.code;
+  }
+  return CBIE_OK;
+}
+
+}  // extern "C"
+
+std::string hlu_stats(const cbie_hlu* f) { return stats_to_json(f->stat); }

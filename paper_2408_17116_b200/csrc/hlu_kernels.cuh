@@ -1,0 +1,436 @@
+// hlu_kernels.cuh — batched device kernels of the H-LU executor.
+//
+// Every kernel takes an array of descriptors (one per independent task of a
+// schedule level) and reads dynamic dimensions (low-rank ranks) from the
+// device-resident rank array, so the host never synchronises on ranks.
+// Matrices are "views" into one complex128 arena: element (i, j) of a view is
+// arena[off + (tr ? i*ld + j : j*ld + i)].
+#pragma once
+#include "lowrank.cuh"
+
+struct View {
+  int64_t off;
+  int ld;
+  int tr;
+};
+struct DimR {     // actual = slot >= 0 ? ranks[slot] : v
+  int v;
+  int slot;
+};
+__device__ __forceinline__ int dimv(DimR d, const int* ranks) { return d.slot >= 0 ? ranks[d.slot] : d.v; }
+__device__ __forceinline__ int64_t vidx(const View& v, int i, int j) {
+  return v.off + (v.tr ? (int64_t)i * v.ld + j : (int64_t)j * v.ld + i);
+}
+
+// ---------------------------------------------------------------------------
+// GEMM: C = alpha A B + beta C      (A m x k, B k x n, C m x n; any views)
+// ---------------------------------------------------------------------------
+struct GemmD {
+  View A, B, C;
+  DimR m, n, k;
+  zc alpha, beta;
+};
+
+constexpr int GT = 32;   // output tile
+constexpr int GK = 16;   // k chunk
+
+__global__ void __launch_bounds__(256) k_gemm(zc* __restrict__ ar, const int* __restrict__ ranks,
+                                              const GemmD* __restrict__ ds) {
+  const GemmD d = ds[blockIdx.z];
+  const int m = dimv(d.m, ranks), n = dimv(d.n, ranks), k = dimv(d.k, ranks);
+  const int i0 = blockIdx.x * GT, j0 = blockIdx.y * GT;
+  if (i0 >= m || j0 >= n) return;
+  __shared__ zc sA[GK][GT + 1];
+  __shared__ zc sB[GK][GT + 1];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;   // 16 x 16 threads, 2x2 outputs each
+  zc acc[2][2] = {{zmk(0, 0), zmk(0, 0)}, {zmk(0, 0), zmk(0, 0)}};
+  for (int k0 = 0; k0 < k; k0 += GK) {
+    for (int e = threadIdx.x; e < GK * GT; e += 256) {
+      const int kk = e / GT, ii = e % GT;
+      const int gi = i0 + ii, gk = k0 + kk;
+      sA[kk][ii] = (gi < m && gk < k) ? ar[vidx(d.A, gi, gk)] : zmk(0, 0);
+      const int gj = j0 + ii;
+      sB[kk][ii] = (gj < n && gk < k) ? ar[vidx(d.B, gk, gj)] : zmk(0, 0);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < GK; ++kk) {
+      const zc a0 = sA[kk][ty], a1 = sA[kk][ty + 16];
+      const zc b0 = sB[kk][tx], b1 = sB[kk][tx + 16];
+      zfma(acc[0][0], a0, b0);
+      zfma(acc[0][1], a0, b1);
+      zfma(acc[1][0], a1, b0);
+      zfma(acc[1][1], a1, b1);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const int gi = i0 + ty + 16 * a, gj = j0 + tx + 16 * b;
+      if (gi < m && gj < n) {
+        const int64_t o = vidx(d.C, gi, gj);
+        zc v = zmul(d.alpha, acc[a][b]);
+        if (d.beta.x != 0.0 || d.beta.y != 0.0) v = zadd(v, zmul(d.beta, ar[o]));
+        ar[o] = v;
+      }
+    }
+}
+
+// ---------------------------------------------------------------------------
+// EW: Y = a X + b Y  (X optional)
+// ---------------------------------------------------------------------------
+struct EwD {
+  View X, Y;
+  DimR m, n;
+  zc a, b;
+  int hasX;
+};
+__global__ void k_ew(zc* __restrict__ ar, const int* __restrict__ ranks, const EwD* __restrict__ ds) {
+  const EwD d = ds[blockIdx.y];
+  const int m = dimv(d.m, ranks), n = dimv(d.n, ranks);
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)m * n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e % m), j = (int)(e / m);
+    const int64_t oy = vidx(d.Y, i, j);
+    zc v = (d.b.x != 0.0 || d.b.y != 0.0) ? zmul(d.b, ar[oy]) : zmk(0, 0);
+    if (d.hasX) v = zadd(v, zmul(d.a, ar[vidx(d.X, i, j)]));
+    ar[oy] = v;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// CONCAT: dst (rows x cap, col-major, ld rows) <- [piece_0 | piece_1 | ...]
+// each piece placed at rows [roff, roff + prow) and zero elsewhere, scaled;
+// ranks[out_slot] <- total columns
+// ---------------------------------------------------------------------------
+struct Piece {
+  View src;
+  int prow, roff;
+  DimR cols;
+  zc scale;
+};
+struct ConcatD {
+  int64_t dst;
+  int rows, out_slot, np;
+  Piece p[4];
+};
+__global__ void k_concat(zc* __restrict__ ar, int* __restrict__ ranks, const ConcatD* __restrict__ ds) {
+  const ConcatD d = ds[blockIdx.y];
+  int c0[5];
+  c0[0] = 0;
+  for (int q = 0; q < d.np; ++q) c0[q + 1] = c0[q] + dimv(d.p[q].cols, ranks);
+  const int tot = c0[d.np];
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)d.rows * tot;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e % d.rows), j = (int)(e / d.rows);
+    int q = 0;
+    while (j >= c0[q + 1]) ++q;
+    const Piece& P = d.p[q];
+    zc v = zmk(0, 0);
+    if (i >= P.roff && i < P.roff + P.prow) v = zmul(P.scale, ar[vidx(P.src, i - P.roff, j - c0[q])]);
+    ar[d.dst + e] = v;
+  }
+  __syncthreads();
+  if (blockIdx.x == 0 && threadIdx.x == 0) ranks[d.out_slot] = tot;
+}
+
+// ---------------------------------------------------------------------------
+// TRSM (left): Y <- op(T)^{-1} Y for a factored dense diagonal leaf T (n x n)
+//   variant 0: T = P^T L U, solve L (unit lower) after applying the row swaps
+//   variant 1: U (upper, non-unit)
+//   variant 2: U^T (lower, non-unit)         [right solves X U^{-1} = (U^{-T} X^T)^T]
+// One CTA per (descriptor, 32-column chunk); the chunk lives in shared memory.
+// ---------------------------------------------------------------------------
+struct TrsmD {
+  int64_t T;
+  int64_t piv;     // offset into the pivot array (variant 0)
+  int n, variant;
+  View Y;
+  DimR p;
+};
+constexpr int TS_COLS = 32;
+__global__ void __launch_bounds__(256) k_trsm(zc* __restrict__ ar, const int* __restrict__ ranks,
+                                              const int* __restrict__ pivs,
+                                              const TrsmD* __restrict__ ds) {
+  const TrsmD d = ds[blockIdx.y];
+  const int p = dimv(d.p, ranks), n = d.n;
+  const int c0 = blockIdx.x * TS_COLS;
+  if (c0 >= p) return;
+  const int nc = min(TS_COLS, p - c0);
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  zc* S = reinterpret_cast<zc*>(smem_raw);   // [nc][n]
+  for (int e = threadIdx.x; e < n * nc; e += blockDim.x) {
+    const int i = e % n, j = e / n;
+    S[j * n + i] = ar[vidx(d.Y, i, c0 + j)];
+  }
+  __syncthreads();
+  const zc* T = ar + d.T;
+  if (d.variant == 0) {
+    if (threadIdx.x < nc) {   // row swaps, sequential per column (zgetrs / _apply_piv order)
+      zc* s = S + threadIdx.x * n;
+      const int* pv = pivs + d.piv;
+      for (int k2 = 0; k2 < n; ++k2) {
+        const int q = pv[k2];
+        if (q != k2) {
+          zc tmp = s[k2];
+          s[k2] = s[q];
+          s[q] = tmp;
+        }
+      }
+    }
+    __syncthreads();
+    for (int j = 0; j < n; ++j) {   // forward, unit diagonal
+      for (int e = threadIdx.x; e < (n - j - 1) * nc; e += blockDim.x) {
+        const int i = j + 1 + e % (n - j - 1), c = e / (n - j - 1);
+        S[c * n + i] = zsub(S[c * n + i], zmul(T[(int64_t)j * n + i], S[c * n + j]));
+      }
+      __syncthreads();
+    }
+  } else if (d.variant == 1) {
+    for (int j = n - 1; j >= 0; --j) {   // backward with U
+      const zc djj = T[(int64_t)j * n + j];
+      if (threadIdx.x < nc) S[threadIdx.x * n + j] = zdiv(S[threadIdx.x * n + j], djj);
+      __syncthreads();
+      for (int e = threadIdx.x; e < j * nc; e += blockDim.x) {
+        const int i = e % j, c = e / j;
+        S[c * n + i] = zsub(S[c * n + i], zmul(T[(int64_t)j * n + i], S[c * n + j]));
+      }
+      __syncthreads();
+    }
+  } else {
+    for (int j = 0; j < n; ++j) {        // forward with U^T: (U^T)[i][j] = U[j][i]
+      const zc djj = T[(int64_t)j * n + j];
+      if (threadIdx.x < nc) S[threadIdx.x * n + j] = zdiv(S[threadIdx.x * n + j], djj);
+      __syncthreads();
+      for (int e = threadIdx.x; e < (n - j - 1) * nc; e += blockDim.x) {
+        const int i = j + 1 + e % (n - j - 1), c = e / (n - j - 1);
+        S[c * n + i] = zsub(S[c * n + i], zmul(T[(int64_t)i * n + j], S[c * n + j]));
+      }
+      __syncthreads();
+    }
+  }
+  for (int e = threadIdx.x; e < n * nc; e += blockDim.x) {
+    const int i = e % n, j = e / n;
+    ar[vidx(d.Y, i, c0 + j)] = S[j * n + i];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// GETRF + rcond: unblocked right-looking LU with partial pivoting (zgetf2:
+// pivot = first max of |Re|+|Im|), then a Hager/Higham 1-norm estimate of
+// ||A^{-1}||_1 (zlacn2) by one warp; rcond < 1e-14 -> SingularDiagonal
+// (hmatrix.py:835-843).  One CTA per diagonal leaf.
+// ---------------------------------------------------------------------------
+struct GetrfD {
+  int64_t A;
+  int64_t piv;
+  int n;
+  int leaf;
+};
+
+__device__ void warp_lu_solve(const zc* A, int n, const int* piv, zc* x, bool herm) {
+  // x <- A^{-1} x  or  A^{-H} x  with A = P^T L U, one warp, x in shared memory
+  const int lane = threadIdx.x & 31;
+  if (!herm) {
+    if (lane == 0)
+      for (int k = 0; k < n; ++k)
+        if (piv[k] != k) {
+          zc t = x[k];
+          x[k] = x[piv[k]];
+          x[piv[k]] = t;
+        }
+    __syncwarp();
+    for (int i = 0; i < n; ++i) {   // L y = x
+      zc s = zmk(0, 0);
+      for (int j = lane; j < i; j += 32) s = zadd(s, zmul(A[(int64_t)j * n + i], x[j]));
+      s = warp_sum(s);
+      if (lane == 0) x[i] = zsub(x[i], s);
+      __syncwarp();
+    }
+    for (int i = n - 1; i >= 0; --i) {   // U z = y
+      zc s = zmk(0, 0);
+      for (int j = i + 1 + lane; j < n; j += 32) s = zadd(s, zmul(A[(int64_t)j * n + i], x[j]));
+      s = warp_sum(s);
+      if (lane == 0) x[i] = zdiv(zsub(x[i], s), A[(int64_t)i * n + i]);
+      __syncwarp();
+    }
+  } else {
+    for (int i = 0; i < n; ++i) {   // U^H y = x
+      zc s = zmk(0, 0);
+      for (int j = lane; j < i; j += 32) s = zadd(s, zcmul(A[(int64_t)i * n + j], x[j]));
+      s = warp_sum(s);
+      if (lane == 0) x[i] = zdiv(zsub(x[i], s), zconj(A[(int64_t)i * n + i]));
+      __syncwarp();
+    }
+    for (int i = n - 1; i >= 0; --i) {   // L^H z = y
+      zc s = zmk(0, 0);
+      for (int j = i + 1 + lane; j < n; j += 32) s = zadd(s, zcmul(A[(int64_t)i * n + j], x[j]));
+      s = warp_sum(s);
+      if (lane == 0) x[i] = zsub(x[i], s);
+      __syncwarp();
+    }
+    if (lane == 0)
+      for (int k = n - 1; k >= 0; --k)
+        if (piv[k] != k) {
+          zc t = x[k];
+          x[k] = x[piv[k]];
+          x[piv[k]] = t;
+        }
+    __syncwarp();
+  }
+}
+
+__global__ void __launch_bounds__(256) k_getrf(zc* __restrict__ ar, int* __restrict__ pivs,
+                                               const GetrfD* __restrict__ ds, double* rcond_out,
+                                               int* flag) {
+  const GetrfD d = ds[blockIdx.x];
+  const int n = d.n;
+  zc* A = ar + d.A;
+  int* piv = pivs + d.piv;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  zc* x = reinterpret_cast<zc*>(smem_raw);   // [n] estimator vector
+  __shared__ double red[LR_NW];
+  __shared__ double s_v[LR_NW];
+  __shared__ int s_i[LR_NW];
+  __shared__ int s_piv;
+  // ||A||_1 of the unfactored block (np.linalg.norm(A, 1))
+  double anorm = 0.0;
+  {
+    double loc = 0.0;
+    for (int j = threadIdx.x; j < n; j += blockDim.x) {
+      double s = 0.0;
+      for (int i = 0; i < n; ++i) {
+        const zc a = A[(int64_t)j * n + i];
+        s += hypot(a.x, a.y);
+      }
+      loc = fmax(loc, s);
+    }
+    for (int o = 16; o > 0; o >>= 1) loc = fmax(loc, __shfl_xor_sync(0xffffffffu, loc, o));
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = loc;
+    __syncthreads();
+    for (int w = 0; w < LR_NW; ++w) anorm = fmax(anorm, red[w]);
+    __syncthreads();
+  }
+  bool zero_pivot = false;
+  for (int j = 0; j < n; ++j) {
+    // pivot: first index of max |Re|+|Im| in column j, rows j..n-1
+    double bv = -1.0;
+    int bi = 0x7fffffff;
+    for (int i = j + threadIdx.x; i < n; i += blockDim.x) {
+      const zc a = A[(int64_t)j * n + i];
+      const double v = fabs(a.x) + fabs(a.y);
+      if (v > bv || (v == bv && i < bi)) {
+        bv = v;
+        bi = i;
+      }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+      if (ov > bv || (ov == bv && oi < bi)) {
+        bv = ov;
+        bi = oi;
+      }
+    }
+    if ((threadIdx.x & 31) == 0) {
+      s_v[threadIdx.x >> 5] = bv;
+      s_i[threadIdx.x >> 5] = bi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double B = s_v[0];
+      int I = s_i[0];
+      for (int w = 1; w < LR_NW; ++w)
+        if (s_v[w] > B || (s_v[w] == B && s_i[w] < I)) {
+          B = s_v[w];
+          I = s_i[w];
+        }
+      s_piv = I;
+      piv[j] = I;
+    }
+    __syncthreads();
+    const int pr = s_piv;
+    if (pr != j)
+      for (int c = threadIdx.x; c < n; c += blockDim.x) {
+        zc t = A[(int64_t)c * n + j];
+        A[(int64_t)c * n + j] = A[(int64_t)c * n + pr];
+        A[(int64_t)c * n + pr] = t;
+      }
+    __syncthreads();
+    const zc ajj = A[(int64_t)j * n + j];
+    if (ajj.x == 0.0 && ajj.y == 0.0) {
+      zero_pivot = true;
+      continue;
+    }
+    const zc rinv = zdiv(zmk(1.0, 0.0), ajj);
+    for (int i = j + 1 + threadIdx.x; i < n; i += blockDim.x)
+      A[(int64_t)j * n + i] = zmul(A[(int64_t)j * n + i], rinv);
+    __syncthreads();
+    const int rem = n - j - 1;
+    for (int e = threadIdx.x; e < rem * rem; e += blockDim.x) {
+      const int i = j + 1 + e % rem, c = j + 1 + e / rem;
+      A[(int64_t)c * n + i] = zsub(A[(int64_t)c * n + i], zmul(A[(int64_t)j * n + i], A[(int64_t)c * n + j]));
+    }
+    __syncthreads();
+  }
+  // rcond via the 1-norm estimator (zlacn2 structure), warp 0 only
+  double rcond = 0.0;
+  if (!zero_pivot && anorm > 0.0 && threadIdx.x < 32) {
+    const int lane = threadIdx.x;
+    double est = 0.0;
+    for (int i = lane; i < n; i += 32) x[i] = zmk(1.0 / n, 0.0);
+    __syncwarp();
+    int jlast = -1;
+    for (int it = 0; it < 5; ++it) {
+      warp_lu_solve(A, n, piv, x, false);   // y = A^{-1} x
+      double s = 0.0;
+      for (int i = lane; i < n; i += 32) s += hypot(x[i].x, x[i].y);
+      s = warp_sum(s);
+      if (it > 0 && s <= est) break;
+      est = s;
+      for (int i = lane; i < n; i += 32) {   // xi = sign(y)
+        const double a = hypot(x[i].x, x[i].y);
+        x[i] = a > 0 ? zmk(x[i].x / a, x[i].y / a) : zmk(1.0, 0.0);
+      }
+      __syncwarp();
+      warp_lu_solve(A, n, piv, x, true);    // z = A^{-H} xi
+      double bv = -1.0;
+      int bi = 0;
+      for (int i = lane; i < n; i += 32) {
+        const double a = hypot(x[i].x, x[i].y);
+        if (a > bv) {
+          bv = a;
+          bi = i;
+        }
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ov > bv || (ov == bv && oi < bi)) {
+          bv = ov;
+          bi = oi;
+        }
+      }
+      if (bi == jlast) break;
+      jlast = bi;
+      for (int i = lane; i < n; i += 32) x[i] = zmk(i == bi ? 1.0 : 0.0, 0.0);
+      __syncwarp();
+    }
+    // alternative estimate with x_i = (-1)^i (1 + i/(n-1))
+    for (int i = lane; i < n; i += 32)
+      x[i] = zmk((i % 2 ? -1.0 : 1.0) * (1.0 + (n > 1 ? (double)i / (n - 1) : 0.0)), 0.0);
+    __syncwarp();
+    warp_lu_solve(A, n, piv, x, false);
+    double s = 0.0;
+    for (int i = lane; i < n; i += 32) s += hypot(x[i].x, x[i].y);
+    s = warp_sum(s);
+    est = fmax(est, 2.0 * s / (3.0 * n));
+    rcond = est > 0.0 ? (1.0 / est) / anorm : 0.0;
+  }
+  if (threadIdx.x == 0) {
+    rcond_out[d.leaf] = rcond;
+    if (!(rcond >= 1e-14)) atomicOr(flag, 1);
+  }
+}

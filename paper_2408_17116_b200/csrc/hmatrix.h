@@ -69,6 +69,8 @@ struct cbie_hmat {
 struct TruncDesc {
   int64_t in_u, in_v;          // arena offsets of the inputs
   int64_t out_u, out_v;        // arena offsets of the outputs (m x cap, n x cap)
+  int ldu, ldv;                // leading dimensions of the inputs
+  int skip_slot;               // >= 0 and ranks[skip_slot] == 0: no-op (adding rank 0)
   int m, n;
   int k;                       // static rank if k_slot < 0
   int k_slot;                  // >= 0: k = ranks[k_slot] (device-resident)

@@ -27,6 +27,7 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
   int* order = reinterpret_cast<int*>(sig + KS);
 
   const int m = d.m, n = d.n;
+  if (d.skip_slot >= 0 && ranks[d.skip_slot] == 0) return;
   const int k = d.k_slot >= 0 ? ranks[d.k_slot] : d.k;
   const bool ident = d.in_v < 0;
   if (k <= 0 || m == 0 || n == 0) {
@@ -40,18 +41,19 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
   zc* M = scratch + (int64_t)blockIdx.x * scratch_per;   // kk1 x kk2, ld kk1
   zc* W = M + (int64_t)kk1 * kk2;                         // kk2 x kk2
 
-  cta_qr(U, m, k, m, rd1, kap1, red);
-  if (!ident) cta_qr(Vt, n, k, n, rd2, kap2, red);
+  const int ldu = d.ldu, ldv = d.ldv;
+  cta_qr(U, m, k, ldu, rd1, kap1, red);
+  if (!ident) cta_qr(Vt, n, k, ldv, rd2, kap2, red);
   // M = R1 R2^T (R2 = I for the dense mode)
   for (int e = threadIdx.x; e < kk1 * kk2; e += LR_NT) {
     const int a = e % kk1, b = e / kk1;
     zc s = zmk(0.0, 0.0);
     if (ident) {
-      s = b == a ? rd1[a] : (b > a ? U[(int64_t)b * m + a] : zmk(0.0, 0.0));
+      s = b == a ? rd1[a] : (b > a ? U[(int64_t)b * ldu + a] : zmk(0.0, 0.0));
     } else {
       for (int c = max(a, b); c < k; ++c) {
-        const zc r1 = c == a ? rd1[a] : U[(int64_t)c * m + a];
-        const zc r2 = c == b ? rd2[b] : Vt[(int64_t)c * n + b];
+        const zc r1 = c == a ? rd1[a] : U[(int64_t)c * ldu + a];
+        const zc r2 = c == b ? rd2[b] : Vt[(int64_t)c * ldv + b];
         s = zadd(s, zmul(r1, r2));
       }
     }
@@ -97,8 +99,8 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
     Vo[(int64_t)l * n + j] = j < kk2 ? zconj(W[(int64_t)order[l] * kk2 + j]) : zmk(0.0, 0.0);
   }
   __syncthreads();
-  cta_apply_q(U, m, kk1, m, kap1, Uo, r, m);
-  if (!ident) cta_apply_q(Vt, n, kk2, n, kap2, Vo, r, n);
+  cta_apply_q(U, m, kk1, ldu, kap1, Uo, r, m);
+  if (!ident) cta_apply_q(Vt, n, kk2, ldv, kap2, Vo, r, n);
   if (threadIdx.x == 0) ranks[d.out_slot] = r;
 }
 

@@ -1,0 +1,77 @@
+"""GPU H-LU + solve (solve_direct) against the reference's own solutions
+(golden fixtures).  Bar: surface current within 10 x aca_tol relative L2
+(BASELINE.json north_star)."""
+
+import numpy as np
+import pytest
+
+from gold import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _problem(kind, **kw):
+    from paper_2408_17116_b200 import geometry as geo, kernels as ker
+    from paper_2408_17116_b200.solver import Problem
+    vac = ker.Medium.from_relative(1.0, 1.0, 1.0)
+    pw = ker.PlaneWave([0, 0, 1], [1, 0, 0], 1.0)
+    if kind == "cfg1":
+        return Problem(geo.unit_sphere_patches(0.5, 1, (6, 6)), ker.FormulationSpec(ker.MFIE_PEC, vac),
+                       pw, aca_tol=1e-6, eta=1.0, n_leaf=128)
+    if kind == "small":
+        return Problem(geo.unit_sphere_patches(0.5, 0, (4, 4)), ker.FormulationSpec(ker.MFIE_PEC, vac), pw)
+    if kind == "muller":
+        spec = ker.FormulationSpec(ker.MULLER, vac, ker.Medium.from_relative(4.0, 1.0, 1.0))
+        return Problem(geo.unit_sphere_patches(0.5, 0, (5, 5)), spec, pw, aca_tol=1e-5)
+    raise ValueError(kind)
+
+
+def _rel(a, b):
+    return np.linalg.norm(a - b) / np.linalg.norm(b)
+
+
+def test_small_direct_matches_reference():
+    from paper_2408_17116_b200.solver import solve_direct
+    g = golden("small_solve.npz")
+    prob = _problem("small")
+    r = solve_direct(prob)
+    assert _rel(r.solution, g["x_direct"]) <= 10 * prob.aca_tol
+    assert _rel(r.solution, g["x_dense"]) <= 100 * prob.aca_tol
+    assert r.residual <= 100 * prob.aca_tol
+
+
+def test_cfg1_direct_matches_reference():
+    from paper_2408_17116_b200.solver import solve_direct
+    g = golden("cfg1_solve.npz")
+    prob = _problem("cfg1")
+    r = solve_direct(prob)
+    assert _rel(r.solution, g["x_direct"]) <= 10 * prob.aca_tol, _rel(r.solution, g["x_direct"])
+    assert _rel(r.solution, g["x_dense"]) <= 10 * prob.aca_tol
+    assert r.metrics["hmatrix_diagnostics"]["demoted_blocks"] == int(g["demoted"])
+
+
+def test_muller_direct_matches_reference():
+    from paper_2408_17116_b200.solver import solve_direct
+    g = golden("muller_solve.npz")
+    prob = _problem("muller")
+    r = solve_direct(prob)
+    assert _rel(r.solution, g["x_direct"]) <= 10 * prob.aca_tol, _rel(r.solution, g["x_direct"])
+
+
+def test_solve_is_deterministic_and_multi_rhs():
+    from paper_2408_17116_b200 import hmatrix as hm
+    from paper_2408_17116_b200.solver import build_hmatrix
+    prob = _problem("small")
+    H, gen, scaled, _ = build_hmatrix(prob)
+    F = hm.hlu_factor(H, prob.effective_trunc_tol)
+    rng = np.random.default_rng(1)
+    b = rng.standard_normal(H.N) + 1j * rng.standard_normal(H.N)
+    x1 = F.solve(b)
+    x2 = F.solve(b)
+    assert np.array_equal(x1, x2)
+    X = F.solve(np.stack([b, -2j * b], 1))
+    assert np.allclose(X[:, 0], x1, rtol=0, atol=1e-13 * np.abs(x1).max())
+    assert np.allclose(X[:, 1], -2j * x1, rtol=0, atol=1e-12 * np.abs(x1).max())
+    assert np.abs(F.solve(np.zeros(H.N, complex))).max() == 0.0
+    F2 = hm.hlu_factor(H, prob.effective_trunc_tol)
+    assert np.array_equal(F2.solve(b), x1)
