@@ -133,9 +133,22 @@ int cbie_hmatvec(cbie_hmat* h, const cbie_c128* x, cbie_c128* y, int nrhs);
 int cbie_hlu_factor(cbie_hmat* h, double trunc_tol, cbie_hlu** out);
 void cbie_hlu_destroy(cbie_hlu* f);
 
+/* One leaf of the H-LU factors (same layout as cbie_hmatrix_leaf); factored
+ * diagonal leaves return LAPACK-style combined L\U in D and 0-based row
+ * pivots in piv (may be NULL).  kind: 0 dense, 1 low rank, 2 factored. */
+int cbie_hlu_leaf(cbie_hlu* f, int64_t leaf, int* kind, int* rank, cbie_c128* D_or_U,
+                  cbie_c128* V, int32_t* piv);
+
 /* x = (LU)^{-1} b, original dof order, [N][nrhs] row-major.
  * HLUFactors.solve (hmatrix.py:807-816). */
 int cbie_hlu_solve(cbie_hlu* f, const cbie_c128* b, cbie_c128* x, int nrhs);
+
+/* Low-rank recompression of host data (truncate_lowrank, hmatrix.py:412-426):
+ * U [m][k] row-major, V [k][n] row-major -> Uo [m][*r], Vo [*r][n] (capacity
+ * min(m, n, k) rows/cols).  V == NULL: truncated SVD of the dense U [m][n]
+ * (hmatrix.py:605-609, k ignored). */
+int cbie_lowrank_truncate(cbie_ctx* ctx, const cbie_c128* U, int m, int k, const cbie_c128* V,
+                          int n, double tol, int* r, cbie_c128* Uo, cbie_c128* Vo);
 
 /* Timings (CUDA events), counts, flops, bytes as one JSON object.
  * which: 0 = context, 1 = hmatrix, 2 = hlu. */

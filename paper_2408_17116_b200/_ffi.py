@@ -48,7 +48,10 @@ _SIGS = {
     "cbie_hmatvec": (ct.c_int, [P, P, P, ct.c_int]),
     "cbie_hlu_factor": (ct.c_int, [P, ct.c_double, ct.POINTER(P)]),
     "cbie_hlu_destroy": (None, [P]),
+    "cbie_hlu_leaf": (ct.c_int, [P, ct.c_int64, ct.POINTER(ct.c_int), ct.POINTER(ct.c_int), P, P, P]),
     "cbie_hlu_solve": (ct.c_int, [P, P, P, ct.c_int]),
+    "cbie_lowrank_truncate": (ct.c_int, [P, P, ct.c_int, ct.c_int, P, ct.c_int, ct.c_double,
+                                         ct.POINTER(ct.c_int), P, P]),
     "cbie_stats_json": (ct.c_int, [P, ct.c_int, ct.c_char_p, ct.c_size_t]),
 }
 

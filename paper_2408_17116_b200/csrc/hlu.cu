@@ -88,23 +88,36 @@ struct Recorder {
   std::vector<Task> tasks;
   double flops = 0.0;
   int64_t trunc_count = 0, gemm_count = 0, trsm_count = 0, getrf_count = 0;
+  bool serial = getenv("CBIE_SERIAL") != nullptr;
 
   int new_buf() {
     last_w.push_back(0);
     max_r.push_back(0);
     return nbuf++;
   }
-  int new_slot(int v0) {
+  std::vector<int> slot_owner;
+  int new_slot(int v0, int owner = -1) {
     init_ranks.push_back(v0);
+    slot_owner.push_back(owner);
     return (int)init_ranks.size() - 1;
   }
+  // buffers whose contents an op consumes through a Mat: data + rank-slot owners
+  void reads_of(const Mat& a, std::vector<int>& v) const {
+    v.push_back(a.buf);
+    if (a.rslot >= 0) v.push_back(slot_owner[a.rslot]);
+    if (a.cslot >= 0) v.push_back(slot_owner[a.cslot]);
+  }
   void add(int kind, int idx, std::initializer_list<int> rd, std::initializer_list<int> wr) {
+    add(kind, idx, std::vector<int>(rd), std::vector<int>(wr));
+  }
+  void add(int kind, int idx, const std::vector<int>& rd, const std::vector<int>& wr) {
     int lvl = 0;
     for (int b : rd)
       if (b >= 0) lvl = std::max(lvl, last_w[b]);
     for (int b : wr)
       if (b >= 0) lvl = std::max(lvl, std::max(last_w[b], max_r[b]));
     ++lvl;
+    if (serial) lvl = (int)tasks.size() + 1;   // debug: strict tape order
     for (int b : rd)
       if (b >= 0) max_r[b] = std::max(max_r[b], lvl);
     for (int b : wr)
@@ -155,7 +168,7 @@ struct Recorder {
     Tmp t = alloc(std::max<int64_t>((int64_t)(m + n) * cap, 1));
     owned.push_back(t);
     r.cap = cap;
-    r.slot = new_slot(0);
+    r.slot = new_slot(0, t.buf);
     r.buf = t.buf;
     r.U.off = t.off;
     r.U.ld = m;
@@ -183,10 +196,11 @@ struct Recorder {
     gemm.push_back(d);
     flops += 8.0 * A.rows * A.cols * B.cols;
     ++gemm_count;
-    if (beta.x != 0.0 || beta.y != 0.0)
-      add(OP_GEMM, (int)gemm.size() - 1, {A.buf, B.buf, C.buf}, {C.buf});
-    else
-      add(OP_GEMM, (int)gemm.size() - 1, {A.buf, B.buf}, {C.buf});
+    std::vector<int> rd;
+    reads_of(A, rd);
+    reads_of(B, rd);
+    reads_of(C, rd);   // C's dims (and data when beta != 0)
+    add(OP_GEMM, (int)gemm.size() - 1, rd, {C.buf});
   }
   // Y = a X + b Y
   void op_ew(const Mat* X, const Mat& Y, zc a, zc b) {
@@ -200,8 +214,10 @@ struct Recorder {
     d.b = b;
     d.hasX = X != nullptr;
     ew.push_back(d);
-    const bool readsY = b.x != 0.0 || b.y != 0.0;
-    add(OP_EW, (int)ew.size() - 1, {X ? X->buf : -1, readsY ? Y.buf : -1}, {Y.buf});
+    std::vector<int> rd;
+    if (X) reads_of(*X, rd);
+    reads_of(Y, rd);
+    add(OP_EW, (int)ew.size() - 1, rd, {Y.buf});
   }
   void op_trsm(const Mat& T, int64_t pivoff, int variant, const Mat& Y) {
     if (Y.cols == 0) return;
@@ -209,7 +225,9 @@ struct Recorder {
     trsm.push_back(d);
     flops += 4.0 * T.rows * T.rows * Y.cols;
     ++trsm_count;
-    add(OP_TRSM, (int)trsm.size() - 1, {T.buf, Y.buf}, {Y.buf});
+    std::vector<int> rd{T.buf};
+    reads_of(Y, rd);
+    add(OP_TRSM, (int)trsm.size() - 1, rd, {Y.buf});
   }
   void op_getrf(const Mat& A, int64_t pivoff, int leaf) {
     getrf.push_back(GetrfD{A.off, pivoff, A.rows, leaf});
@@ -227,15 +245,20 @@ struct Recorder {
     d.np = (int)ps.size();
     for (int i = 0; i < d.np; ++i) d.p[i] = ps[i];
     cat.push_back(d);
-    int b[4] = {-1, -1, -1, -1};
-    for (size_t i = 0; i < srcbufs.size(); ++i) b[i] = srcbufs[i];
-    add(OP_CONCAT, (int)cat.size() - 1, {b[0], b[1], b[2], b[3]}, {dstbuf});
+    std::vector<int> rd(srcbufs);
+    for (const Piece& p : ps) {
+      if (p.cols.slot >= 0) rd.push_back(slot_owner[p.cols.slot]);
+    }
+    add(OP_CONCAT, (int)cat.size() - 1, rd, {dstbuf});
   }
   void op_trunc(const TruncDesc& d, int kmax, int rdbuf, int rdbuf2, int wrbuf) {
     trunc.push_back(d);
     trunc_kmax.push_back(kmax);
     ++trunc_count;
-    add(OP_TRUNC, (int)trunc.size() - 1, {rdbuf, rdbuf2, wrbuf}, {rdbuf, wrbuf});
+    std::vector<int> rd{rdbuf, rdbuf2, wrbuf};
+    if (d.k_slot >= 0) rd.push_back(slot_owner[d.k_slot]);
+    if (d.skip_slot >= 0) rd.push_back(slot_owner[d.skip_slot]);
+    add(OP_TRUNC, (int)trunc.size() - 1, rd, {rdbuf, wrbuf});
   }
 };
 
@@ -400,7 +423,7 @@ struct Builder {
     const int kc = Tg.cap + U.cols;
     Recorder::Tmp t = R.alloc((int64_t)(m + n) * kc);
     own.push_back(t);
-    const int ks = R.new_slot(0);
+    const int ks = R.new_slot(0, t.buf);
     std::vector<Piece> pu{Piece{Tg.U.view(), m, 0, Tg.U.Cc(), zmk(1, 0)},
                           Piece{U.view(), U.rows, 0, U.Cc(), sign}};
     std::vector<Piece> pv{Piece{Tg.Vt.view(), n, 0, Tg.Vt.Cc(), zmk(1, 0)},
@@ -573,7 +596,7 @@ struct Builder {
     for (auto& p : parts) kc += p.cap;
     Recorder::Tmp t = R.alloc((int64_t)(m + n) * kc);
     own2.push_back(t);
-    const int ks = R.new_slot(0);
+    const int ks = R.new_slot(0, t.buf);
     std::vector<Piece> pu, pv;
     std::vector<int> bu;
     for (size_t i = 0; i < parts.size(); ++i) {
@@ -741,6 +764,9 @@ struct Builder {
 // ---------------------------------------------------------------------------
 struct Exec {
   int levels = 0, launches = 0;
+  double kind_ms[OP_NKIND] = {0, 0, 0, 0, 0, 0};
+  int kind_launch[OP_NKIND] = {0, 0, 0, 0, 0, 0};
+  int64_t kind_tasks[OP_NKIND] = {0, 0, 0, 0, 0, 0};
 };
 
 Exec execute(Recorder& R, zc* arena, int* ranks, int* piv, double* rcond, int* flag,
@@ -814,12 +840,21 @@ Exec execute(Recorder& R, zc* arena, int* ranks, int* piv, double* rcond, int* f
   CK(cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem));
   const size_t getrf_smem = (size_t)maxn_getrf * sizeof(zc);
   int lvl = -1;
+  const bool prof = getenv("CBIE_PROFILE") != nullptr;
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  if (prof) {
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+  }
   for (auto& gr : groups) {
     if (gr.level != lvl) {
       ++ex.levels;
       lvl = gr.level;
     }
     ++ex.launches;
+    ex.kind_launch[gr.kind]++;
+    ex.kind_tasks[gr.kind] += gr.count;
+    if (prof) cudaEventRecord(e0, s);
     switch (gr.kind) {
       case OP_GEMM: {
         int mt = 1, nt = 1;
@@ -864,6 +899,17 @@ Exec execute(Recorder& R, zc* arena, int* ranks, int* piv, double* rcond, int* f
         break;
     }
     CKL();
+    if (prof) {
+      cudaEventRecord(e1, s);
+      cudaEventSynchronize(e1);
+      float ms = 0;
+      cudaEventElapsedTime(&ms, e0, e1);
+      ex.kind_ms[gr.kind] += ms;
+    }
+  }
+  if (prof) {
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
   }
   (void)gemm_tiles;
   CK(cudaStreamSynchronize(s));
@@ -900,10 +946,12 @@ static void hlu_factor_impl(cbie_hlu* F) {
   auto t0 = std::chrono::steady_clock::now();
   Recorder R;
   R.leaf_end = leaf_end;
-  R.pool_budget = (int64_t)8 << 30 >> 4;   // 8 GiB of temporaries before chunk reuse
+  // temporaries before chunk reuse (GiB, CBIE_POOL_GB overrides)
+  R.pool_budget = (int64_t)((getenv("CBIE_POOL_GB") ? atof(getenv("CBIE_POOL_GB")) : 8.0) *
+                            (double)(1ll << 30)) / (int64_t)sizeof(zc);
   for (int li = 0; li < nleaf; ++li) {
     R.new_buf();
-    R.new_slot(0);
+    R.new_slot(0, li);
   }
   Builder B(R, *F);
   B.factor(T.root_node);
@@ -935,6 +983,14 @@ static void hlu_factor_impl(cbie_hlu* F) {
   CK(cudaMemcpy(&hovf, ovf.p, 8, cudaMemcpyDeviceToHost));
   F->leaf_end = leaf_end;
   F->stat["levels"] = ex.levels;
+  {
+    const char* nm[OP_NKIND] = {"gemm", "ew", "concat", "trsm", "getrf", "trunc"};
+    for (int k = 0; k < OP_NKIND; ++k) {
+      F->stat[std::string("launch_") + nm[k]] = ex.kind_launch[k];
+      F->stat[std::string("tasks_") + nm[k]] = (double)ex.kind_tasks[k];
+      if (getenv("CBIE_PROFILE")) F->stat[std::string("ms_") + nm[k]] = ex.kind_ms[k];
+    }
+  }
   F->stat["launches"] = ex.launches;
   F->stat["tasks"] = (double)R.tasks.size();
   F->stat["flops"] = R.flops;
@@ -973,7 +1029,7 @@ static void hlu_solve_impl(cbie_hlu* F, const zc* b, zc* x, int nrhs) {
   const int nleaf = (int)T.leaves.size();
   for (int li = 0; li < nleaf; ++li) {
     R.new_buf();
-    R.new_slot(0);
+    R.new_slot(0, li);
   }
   // the rank slots of the factors live in F->ranks (same leaf slot numbering)
   std::vector<Recorder::Tmp> own;
@@ -1038,6 +1094,50 @@ int cbie_hlu_factor(cbie_hmat* h, double trunc_tol, cbie_hlu** out) {
 }
 
 void cbie_hlu_destroy(cbie_hlu* f) { delete f; }
+
+int cbie_hlu_leaf(cbie_hlu* f, int64_t leaf, int* kind, int* rank, cbie_c128* D_or_U,
+                  cbie_c128* V, int32_t* piv) {
+  try {
+    const Tree& T = f->tree;
+    if (leaf < 0 || leaf >= (int64_t)T.leaves.size()) throw cbie_error(CBIE_EINVALID, "leaf index");
+    cudaSetDevice(f->H->ctx->device);
+    const auto& L = T.leaves[leaf];
+    const int m = L.m, n = L.n;
+    if (L.kind == BLK_DENSE) {
+      *kind = f->pivoff[leaf] >= 0 ? 2 : 0;
+      *rank = 0;
+      if (D_or_U) {
+        std::vector<zc> cm((size_t)m * n);
+        CK(cudaMemcpy(cm.data(), f->arena.p + L.off_d, sizeof(zc) * cm.size(), cudaMemcpyDeviceToHost));
+        zc* o = reinterpret_cast<zc*>(D_or_U);
+        for (int i = 0; i < m; ++i)
+          for (int j = 0; j < n; ++j) o[(size_t)i * n + j] = cm[(size_t)j * m + i];
+      }
+      if (piv && f->pivoff[leaf] >= 0)
+        CK(cudaMemcpy(piv, f->piv.p + f->pivoff[leaf], sizeof(int) * m, cudaMemcpyDeviceToHost));
+    } else {
+      *kind = 1;
+      int r = 0;
+      CK(cudaMemcpy(&r, f->ranks.p + leaf, sizeof(int), cudaMemcpyDeviceToHost));
+      *rank = r;
+      if (D_or_U && r) {
+        std::vector<zc> cu((size_t)m * r), cv((size_t)n * r);
+        CK(cudaMemcpy(cu.data(), f->arena.p + L.off_u, sizeof(zc) * cu.size(), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(cv.data(), f->arena.p + L.off_v, sizeof(zc) * cv.size(), cudaMemcpyDeviceToHost));
+        zc* ou = reinterpret_cast<zc*>(D_or_U);
+        zc* ov = reinterpret_cast<zc*>(V);
+        for (int i = 0; i < m; ++i)
+          for (int l = 0; l < r; ++l) ou[(size_t)i * r + l] = cu[(size_t)l * m + i];
+        for (int l = 0; l < r; ++l)
+          for (int j = 0; j < n; ++j) ov[(size_t)l * n + j] = cv[(size_t)l * n + j];
+      }
+    }
+  } catch (const cbie_error& e) {
+    f->H->ctx->err = e.what();
+    return e.code;
+  }
+  return CBIE_OK;
+}
 
 int cbie_hlu_solve(cbie_hlu* f, const cbie_c128* b, cbie_c128* x, int nrhs) {
   try {

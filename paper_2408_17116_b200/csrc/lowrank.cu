@@ -125,3 +125,69 @@ void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int
     CKL();
   }
 }
+
+extern "C" int cbie_lowrank_truncate(cbie_ctx* c, const cbie_c128* U, int m, int k,
+                                     const cbie_c128* V, int n, double tol, int* r,
+                                     cbie_c128* Uo, cbie_c128* Vo) {
+  try {
+    cudaSetDevice(c->device);
+    cudaStream_t s = c->stream;
+    const bool dense = V == nullptr;
+    if (dense) k = n;
+    if (m <= 0 || n <= 0 || k <= 0) throw cbie_error(CBIE_EINVALID, "empty factors");
+    const int cap = std::min(std::min(m, n), k);
+    // arena: U col-major m x k | Vt col-major n x k | Uo m x cap | Vto n x cap
+    std::vector<zc> h((size_t)(m + n) * k + (size_t)(m + n) * cap);
+    const zc* hu = reinterpret_cast<const zc*>(U);
+    for (int i = 0; i < m; ++i)
+      for (int l = 0; l < k; ++l) h[(size_t)l * m + i] = hu[(size_t)i * k + l];
+    if (!dense) {
+      const zc* hv = reinterpret_cast<const zc*>(V);
+      for (int l = 0; l < k; ++l)
+        for (int j = 0; j < n; ++j) h[(size_t)m * k + (size_t)l * n + j] = hv[(size_t)l * n + j];
+    }
+    DBuf<zc> ar;
+    ar.upload(h, s);
+    DBuf<int> ranks;
+    std::vector<int> r0(2, 0);
+    ranks.upload(r0, s);
+    TruncDesc d;
+    d.in_u = 0;
+    d.in_v = dense ? -1 : (int64_t)m * k;
+    d.ldu = m;
+    d.ldv = n;
+    d.skip_slot = -1;
+    d.out_u = (int64_t)(m + n) * k;
+    d.out_v = d.out_u + (int64_t)m * cap;
+    d.m = m;
+    d.n = n;
+    d.k = k;
+    d.k_slot = -1;
+    d.cap = cap;
+    d.out_slot = 0;
+    DBuf<TruncDesc> dd;
+    dd.upload(&d, 1, s);
+    DBuf<unsigned long long> ovf;
+    ovf.alloc(1);
+    CK(cudaMemsetAsync(ovf.p, 0, 8, s));
+    DBuf<zc> scratch;
+    const int kmax = dense ? std::max(m, n) : std::min(k, std::max(m, n));
+    launch_truncate(ar.p, ranks.p, dd.p, 1, kmax, tol, ovf.p, scratch, s);
+    int rr = 0;
+    CK(cudaMemcpyAsync(&rr, ranks.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    std::vector<zc> out((size_t)(m + n) * cap);
+    CK(cudaMemcpyAsync(out.data(), ar.p + d.out_u, sizeof(zc) * out.size(), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    *r = rr;
+    zc* uo = reinterpret_cast<zc*>(Uo);
+    zc* vo = reinterpret_cast<zc*>(Vo);
+    for (int i = 0; i < m; ++i)
+      for (int l = 0; l < rr; ++l) uo[(size_t)i * rr + l] = out[(size_t)l * m + i];
+    for (int l = 0; l < rr; ++l)
+      for (int j = 0; j < n; ++j) vo[(size_t)l * n + j] = out[(size_t)m * cap + (size_t)l * n + j];
+  } catch (const cbie_error& e) {
+    c->err = e.what();
+    return e.code;
+  }
+  return CBIE_OK;
+}

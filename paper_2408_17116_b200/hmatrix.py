@@ -148,6 +148,28 @@ class HLUFactors:
     def stats(self) -> dict:
         return dict(self._stats)
 
+    def leaf(self, i: int):
+        """('dense', D) | ('lu', LU, piv) | ('lowrank', U, V) for leaf i (permuted order)."""
+        perm, lv = self.H.tree()
+        C = self.H.C
+        m = int(lv[i, 1] - lv[i, 0]) * C
+        n = int(lv[i, 3] - lv[i, 2]) * C
+        kind, rank = ct.c_int(), ct.c_int()
+        self.dev.check(self.dev.lib.cbie_hlu_leaf(self.h, int(i), ct.byref(kind), ct.byref(rank),
+                                                  None, None, None))
+        if kind.value in (0, 2):
+            D = np.empty((m, n), complex)
+            piv = np.empty(m, np.int32)
+            self.dev.check(self.dev.lib.cbie_hlu_leaf(self.h, int(i), ct.byref(kind), ct.byref(rank),
+                                                      _ffi.ptr(D), None, _ffi.ptr(piv)))
+            return ("lu", D, piv) if kind.value == 2 else ("dense", D)
+        r = rank.value
+        U = np.empty((m, r), complex)
+        V = np.empty((r, n), complex)
+        self.dev.check(self.dev.lib.cbie_hlu_leaf(self.h, int(i), ct.byref(kind), ct.byref(rank),
+                                                  _ffi.ptr(U), _ffi.ptr(V), None))
+        return ("lowrank", U, V)
+
 
 def hlu_factor(H: HMatrix, tol: float) -> HLUFactors:
     return HLUFactors(H, tol)
