@@ -53,6 +53,12 @@ int cbie_create(int device, cbie_ctx** out);
 void cbie_destroy(cbie_ctx* ctx);
 const char* cbie_last_error(const cbie_ctx* ctx);
 
+/* Number of libcbie kernel launches so far (process-wide counter). */
+int64_t cbie_launch_count(void);
+
+/* The context's CUDA stream (cudaStream_t), for event timing by the caller. */
+void* cbie_stream(cbie_ctx* ctx);
+
 /* Patch geometry, uniform order nu x nv for all patches.
  *   samples      [npatch][nu][nv][3]   == Patch.samples[l, k, :]   (geometry.py:100-117)
  *   chart_kind   [npatch]              CBIE_CHART_*

@@ -32,6 +32,8 @@ _SIGS = {
     "cbie_create": (ct.c_int, [ct.c_int, ct.POINTER(P)]),
     "cbie_destroy": (None, [P]),
     "cbie_last_error": (ct.c_char_p, [P]),
+    "cbie_launch_count": (ct.c_int64, []),
+    "cbie_stream": (ct.c_void_p, [P]),
     "cbie_set_geometry": (ct.c_int, [P, ct.c_int, ct.c_int, ct.c_int, P, P, P, P, P]),
     "cbie_node_frames": (ct.c_int, [P, P, P, P, P]),
     "cbie_set_formulation": (ct.c_int, [P, ct.c_int, ct.c_double, C128, C128, C128, C128, C128,

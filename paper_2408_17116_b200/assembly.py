@@ -85,6 +85,17 @@ class GpuGenerator:
         self.row_scale = np.tile(self.row_c, n)
         self.col_scale = np.tile(self.col_c, n)
 
+    def classify(self):
+        """Re-run classification + near-field pair blocks on the device (one
+        pass of the fill's K1/K3 stage; the geometry stays resident)."""
+        nn, ns, nf = ct.c_int64(), ct.c_int64(), ct.c_int64()
+        self.dev.check(self.dev.lib.cbie_classify(self.dev.h, ct.byref(nn), ct.byref(ns), ct.byref(nf)))
+        self.n_near, self.n_self, self.newton_fallbacks = nn.value, ns.value, nf.value
+
+    @property
+    def stream(self) -> int:
+        return int(self.dev.lib.cbie_stream(self.dev.h) or 0)
+
     # -- classification export -------------------------------------------------------
     def classification(self):
         m = self.n_near + self.n_self

@@ -115,7 +115,14 @@ struct cbie_error : std::runtime_error {
                            __FILE__ + ":" + std::to_string(__LINE__));                    \
   } while (0)
 
-#define CKL() CK(cudaGetLastError())
+// every kernel launch site calls CKL(); it also counts launches (cbie_launch_count)
+#include <atomic>
+extern std::atomic<long long> g_cbie_launches;
+#define CKL()                 \
+  do {                        \
+    ++g_cbie_launches;        \
+    CK(cudaGetLastError());   \
+  } while (0)
 
 template <class T>
 struct DBuf {

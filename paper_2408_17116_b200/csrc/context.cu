@@ -256,6 +256,8 @@ void ctx_set_formulation(cbie_ctx* c, int kind, double omega, zc k1, zc k2, zc e
   c->N = (int64_t)c->npts * p.C;
 }
 
+std::atomic<long long> g_cbie_launches{0};
+
 // ---------------------------------------------------------------------------
 // C-ABI
 // ---------------------------------------------------------------------------
@@ -304,6 +306,10 @@ void cbie_destroy(cbie_ctx* c) {
 }
 
 const char* cbie_last_error(const cbie_ctx* c) { return c ? c->err.c_str() : "null context"; }
+
+int64_t cbie_launch_count(void) { return g_cbie_launches.load(); }
+
+void* cbie_stream(cbie_ctx* c) { return c ? (void*)c->stream : nullptr; }
 
 int cbie_set_geometry(cbie_ctx* c, int npatch, int nu, int nv, const double* samples,
                       const int* chart_kind, const double* chart_params, const double* star_coef,

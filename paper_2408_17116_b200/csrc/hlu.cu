@@ -60,7 +60,7 @@ struct LR {
   Mat V() const { return Vt.T(); }
 };
 
-enum OpKind { OP_GEMM, OP_EW, OP_CONCAT, OP_TRSM, OP_GETRF, OP_TRUNC, OP_NKIND };
+enum OpKind { OP_GEMM, OP_EW, OP_CONCAT, OP_TRSM, OP_GETRF, OP_TRUNC, OP_DLR, OP_NKIND };
 
 struct Task {
   int kind, idx, level;
@@ -85,6 +85,8 @@ struct Recorder {
   std::vector<GetrfD> getrf;
   std::vector<TruncDesc> trunc;
   std::vector<int> trunc_kmax;
+  std::vector<DenseLRDesc> dlr;
+  double tol = 1e-4;
   std::vector<Task> tasks;
   double flops = 0.0;
   int64_t trunc_count = 0, gemm_count = 0, trsm_count = 0, getrf_count = 0;
@@ -250,6 +252,24 @@ struct Recorder {
       if (p.cols.slot >= 0) rd.push_back(slot_owner[p.cols.slot]);
     }
     add(OP_CONCAT, (int)cat.size() - 1, rd, {dstbuf});
+  }
+  void op_dlr(const Mat& P, const LR& o) {
+    DenseLRDesc d;
+    d.p = P.off;
+    d.out_u = o.U.off;
+    d.out_v = o.Vt.off;
+    d.m = P.rows;
+    d.n = P.cols;
+    d.ld = P.ld;
+    d.cap = o.cap;
+    d.out_slot = o.slot;
+    d.l0 = 32;
+    d.tol = tol;
+    dlr.push_back(d);
+    flops += 8.0 * 5.0 * P.rows * (double)P.cols * std::min(32, o.cap);
+    std::vector<int> rd;
+    reads_of(P, rd);
+    add(OP_DLR, (int)dlr.size() - 1, rd, {o.buf});
   }
   void op_trunc(const TruncDesc& d, int kmax, int rdbuf, int rdbuf2, int wrbuf) {
     trunc.push_back(d);
@@ -457,23 +477,7 @@ struct Builder {
   LR dense_to_lr(const Mat& P, std::vector<Recorder::Tmp>& own) {
     const int m = P.rows, n = P.cols;
     LR o = R.tmp_lr(m, n, std::min(m, n), own);
-    TruncDesc d;
-    d.in_u = P.off;
-    d.in_v = -1;
-    d.ldu = P.ld;
-    d.ldv = n;
-    d.out_u = o.U.off;
-    d.out_v = o.Vt.off;
-    d.m = m;
-    d.n = n;
-    d.k = n;
-    d.k_slot = -1;
-    d.cap = o.cap;
-    d.out_slot = o.slot;
-    d.skip_slot = -1;
-    R.op_trunc(d, std::max(m, n), P.buf, -1, o.buf);
-    R.flops += 4.0 * (4.0 * std::max(m, n) * (double)std::min(m, n) * std::min(m, n) +
-                      22.0 * std::pow(std::min(m, n), 3));
+    R.op_dlr(P, o);
     return o;
   }
 
@@ -764,9 +768,11 @@ struct Builder {
 // ---------------------------------------------------------------------------
 struct Exec {
   int levels = 0, launches = 0;
-  double kind_ms[OP_NKIND] = {0, 0, 0, 0, 0, 0};
-  int kind_launch[OP_NKIND] = {0, 0, 0, 0, 0, 0};
-  int64_t kind_tasks[OP_NKIND] = {0, 0, 0, 0, 0, 0};
+  double trunc_kernel_ms = 0.0;
+  int trunc_launches = 0;
+  double kind_ms[OP_NKIND] = {};
+  int kind_launch[OP_NKIND] = {};
+  int64_t kind_tasks[OP_NKIND] = {};
 };
 
 Exec execute(Recorder& R, zc* arena, int* ranks, int* piv, double* rcond, int* flag,
@@ -783,6 +789,7 @@ Exec execute(Recorder& R, zc* arena, int* ranks, int* piv, double* rcond, int* f
   std::vector<TrsmD> t;
   std::vector<GetrfD> f;
   std::vector<TruncDesc> tr;
+  std::vector<DenseLRDesc> dl;
   struct Grp {
     int kind, start, count, level, kmax;
   };
@@ -797,6 +804,7 @@ Exec execute(Recorder& R, zc* arena, int* ranks, int* piv, double* rcond, int* f
       case OP_CONCAT: gr.start = (int)c.size(); break;
       case OP_TRSM: gr.start = (int)t.size(); break;
       case OP_GETRF: gr.start = (int)f.size(); break;
+      case OP_DLR: gr.start = (int)dl.size(); break;
       default: gr.start = (int)tr.size(); break;
     }
     for (; j < ts.size() && ts[j].kind == kind && ts[j].level == lvl; ++j) {
@@ -807,6 +815,7 @@ Exec execute(Recorder& R, zc* arena, int* ranks, int* piv, double* rcond, int* f
         case OP_CONCAT: c.push_back(R.cat[id]); break;
         case OP_TRSM: t.push_back(R.trsm[id]); break;
         case OP_GETRF: f.push_back(R.getrf[id]); break;
+        case OP_DLR: dl.push_back(R.dlr[id]); break;
         default:
           tr.push_back(R.trunc[id]);
           gr.kmax = std::max(gr.kmax, R.trunc_kmax[id]);
@@ -823,6 +832,9 @@ Exec execute(Recorder& R, zc* arena, int* ranks, int* piv, double* rcond, int* f
   DBuf<TrsmD> dt;
   DBuf<GetrfD> df;
   DBuf<TruncDesc> dtr;
+  DBuf<DenseLRDesc> ddl;
+  ddl.upload(dl, s);
+  DBuf<zc> dlr_scratch;
   dg.upload(g, s);
   de.upload(e, s);
   dc.upload(c, s);
@@ -846,6 +858,7 @@ Exec execute(Recorder& R, zc* arena, int* ranks, int* piv, double* rcond, int* f
     cudaEventCreate(&e0);
     cudaEventCreate(&e1);
   }
+  std::vector<cudaEvent_t> tev;   // (start, stop) pairs around every truncation launch
   for (auto& gr : groups) {
     if (gr.level != lvl) {
       ++ex.levels;
@@ -894,9 +907,27 @@ Exec execute(Recorder& R, zc* arena, int* ranks, int* piv, double* rcond, int* f
       case OP_GETRF:
         k_getrf<<<gr.count, 256, getrf_smem, s>>>(arena, piv, df.p + gr.start, rcond, flag);
         break;
-      default:
-        launch_truncate(arena, ranks, dtr.p + gr.start, gr.count, gr.kmax, tol, ovf, trunc_scratch, s);
+      case OP_DLR: {
+        int mm = 1, nn = 1, cc = 1;
+        for (int i = 0; i < gr.count; ++i) {
+          mm = std::max(mm, dl[gr.start + i].m);
+          nn = std::max(nn, dl[gr.start + i].n);
+          cc = std::max(cc, dl[gr.start + i].cap);
+        }
+        launch_dense_lr(arena, ranks, ddl.p + gr.start, gr.count, mm, nn, cc, dlr_scratch, s);
         break;
+      }
+      default: {
+        cudaEvent_t a, b;
+        cudaEventCreate(&a);
+        cudaEventCreate(&b);
+        cudaEventRecord(a, s);
+        launch_truncate(arena, ranks, dtr.p + gr.start, gr.count, gr.kmax, tol, ovf, trunc_scratch, s);
+        cudaEventRecord(b, s);
+        tev.push_back(a);
+        tev.push_back(b);
+        break;
+      }
     }
     CKL();
     if (prof) {
@@ -913,6 +944,14 @@ Exec execute(Recorder& R, zc* arena, int* ranks, int* piv, double* rcond, int* f
   }
   (void)gemm_tiles;
   CK(cudaStreamSynchronize(s));
+  for (size_t i = 0; i + 1 < tev.size(); i += 2) {
+    float ms = 0;
+    cudaEventElapsedTime(&ms, tev[i], tev[i + 1]);
+    ex.trunc_kernel_ms += ms;
+    ++ex.trunc_launches;
+    cudaEventDestroy(tev[i]);
+    cudaEventDestroy(tev[i + 1]);
+  }
   return ex;
 }
 
@@ -945,6 +984,7 @@ static void hlu_factor_impl(cbie_hlu* F) {
     }
   auto t0 = std::chrono::steady_clock::now();
   Recorder R;
+  R.tol = F->tol;
   R.leaf_end = leaf_end;
   // temporaries before chunk reuse (GiB, CBIE_POOL_GB overrides)
   R.pool_budget = (int64_t)((getenv("CBIE_POOL_GB") ? atof(getenv("CBIE_POOL_GB")) : 8.0) *
@@ -983,8 +1023,24 @@ static void hlu_factor_impl(cbie_hlu* F) {
   CK(cudaMemcpy(&hovf, ovf.p, 8, cudaMemcpyDeviceToHost));
   F->leaf_end = leaf_end;
   F->stat["levels"] = ex.levels;
+  F->stat["trunc_kernel_ms"] = ex.trunc_kernel_ms;
+  F->stat["trunc_launches"] = ex.trunc_launches;
   {
-    const char* nm[OP_NKIND] = {"gemm", "ew", "concat", "trsm", "getrf", "trunc"};
+    // algorithmic bytes of the recompressions actually executed:
+    // B_rc = 16 (m + n) (4k + r), k / r read back from the device rank slots
+    std::vector<int> rk(R.init_ranks.size());
+    CK(cudaMemcpy(rk.data(), F->ranks.p, sizeof(int) * rk.size(), cudaMemcpyDeviceToHost));
+    double bytes = 0.0;
+    for (auto& d : R.trunc) {
+      if (d.skip_slot >= 0 && rk[d.skip_slot] == 0) continue;
+      const double k = d.k_slot >= 0 ? rk[d.k_slot] : d.k;
+      const double r = rk[d.out_slot];
+      bytes += 16.0 * (d.m + d.n) * (4.0 * k + r);
+    }
+    F->stat["trunc_alg_bytes"] = bytes;
+  }
+  {
+    const char* nm[OP_NKIND] = {"gemm", "ew", "concat", "trsm", "getrf", "trunc", "dense_lr"};
     for (int k = 0; k < OP_NKIND; ++k) {
       F->stat[std::string("launch_") + nm[k]] = ex.kind_launch[k];
       F->stat[std::string("tasks_") + nm[k]] = (double)ex.kind_tasks[k];

@@ -80,3 +80,15 @@ struct TruncDesc {
 // kmax >= every min(m,k), min(n,k) (dense mode: min(m,n) and n) in the batch
 void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
                      unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s);
+
+// lowrank.cu: dense block -> (Q, B) by an adaptive randomized range finder
+struct DenseLRDesc {
+  int64_t p;                   // arena offset of P (col-major, ld)
+  int64_t out_u, out_v;        // U m x cap, Vt n x cap
+  int m, n, ld, cap;
+  int out_slot;                // ranks[out_slot] <- l
+  int l0;                      // initial sample size
+  double tol;
+};
+void launch_dense_lr(zc* arena, int* ranks, const DenseLRDesc* d_desc, int nd, int max_m, int max_n,
+                     int max_cap, DBuf<zc>& scratch, cudaStream_t s);

@@ -191,3 +191,139 @@ extern "C" int cbie_lowrank_truncate(cbie_ctx* c, const cbie_c128* U, int m, int
   }
   return CBIE_OK;
 }
+
+// ---------------------------------------------------------------------------
+// Dense -> low rank by an adaptive randomized range finder (one CTA per task).
+// P (m x n, col-major, ld) ~= Q B, Q (m x l) orthonormal, B = Q^H P, with one
+// power iteration; l doubles until the Frobenius residual
+// sqrt(|P|_F^2 - |B|_F^2) <= tol * s0_lb (s0_lb = largest row norm of B, a
+// lower bound of s_0).  Replaces the full SVD of dense updates landing in
+// low-rank targets (hmatrix.py:605-609); the result (U = Q, Vt = B^T, rank l)
+// is truncated exactly by the following add_lowrank recompression.
+// ---------------------------------------------------------------------------
+namespace {
+__device__ __forceinline__ double hash_unit(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t h = a * 0x9E3779B1u ^ (b + 0x7F4A7C15u) * 0x85EBCA77u ^ (c + 0x165667B1u) * 0xC2B2AE3Du;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  h *= 0x297A2D39u;
+  h ^= h >> 15;
+  return (double)h * (2.0 / 4294967296.0) - 1.0;
+}
+
+__global__ void __launch_bounds__(LR_NT) k_dense_lr(zc* arena, int* ranks,
+                                                    const DenseLRDesc* __restrict__ ds,
+                                                    zc* scratch, int64_t scratch_per) {
+  const DenseLRDesc d = ds[blockIdx.x];
+  const int m = d.m, n = d.n, ld = d.ld;
+  const zc* P = arena + d.p;
+  zc* U = arena + d.out_u;   // m x cap
+  zc* Vt = arena + d.out_v;  // n x cap
+  zc* Y = scratch + (int64_t)blockIdx.x * scratch_per;   // m x cap
+  zc* Z = Y + (int64_t)m * d.cap;                          // n x cap
+  __shared__ double red[LR_NW];
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  zc* rd = reinterpret_cast<zc*>(smem_raw);
+  double* kap = reinterpret_cast<double*>(rd + d.cap);
+  double pf2 = 0.0;
+  for (int64_t e = threadIdx.x; e < (int64_t)m * n; e += LR_NT)
+    pf2 += zabs2(P[(e / m) * ld + e % m]);
+  pf2 = block_sum(pf2, red);
+  if (pf2 == 0.0) {
+    if (threadIdx.x == 0) ranks[d.out_slot] = 0;
+    return;
+  }
+  const int full = min(m, n);
+  int l = min(d.l0, full);
+  for (int attempt = 0;; ++attempt) {
+    const bool exact = 2 * l > full;
+    if (exact) l = full;
+    // Y = P * Omega   (exact: Y = P's first l = min(m,n) columns span... use P itself)
+    if (exact && l == n) {
+      for (int64_t e = threadIdx.x; e < (int64_t)m * l; e += LR_NT)
+        Y[e] = P[(e / m) * ld + e % m];
+    } else {
+      for (int64_t e = threadIdx.x; e < (int64_t)m * l; e += LR_NT) {
+        const int i = (int)(e % m), c = (int)(e / m);
+        zc s = zmk(0.0, 0.0);
+        for (int j = 0; j < n; ++j)
+          zfma(s, P[(int64_t)j * ld + i], zmk(hash_unit(j, c, 2 * attempt), hash_unit(j, c, 2 * attempt + 1)));
+        Y[e] = s;
+      }
+      __syncthreads();
+      // one power iteration: Z = P^H Y, Y = P Z
+      for (int64_t e = threadIdx.x; e < (int64_t)n * l; e += LR_NT) {
+        const int j = (int)(e % n), c = (int)(e / n);
+        zc s = zmk(0.0, 0.0);
+        for (int i = 0; i < m; ++i) zfma(s, zconj(P[(int64_t)j * ld + i]), Y[(int64_t)c * m + i]);
+        Z[e] = s;
+      }
+      __syncthreads();
+      for (int64_t e = threadIdx.x; e < (int64_t)m * l; e += LR_NT) {
+        const int i = (int)(e % m), c = (int)(e / m);
+        zc s = zmk(0.0, 0.0);
+        for (int j = 0; j < n; ++j) zfma(s, P[(int64_t)j * ld + i], Z[(int64_t)c * n + j]);
+        Y[e] = s;
+      }
+    }
+    __syncthreads();
+    cta_qr(Y, m, l, m, rd, kap, red);
+    const int lq = min(m, l);
+    // Q = H_0..H_{lq-1} [I; 0] into U
+    for (int64_t e = threadIdx.x; e < (int64_t)m * lq; e += LR_NT) {
+      const int i = (int)(e % m), c = (int)(e / m);
+      U[e] = zmk(i == c ? 1.0 : 0.0, 0.0);
+    }
+    __syncthreads();
+    cta_apply_q(Y, m, lq, m, kap, U, lq, m);
+    // Vt = P^T conj(Q)  (B = Q^H P, Vt = B^T)
+    double bf2 = 0.0;
+    for (int64_t e = threadIdx.x; e < (int64_t)n * lq; e += LR_NT) {
+      const int j = (int)(e % n), c = (int)(e / n);
+      zc s = zmk(0.0, 0.0);
+      for (int i = 0; i < m; ++i) zfma(s, P[(int64_t)j * ld + i], zconj(U[(int64_t)c * m + i]));
+      Vt[e] = s;
+      bf2 += zabs2(s);
+    }
+    bf2 = block_sum(bf2, red);
+    double rowmax = 0.0;
+    for (int c = threadIdx.x; c < lq; c += LR_NT) {
+      double s = 0.0;
+      for (int j = 0; j < n; ++j) s += zabs2(Vt[(int64_t)c * n + j]);
+      rowmax = fmax(rowmax, s);
+    }
+    for (int o = 16; o > 0; o >>= 1) rowmax = fmax(rowmax, __shfl_xor_sync(0xffffffffu, rowmax, o));
+    __syncthreads();
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = rowmax;
+    __syncthreads();
+    double s0 = 0.0;
+    for (int w = 0; w < LR_NW; ++w) s0 = fmax(s0, red[w]);
+    __syncthreads();
+    s0 = sqrt(s0);
+    const double resid = sqrt(fmax(pf2 - bf2, 0.0));
+    if (exact || resid <= d.tol * s0 || 2 * l > d.cap) {
+      if (threadIdx.x == 0) ranks[d.out_slot] = lq;
+      return;
+    }
+    l *= 2;
+    __syncthreads();
+  }
+}
+}  // namespace
+
+void launch_dense_lr(zc* arena, int* ranks, const DenseLRDesc* d_desc, int nd, int max_m, int max_n,
+                     int max_cap, DBuf<zc>& scratch, cudaStream_t s) {
+  if (nd == 0) return;
+  const int64_t per = (int64_t)(max_m + max_n) * max_cap;
+  const int wave = (int)std::max<int64_t>(1, ((int64_t)1 << 30) / (per * (int64_t)sizeof(zc)));
+  const size_t need = (size_t)std::min(wave, nd) * per;
+  if (scratch.n < need) scratch.alloc(need);
+  const size_t smem = (size_t)max_cap * (sizeof(zc) + sizeof(double));
+  CK(cudaFuncSetAttribute(k_dense_lr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  for (int b0 = 0; b0 < nd; b0 += wave) {
+    int nb = std::min(wave, nd - b0);
+    k_dense_lr<<<nb, LR_NT, smem, s>>>(arena, ranks, d_desc + b0, scratch.p, per);
+    CKL();
+  }
+}
