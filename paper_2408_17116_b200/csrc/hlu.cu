@@ -19,6 +19,8 @@
 #include "hmatrix.h"
 
 std::string stats_to_json(const std::map<std::string, double>& m);
+void trunc_prof_enable(bool on, int onesided);
+void trunc_prof_read(unsigned long long* h);
 void hmat_apply(cbie_hmat* H, const zc* d_xp, zc* d_yp, int nrhs, cudaStream_t s);
 
 namespace {
@@ -1013,6 +1015,7 @@ static void hlu_factor_impl(cbie_hlu* F) {
   ovf.alloc(1);
   CK(cudaMemsetAsync(ovf.p, 0, 8, s));
   DBuf<zc> scratch;
+  if (getenv("CBIE_PROFILE")) trunc_prof_enable(true, getenv("CBIE_ONESIDED") ? 1 : 0);
   EvTimer tm;
   tm.start(s);
   Exec ex = execute(R, F->arena.p, F->ranks.p, F->piv.p, F->rcond.p, flag.p, ovf.p, scratch, F->tol, s);
@@ -1024,6 +1027,13 @@ static void hlu_factor_impl(cbie_hlu* F) {
   F->leaf_end = leaf_end;
   F->stat["levels"] = ex.levels;
   F->stat["trunc_kernel_ms"] = ex.trunc_kernel_ms;
+  if (getenv("CBIE_PROFILE")) {
+    unsigned long long h[6] = {0, 0, 0, 0, 0, 0};
+    trunc_prof_read(h);
+    const char* nm[4] = {"qr", "core", "svd", "apply"};
+    for (int i = 0; i < 4; ++i) F->stat[std::string("trunc_cyc_") + nm[i]] = h[4] ? (double)h[i] / h[4] : 0;
+    F->stat["trunc_mean_sweeps"] = h[4] ? (double)h[5] / h[4] : 0;
+  }
   F->stat["trunc_launches"] = ex.trunc_launches;
   {
     // algorithmic bytes of the recompressions actually executed:
@@ -1031,11 +1041,30 @@ static void hlu_factor_impl(cbie_hlu* F) {
     std::vector<int> rk(R.init_ranks.size());
     CK(cudaMemcpy(rk.data(), F->ranks.p, sizeof(int) * rk.size(), cudaMemcpyDeviceToHost));
     double bytes = 0.0;
+    int hist[7] = {0, 0, 0, 0, 0, 0, 0};
+    double ksum = 0.0, rsum = 0.0;
+    int nexec = 0;
     for (auto& d : R.trunc) {
       if (d.skip_slot >= 0 && rk[d.skip_slot] == 0) continue;
       const double k = d.k_slot >= 0 ? rk[d.k_slot] : d.k;
       const double r = rk[d.out_slot];
       bytes += 16.0 * (d.m + d.n) * (4.0 * k + r);
+      const int kb = k <= 16 ? 0 : k <= 32 ? 1 : k <= 64 ? 2 : k <= 128 ? 3 : k <= 256 ? 4 : 5;
+      hist[kb]++;
+      ksum += k;
+      rsum += r;
+      ++nexec;
+    }
+    const char* hn[6] = {"k_le16", "k_le32", "k_le64", "k_le128", "k_le256", "k_gt256"};
+    for (int i = 0; i < 6; ++i) F->stat[std::string("trunc_") + hn[i]] = hist[i];
+    F->stat["trunc_mean_k"] = nexec ? ksum / nexec : 0.0;
+    F->stat["trunc_mean_r"] = nexec ? rsum / nexec : 0.0;
+    {
+      std::vector<int> dk;
+      for (auto& d : R.dlr) dk.push_back(rk[d.out_slot]);
+      double s = 0;
+      for (int v : dk) s += v;
+      F->stat["dense_lr_mean_l"] = dk.empty() ? 0.0 : s / dk.size();
     }
     F->stat["trunc_alg_bytes"] = bytes;
   }

@@ -11,11 +11,16 @@
 
 namespace {
 
+constexpr int SMEM_J = 64;   // cores up to 64 x 64 run the Jacobi SVD in shared memory
+__device__ int prof_onesided_flag_dev = 0;
+
 __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
                                                     const TruncDesc* __restrict__ descs,
                                                     zc* scratch, int64_t scratch_per, int KS,
-                                                    double tol, unsigned long long* overflow) {
+                                                    double tol, unsigned long long* overflow,
+                                                    unsigned long long* prof) {
   const TruncDesc d = descs[blockIdx.x];
+  long long tc0 = clock64();
   __shared__ double red[LR_NW];
   __shared__ int flag;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -44,6 +49,7 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
   const int ldu = d.ldu, ldv = d.ldv;
   cta_qr(U, m, k, ldu, rd1, kap1, red);
   if (!ident) cta_qr(Vt, n, k, ldv, rd2, kap2, red);
+  long long tc1 = clock64();
   // M = R1 R2^T (R2 = I for the dense mode)
   for (int e = threadIdx.x; e < kk1 * kk2; e += LR_NT) {
     const int a = e % kk1, b = e / kk1;
@@ -60,14 +66,35 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
     M[(int64_t)b * kk1 + a] = s;
   }
   __syncthreads();
-  cta_jacobi(M, kk1, kk2, kk1, W, kk2, &flag);
-  // singular values and descending order (stable)
-  for (int c = threadIdx.x; c < kk2; c += LR_NT) {
-    double s = 0.0;
-    for (int i = 0; i < kk1; ++i) s += zabs2(M[(int64_t)c * kk1 + i]);
-    sig[c] = sqrt(s);
+  long long tc2 = clock64();
+  int sweeps = 0;
+  if (kk1 <= SMEM_J && kk2 <= SMEM_J) {
+    // one-sided Jacobi with M and W resident in shared memory
+    zc* Ms = reinterpret_cast<zc*>(order + KS);
+    Ms = reinterpret_cast<zc*>((reinterpret_cast<uintptr_t>(Ms) + 15) & ~uintptr_t(15));
+    zc* Ws = Ms + SMEM_J * SMEM_J;
+    for (int e = threadIdx.x; e < kk1 * kk2; e += LR_NT) Ms[e] = M[e];
+    __syncthreads();
+    sweeps = cta_jacobi(Ms, kk1, kk2, kk1, Ws, kk2, &flag, red);
+    for (int c = threadIdx.x; c < kk2; c += LR_NT) {
+      double sq = 0.0;
+      for (int i = 0; i < kk1; ++i) sq += zabs2(Ms[c * kk1 + i]);
+      sig[c] = sqrt(sq);
+    }
+    for (int e = threadIdx.x; e < kk1 * kk2; e += LR_NT) M[e] = Ms[e];
+    for (int e = threadIdx.x; e < kk2 * kk2; e += LR_NT) W[e] = Ws[e];
+    __syncthreads();
+  } else {
+    sweeps = cta_jacobi(M, kk1, kk2, kk1, W, kk2, &flag, red);
+    // singular values and descending order (stable)
+    for (int c = threadIdx.x; c < kk2; c += LR_NT) {
+      double s = 0.0;
+      for (int i = 0; i < kk1; ++i) s += zabs2(M[(int64_t)c * kk1 + i]);
+      sig[c] = sqrt(s);
+    }
+    __syncthreads();
   }
-  __syncthreads();
+  long long tc3 = clock64();
   for (int c = threadIdx.x; c < kk2; c += LR_NT) {
     int pos = 0;
     for (int o = 0; o < kk2; ++o)
@@ -101,10 +128,34 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
   __syncthreads();
   cta_apply_q(U, m, kk1, ldu, kap1, Uo, r, m);
   if (!ident) cta_apply_q(Vt, n, kk2, ldv, kap2, Vo, r, n);
-  if (threadIdx.x == 0) ranks[d.out_slot] = r;
+  if (threadIdx.x == 0) {
+    ranks[d.out_slot] = r;
+    if (prof) {
+      long long tc4 = clock64();
+      atomicAdd(prof + 0, (unsigned long long)(tc1 - tc0));
+      atomicAdd(prof + 1, (unsigned long long)(tc2 - tc1));
+      atomicAdd(prof + 2, (unsigned long long)(tc3 - tc2));
+      atomicAdd(prof + 3, (unsigned long long)(tc4 - tc3));
+      atomicAdd(prof + 4, 1ull);
+      atomicAdd(prof + 5, (unsigned long long)sweeps);
+    }
+  }
 }
 
 }  // namespace
+
+unsigned long long* g_trunc_prof = nullptr;   // debug cycle counters (CBIE_PROFILE)
+
+void trunc_prof_enable(bool on, int onesided) {
+  if (on && !g_trunc_prof) {
+    cudaMalloc(&g_trunc_prof, 8 * sizeof(unsigned long long));
+    cudaMemset(g_trunc_prof, 0, 8 * sizeof(unsigned long long));
+  }
+  cudaMemcpyToSymbol(prof_onesided_flag_dev, &onesided, sizeof(int));
+}
+void trunc_prof_read(unsigned long long* h) {
+  if (g_trunc_prof) cudaMemcpy(h, g_trunc_prof, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+}
 
 void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
                      unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s) {
@@ -115,13 +166,14 @@ void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int
   const int wave = (int)std::max<int64_t>(1, ((int64_t)1 << 30) / (per * (int64_t)sizeof(zc)));
   const size_t need = (size_t)std::min(wave, nd) * per;
   if (scratch.n < need) scratch.alloc(need);
-  const size_t smem = (size_t)kmax * (2 * sizeof(zc) + 3 * sizeof(double) + sizeof(int));
-  if (smem > 200 * 1024) throw cbie_error(CBIE_EINVALID, "truncation dimension too large");
+  const size_t smem = (size_t)kmax * (2 * sizeof(zc) + 3 * sizeof(double) + sizeof(int)) + 16 +
+                      (size_t)SMEM_J * SMEM_J * 2 * sizeof(zc);
+  if (smem > 220 * 1024) throw cbie_error(CBIE_EINVALID, "truncation dimension too large");
   CK(cudaFuncSetAttribute(k_truncate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (int b0 = 0; b0 < nd; b0 += wave) {
     int nb = std::min(wave, nd - b0);
     k_truncate<<<nb, LR_NT, smem, s>>>(arena, ranks, d_desc + b0, scratch.p, per, kmax, tol,
-                                       overflow);
+                                       overflow, g_trunc_prof);
     CKL();
   }
 }

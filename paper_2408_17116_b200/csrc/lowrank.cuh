@@ -8,7 +8,7 @@
 #pragma once
 #include "common.cuh"
 
-constexpr int LR_NT = 256;
+constexpr int LR_NT = 512;
 constexpr int LR_NW = LR_NT / 32;
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -97,8 +97,15 @@ __device__ __forceinline__ void cta_apply_q(const zc* A, int m, int kk, int ld, 
 
 // One-sided Jacobi: M (p x q, ldm) <- M W with orthogonal columns, W (q x q,
 // ldw) unitary (initialised here to I).  Returns the number of sweeps.
-__device__ __forceinline__ int cta_jacobi(zc* M, int p, int q, int ldm, zc* W, int ldw, int* flag) {
+__device__ __forceinline__ int cta_jacobi(zc* M, int p, int q, int ldm, zc* W, int ldw, int* flag,
+                                          double* red) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // columns below 1e-12 |M|_F are numerical noise for every truncation tolerance
+  // used here (>= 1e-8); rotating them only chases rounding, so they are skipped
+  double f2 = 0.0;
+  for (int e = threadIdx.x; e < p * q; e += LR_NT) f2 += zabs2(M[(int64_t)(e / p) * ldm + e % p]);
+  f2 = block_sum(f2, red);
+  const double floor2 = 1e-24 * f2;
   for (int e = threadIdx.x; e < q * q; e += LR_NT) {
     int i = e % q, j = e / q;
     W[(int64_t)j * ldw + i] = zmk(i == j ? 1.0 : 0.0, 0.0);
@@ -107,7 +114,7 @@ __device__ __forceinline__ int cta_jacobi(zc* M, int p, int q, int ldm, zc* W, i
   if (q < 2) return 0;
   const int qe = q + (q & 1);
   int sweep = 0;
-  for (; sweep < 60; ++sweep) {
+  for (; sweep < 40; ++sweep) {
     if (threadIdx.x == 0) *flag = 0;
     __syncthreads();
     for (int r = 0; r < qe - 1; ++r) {
@@ -130,7 +137,7 @@ __device__ __forceinline__ int cta_jacobi(zc* M, int p, int q, int ldm, zc* W, i
         be = warp_sum(be);
         ga = warp_sum(ga);
         const double g = sqrt(zabs2(ga));
-        if (!(g > 1e-15 * sqrt(al * be)) || g == 0.0) continue;
+        if (!(g > 1e-14 * sqrt(al * be)) || g == 0.0 || fmin(al, be) < floor2) continue;
         const double zeta = (be - al) / (2.0 * g);
         const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
         const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
@@ -150,6 +157,91 @@ __device__ __forceinline__ int cta_jacobi(zc* M, int p, int q, int ldm, zc* W, i
           wy[i] = zadd(zmul(se, xi), zscale(yi, cs));
         }
         if (lane == 0) *flag = 1;
+      }
+      __syncthreads();
+    }
+    if (*flag == 0) break;
+    __syncthreads();
+  }
+  return sweep;
+}
+
+// Hermitian two-sided Jacobi on the Gram matrix G = M^H M (q x q, in shared
+// memory): G <- J^H G J until off-diagonal |g_pq| <= 1e-15 sqrt(g_pp g_qq),
+// W <- W J (W q x q, shared, initialised to I).  Rounds use the parallel
+// round-robin ordering; each round = rotation parameters (one thread per
+// pair), column update, row update.  Returns sweeps.
+__device__ __forceinline__ int cta_herm_jacobi(zc* G, zc* W, int q, double* cs_c, zc* cs_s,
+                                               int* pa, int* pb, int* flag) {
+  for (int e = threadIdx.x; e < q * q; e += LR_NT) {
+    const int i = e % q, j = e / q;
+    W[j * q + i] = zmk(i == j ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+  if (q < 2) return 0;
+  const int qe = q + (q & 1), np = qe / 2;
+  int sweep = 0;
+  for (; sweep < 60; ++sweep) {
+    if (threadIdx.x == 0) *flag = 0;
+    __syncthreads();
+    for (int r = 0; r < qe - 1; ++r) {
+      // (1) rotation parameters
+      for (int pi = threadIdx.x; pi < np; pi += LR_NT) {
+        const int xa = pi, xb = qe - 1 - pi;
+        int a = xa == 0 ? 0 : ((xa - 1 + r) % (qe - 1)) + 1;
+        int b = xb == 0 ? 0 : ((xb - 1 + r) % (qe - 1)) + 1;
+        if (a > b) {
+          const int t = a;
+          a = b;
+          b = t;
+        }
+        pa[pi] = a;
+        pb[pi] = b;
+        cs_c[pi] = -1.0;   // inactive
+        cs_s[pi] = zmk(0.0, 0.0);
+        if (b >= q) continue;
+        const double ga = G[a * q + a].x, gb = G[b * q + b].x;
+        const zc g = G[b * q + a];   // G[a][b] (column-major: col b, row a)
+        const double ag = sqrt(zabs2(g));
+        if (!(ag > 1e-15 * sqrt(fabs(ga * gb))) || ag == 0.0) continue;
+        const double zeta = (gb - ga) / (2.0 * ag);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double c = 1.0 / sqrt(1.0 + t * t);
+        cs_c[pi] = c;
+        // s e^{-i phi} with e^{i phi} = g / |g|
+        cs_s[pi] = zmk(c * t * g.x / ag, -c * t * g.y / ag);
+        *flag = 1;
+      }
+      __syncthreads();
+      // (2) columns: G J and W J.  J = [[c, s], [-s e^{-i phi}, c e^{-i phi}]]
+      //     col a' = c col a - s e^{-i phi} col b ;  col b' = s col a + c e^{-i phi} col b
+      for (int e = threadIdx.x; e < np * q * 2; e += LR_NT) {
+        const int which = e / (np * q);        // 0: G, 1: W
+        const int pi = (e / q) % np, i = e % q;
+        const double c = cs_c[pi];
+        if (c < 0.0) continue;
+        const zc se = cs_s[pi];                 // s e^{-i phi}
+        const double s = sqrt(zabs2(se));
+        const zc eph = s > 0 ? zmk(se.x / s, se.y / s) : zmk(1.0, 0.0);   // e^{-i phi}
+        zc* X = which ? W : G;
+        const int a = pa[pi], b = pb[pi];
+        const zc xa = X[a * q + i], xb = X[b * q + i];
+        X[a * q + i] = zsub(zscale(xa, c), zmul(se, xb));
+        X[b * q + i] = zadd(zscale(xa, s), zmul(zscale(eph, c), xb));
+      }
+      __syncthreads();
+      // (3) rows: J^H G.  row a' = c row a - s e^{+i phi} row b ; row b' = s row a + c e^{+i phi} row b
+      for (int e = threadIdx.x; e < np * q; e += LR_NT) {
+        const int pi = e / q, j = e % q;
+        const double c = cs_c[pi];
+        if (c < 0.0) continue;
+        const zc se = zconj(cs_s[pi]);          // s e^{+i phi}
+        const double s = sqrt(zabs2(se));
+        const zc eph = s > 0 ? zmk(se.x / s, se.y / s) : zmk(1.0, 0.0);
+        const int a = pa[pi], b = pb[pi];
+        const zc ya = G[j * q + a], yb = G[j * q + b];
+        G[j * q + a] = zsub(zscale(ya, c), zmul(se, yb));
+        G[j * q + b] = zadd(zscale(ya, s), zmul(zscale(eph, c), yb));
       }
       __syncthreads();
     }
