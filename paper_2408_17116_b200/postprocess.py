@@ -1,0 +1,72 @@
+"""Far field and bistatic RCS from a solution vector (host numpy; used for the
+RCS parity check of BASELINE.json, not part of the accelerated path).
+Restates postprocess.py:30-233 (density_grids, _patch_tables native branch,
+far_field, rcs_cut)."""
+
+from __future__ import annotations
+
+import numpy as np
+
+from . import geometry as geo
+
+
+def _fejer_weights(n):
+    th = (2.0 * np.arange(n) + 1.0) * np.pi / (2.0 * n)
+    w = np.ones(n)
+    for m in range(1, n // 2 + 1):
+        w -= 2.0 * np.cos(2 * m * th) / (4 * m * m - 1)
+    return (2.0 / n) * w
+
+
+def _node_diff(n):
+    x = geo.fejer_nodes(n)
+    S = geo._vander(x, n)
+    return S @ geo._dcoef(n) @ geo._analysis(n)
+
+
+def radiation_tables(gen, solution):
+    """pos, w (a_u F^u + a_v F^v), w div F per node; (M tables for Muller)."""
+    C = gen.C
+    nu, nv = gen.nu, gen.nv
+    npatch = len(gen.patches)
+    wgt = (_fejer_weights(nv)[:, None] * _fejer_weights(nu)[None, :]).ravel()
+    Du, Dv = _node_diff(nu), _node_diff(nv)
+    F = solution.reshape(npatch, nv * nu, C)
+    au = gen.a_u.reshape(npatch, nv * nu, 3)
+    av = gen.a_v.reshape(npatch, nv * nu, 3)
+    out = []
+    for cu, cv in ((0, 1), (2, 3))[: C // 2]:
+        vec = wgt[None, :, None] * (F[:, :, cu, None] * au + F[:, :, cv, None] * av)
+        gu = F[:, :, cu].reshape(npatch, nv, nu)          # [patch][k][l]
+        gv = F[:, :, cv].reshape(npatch, nv, nu)
+        du = np.einsum("pkl,ml->pkm", gu, Du).reshape(npatch, -1)
+        dv = np.einsum("pkl,nk->pnl", gv, Dv).reshape(npatch, -1)
+        out.append((vec.reshape(-1, 3), (wgt[None, :] * (du + dv)).reshape(-1)))
+    return gen.pos, out
+
+
+def far_field(problem, gen, solution, theta, phi):
+    med = problem.spec.outer
+    k, omega = med.k, med.omega
+    pos, tabs = radiation_tables(gen, solution)
+    rhat = np.stack([np.sin(theta) * np.cos(phi), np.sin(theta) * np.sin(phi), np.cos(theta)], 1)
+    phase = np.exp(1j * k * (rhat @ pos.T))
+    wJ, wdJ = tabs[0]
+    F = -(1.0 / (4 * np.pi)) * (1j * omega * med.mu * (phase @ wJ)
+                                + (k / (omega * med.eps)) * rhat * (phase @ wdJ)[:, None])
+    if len(tabs) > 1:
+        F = F + (1.0 / (4 * np.pi)) * 1j * k * np.cross(rhat, phase @ tabs[1][0])
+    return F - rhat * np.sum(F * rhat, axis=1)[:, None], rhat
+
+
+def rcs_cut(problem, gen, solution, phi_deg, theta_deg):
+    """sigma (m^2) and sigma (dBsm) over theta at fixed phi (postprocess.py:215-233)."""
+    theta = np.deg2rad(np.asarray(theta_deg, float))
+    phi = np.full_like(theta, np.deg2rad(phi_deg))
+    F, _ = far_field(problem, gen, solution, theta, phi)
+    that = np.stack([np.cos(theta) * np.cos(phi), np.cos(theta) * np.sin(phi), -np.sin(theta)], 1)
+    phat = np.stack([-np.sin(phi), np.cos(phi), np.zeros_like(phi)], 1)
+    et = np.sum(F * that, axis=1)
+    ep = np.sum(F * phat, axis=1)
+    sigma = 4 * np.pi * (np.abs(et) ** 2 + np.abs(ep) ** 2) / problem.excitation.amplitude ** 2
+    return sigma, 10.0 * np.log10(np.maximum(sigma, 1e-300))
