@@ -414,7 +414,14 @@ static void hmatrix_build(cbie_hmat* H, int n_leaf) {
   ovf.alloc(1);
   CK(cudaMemsetAsync(ovf.p, 0, 8, s));
   DBuf<zc> scratch;
-  launch_truncate(H->arena.p, H->rank.p, dtd.p, (int)td.size(), kmax, H->tol, ovf.p, scratch, s);
+  int kcm = 1, mnm = 1;
+  for (auto& d : td) {
+    kcm = std::max(kcm, d.cap + 1);
+    mnm = std::max(mnm, std::max(d.m, d.n));
+  }
+  for (auto& a : aca) kcm = std::max(kcm, a.kmax + 1);
+  launch_truncate(H->arena.p, H->rank.p, dtd.p, (int)td.size(), kmax, H->tol, ovf.p, scratch, s,
+                  kcm, mnm);
   const double trunc_ms = tm.stop_ms(s);
   // ---- demotion: RankOverflow -> dense leaf (hmatrix.py:259-263) ----
   std::vector<int> demote;

@@ -924,7 +924,14 @@ Exec execute(Recorder& R, zc* arena, int* ranks, int* piv, double* rcond, int* f
         cudaEventCreate(&a);
         cudaEventCreate(&b);
         cudaEventRecord(a, s);
-        launch_truncate(arena, ranks, dtr.p + gr.start, gr.count, gr.kmax, tol, ovf, trunc_scratch, s);
+        int kcm = 1, mnm = 1;
+        for (int i = 0; i < gr.count; ++i) {
+          const TruncDesc& td = tr[gr.start + i];
+          kcm = std::max(kcm, td.k);
+          mnm = std::max(mnm, std::max(td.m, td.n));
+        }
+        launch_truncate(arena, ranks, dtr.p + gr.start, gr.count, gr.kmax, tol, ovf, trunc_scratch, s,
+                        kcm, mnm);
         cudaEventRecord(b, s);
         tev.push_back(a);
         tev.push_back(b);

@@ -78,8 +78,10 @@ struct TruncDesc {
   int out_slot;                // ranks[out_slot] <- r
 };
 // kmax >= every min(m,k), min(n,k) (dense mode: min(m,n) and n) in the batch
+// kc_max / mn_max: largest concatenated capacity and max(m, n) (randomized-path scratch)
 void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
-                     unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s);
+                     unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s,
+                     int kc_max = 0, int mn_max = 0);
 
 // lowrank.cu: dense block -> (Q, B) by an adaptive randomized range finder
 struct DenseLRDesc {

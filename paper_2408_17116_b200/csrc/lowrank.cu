@@ -14,6 +14,152 @@ namespace {
 constexpr int SMEM_J = 64;   // cores up to 64 x 64 run the Jacobi SVD in shared memory
 __device__ int prof_onesided_flag_dev = 0;
 
+constexpr int KEXACT = 64;    // concatenated ranks above this use the randomized path
+constexpr int RL0 = 32;       // initial sketch size
+
+__device__ __forceinline__ double hash_u(uint32_t a, uint32_t b, uint32_t c) {
+  uint32_t h = a * 0x9E3779B1u ^ (b + 0x7F4A7C15u) * 0x85EBCA77u ^ (c + 0x165667B1u) * 0xC2B2AE3Du;
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  h *= 0x297A2D39u;
+  h ^= h >> 15;
+  return (double)h * (2.0 / 4294967296.0) - 1.0;
+}
+
+// C (rows x l, col-major ldc) = op(A) * B where op selects how A (given col-major
+// with leading dimension lda) is read: mode 0: C = A B (A rows x kk); mode 1:
+// C = A^T B (A kk x rows); mode 2: C = A^H B; mode 3: C = conj(A) B.
+__device__ __forceinline__ void cta_gemm_small(zc* C, int ldc, const zc* A, int lda, const zc* B,
+                                               int ldb, int rows, int kk, int l, int mode) {
+  for (int64_t e = threadIdx.x; e < (int64_t)rows * l; e += LR_NT) {
+    const int i = (int)(e % rows), c = (int)(e / rows);
+    zc s = zmk(0.0, 0.0);
+    const zc* b = B + (int64_t)c * ldb;
+    if (mode == 0) {
+      for (int a = 0; a < kk; ++a) zfma(s, A[(int64_t)a * lda + i], b[a]);
+    } else if (mode == 1) {
+      const zc* ai = A + (int64_t)i * lda;
+      for (int a = 0; a < kk; ++a) zfma(s, ai[a], b[a]);
+    } else if (mode == 2) {
+      const zc* ai = A + (int64_t)i * lda;
+      for (int a = 0; a < kk; ++a) zfma(s, zconj(ai[a]), b[a]);
+    } else {
+      for (int a = 0; a < kk; ++a) zfma(s, zconj(A[(int64_t)a * lda + i]), b[a]);
+    }
+    C[e] = s;
+  }
+  __syncthreads();
+}
+
+// Randomized recompression of A = U V (U m x k, V = Vt^T), k > KEXACT:
+// adaptive range finder with one power iteration, exact SVD of the l x l core.
+// Accepts when the sketch shows >= 4 singular values below tol * s0, else
+// doubles l (<= SMEM_J).  Returns false if l would exceed SMEM_J.
+__device__ bool rand_truncate(const TruncDesc& d, zc* arena, int* ranks, int k, zc* sc,
+                              int64_t scper, double tol, zc* rdv, double* kapv, double* sig,
+                              int* order, zc* Ms, zc* Ws, double* red, int* flag,
+                              unsigned long long* overflow) {
+  const int m = d.m, n = d.n;
+  const zc* U = arena + d.in_u;
+  const zc* Vt = arena + d.in_v;
+  const int lmax = min(SMEM_J, min(m, n));
+  int l = min(RL0, lmax);
+  zc* Y = sc;                         // m x lmax  (becomes Q)
+  zc* Z = Y + (int64_t)m * SMEM_J;    // n x lmax  (becomes Bt, then its reflectors)
+  zc* T = Z + (int64_t)n * SMEM_J;    // k x lmax
+  zc* Om = T + (int64_t)k * SMEM_J;   // n x lmax  (Omega, then Q2 output staging)
+  (void)scper;
+  for (int attempt = 0;; ++attempt) {
+    for (int64_t e = threadIdx.x; e < (int64_t)n * l; e += LR_NT)
+      Om[e] = zmk(hash_u((uint32_t)(e % n), (uint32_t)(e / n), 2 * attempt),
+                  hash_u((uint32_t)(e % n), (uint32_t)(e / n), 2 * attempt + 1));
+    __syncthreads();
+    cta_gemm_small(T, k, Vt, d.ldv, Om, n, k, n, l, 1);   // T = Vt^T Om      (k x l)
+    cta_gemm_small(Y, m, U, d.ldu, T, k, m, k, l, 0);     // Y = U T          (m x l)
+    // no power iteration: without re-orthonormalisation (A A^H)^q A Omega loses the
+    // singular directions below eps^(1/(2q+1)) s0, which the truncation needs; a
+    // 16-column oversampling margin is used instead
+    for (int q = 0; q < 0; ++q) {
+      cta_gemm_small(T, k, U, d.ldu, Y, m, k, m, l, 2);   // T = U^H Y        (k x l)
+      cta_gemm_small(Z, n, Vt, d.ldv, T, k, n, k, l, 3);  // Z = conj(Vt) T   (n x l)
+      cta_gemm_small(T, k, Vt, d.ldv, Z, n, k, n, l, 1);  // T = Vt^T Z       (k x l)
+      cta_gemm_small(Y, m, U, d.ldu, T, k, m, k, l, 0);   // Y = U T          (m x l)
+    }
+    cta_qr(Y, m, l, m, rdv, kapv, red);
+    // explicit Q (m x l) into Om (reuse, needs m <= n? use Z's region? ) -> stage in Om2
+    zc* Q = Om + (int64_t)n * SMEM_J;  // m x l (extra region)
+    for (int64_t e = threadIdx.x; e < (int64_t)m * l; e += LR_NT) {
+      const int i = (int)(e % m), c = (int)(e / m);
+      Q[e] = zmk(i == c ? 1.0 : 0.0, 0.0);
+    }
+    __syncthreads();
+    cta_apply_q(Y, m, l, m, kapv, Q, l, m);
+    // T = U^H Q (k x l);  Bt = Vt T (n x l)  [B = Q^H U V, Bt = B^T = Vt (U^T conj Q) = Vt conj(T)]
+    cta_gemm_small(T, k, U, d.ldu, Q, m, k, m, l, 2);
+    for (int64_t e = threadIdx.x; e < (int64_t)k * l; e += LR_NT) T[e] = zconj(T[e]);
+    __syncthreads();
+    cta_gemm_small(Z, n, Vt, d.ldv, T, k, n, k, l, 0);    // Z = Bt (n x l)
+    // exact SVD of B = R2^T Q2^T:  QR(Bt) = Q2 R2, core M = R2^T (l x l)
+    cta_qr(Z, n, l, n, rdv, kapv, red);
+    for (int e = threadIdx.x; e < l * l; e += LR_NT) {
+      const int a = e % l, b = e / l;   // M[a][b] = R2[b][a]
+      Ms[e] = a == b ? rdv[a] : (a > b ? Z[(int64_t)a * n + b] : zmk(0.0, 0.0));
+    }
+    __syncthreads();
+    cta_jacobi(Ms, l, l, l, Ws, l, flag, red);
+    for (int c = threadIdx.x; c < l; c += LR_NT) {
+      double sq = 0.0;
+      for (int i = 0; i < l; ++i) sq += zabs2(Ms[c * l + i]);
+      sig[c] = sqrt(sq);
+    }
+    __syncthreads();
+    for (int c = threadIdx.x; c < l; c += LR_NT) {
+      int pos = 0;
+      for (int o = 0; o < l; ++o)
+        if (sig[o] > sig[c] || (sig[o] == sig[c] && o < c)) ++pos;
+      order[pos] = c;
+    }
+    __syncthreads();
+    const double s0 = sig[order[0]];
+    int r = 0;
+    if (s0 > 0.0) {
+      for (int c = 0; c < l; ++c)
+        if (sig[c] > tol * s0) ++r;
+      r = max(r, 1);
+    }
+    if (!(r <= l - 16)) {   // sketch too small: grow, or give up (exact path)
+      if (l >= lmax) return false;
+      l = min(2 * l, lmax);
+      __syncthreads();
+      continue;
+    }
+    if (r > d.cap) {
+      if (threadIdx.x == 0) atomicAdd(overflow, 1ull);
+      r = d.cap;
+    }
+    // U' = Q (M W)[:, order[:r]]   (m x r)
+    zc* Uo = arena + d.out_u;
+    zc* Vo = arena + d.out_v;
+    for (int64_t e = threadIdx.x; e < (int64_t)m * r; e += LR_NT) {
+      const int i = (int)(e % m), c = (int)(e / m);
+      const zc* mc = Ms + order[c] * l;
+      zc s = zmk(0.0, 0.0);
+      for (int a = 0; a < l; ++a) zfma(s, Q[(int64_t)a * m + i], mc[a]);
+      Uo[e] = s;
+    }
+    // Vt' = Q2 [conj(W[:, order[:r]]); 0]
+    for (int64_t e = threadIdx.x; e < (int64_t)n * r; e += LR_NT) {
+      const int j = (int)(e % n), c = (int)(e / n);
+      Vo[e] = j < l ? zconj(Ws[order[c] * l + j]) : zmk(0.0, 0.0);
+    }
+    __syncthreads();
+    cta_apply_q(Z, n, l, n, kapv, Vo, r, n);
+    if (threadIdx.x == 0) ranks[d.out_slot] = r;
+    return true;
+  }
+}
+
 __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
                                                     const TruncDesc* __restrict__ descs,
                                                     zc* scratch, int64_t scratch_per, int KS,
@@ -38,6 +184,16 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
   if (k <= 0 || m == 0 || n == 0) {
     if (threadIdx.x == 0) ranks[d.out_slot] = 0;
     return;
+  }
+  if (!ident && k > KEXACT && min(m, n) > 2 * RL0) {
+    zc* Ms = reinterpret_cast<zc*>(order + KS);
+    Ms = reinterpret_cast<zc*>((reinterpret_cast<uintptr_t>(Ms) + 15) & ~uintptr_t(15));
+    zc* Ws = Ms + SMEM_J * SMEM_J;
+    zc* sc = scratch + (int64_t)blockIdx.x * scratch_per;
+    if (rand_truncate(d, arena, ranks, k, sc, scratch_per, tol, rd1, kap1, sig, order, Ms, Ws, red,
+                      &flag, overflow))
+      return;
+    __syncthreads();
   }
   zc* U = arena + d.in_u;
   zc* Vt = ident ? nullptr : arena + d.in_v;
@@ -158,10 +314,12 @@ void trunc_prof_read(unsigned long long* h) {
 }
 
 void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
-                     unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s) {
+                     unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, int kc_max,
+                     int mn_max) {
   if (nd == 0) return;
-  kmax = std::max(kmax, 1);
-  const int64_t per = (int64_t)kmax * kmax * 2;
+  kmax = std::max(std::max(kmax, 1), SMEM_J);
+  const int64_t per = std::max<int64_t>((int64_t)kmax * kmax * 2,
+                                        (int64_t)SMEM_J * (4 * (int64_t)mn_max + kc_max + 1));
   // waves keep the Jacobi scratch bounded (<= 1 GiB); the buffer is reused across calls
   const int wave = (int)std::max<int64_t>(1, ((int64_t)1 << 30) / (per * (int64_t)sizeof(zc)));
   const size_t need = (size_t)std::min(wave, nd) * per;
@@ -224,7 +382,7 @@ extern "C" int cbie_lowrank_truncate(cbie_ctx* c, const cbie_c128* U, int m, int
     CK(cudaMemsetAsync(ovf.p, 0, 8, s));
     DBuf<zc> scratch;
     const int kmax = dense ? std::max(m, n) : std::min(k, std::max(m, n));
-    launch_truncate(ar.p, ranks.p, dd.p, 1, kmax, tol, ovf.p, scratch, s);
+    launch_truncate(ar.p, ranks.p, dd.p, 1, kmax, tol, ovf.p, scratch, s, k, std::max(m, n));
     int rr = 0;
     CK(cudaMemcpyAsync(&rr, ranks.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     std::vector<zc> out((size_t)(m + n) * cap);
