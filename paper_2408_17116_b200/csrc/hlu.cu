@@ -34,9 +34,19 @@ struct Mat {
   int rows = 0, cols = 0;      // capacities / static sizes
   int rslot = -1, cslot = -1;  // dynamic dims
   int buf = -1;                // dependency buffer id
+  int rid = -1;                // region of the buffer (-1 = whole buffer)
+  int nr0 = 0, nr1 = 1 << 30, nc0 = 0, nc1 = 1 << 30;   // rectangle in the region's storage
   View view() const { return View{off, ld, tr}; }
   DimR R() const { return DimR{rows, rslot}; }
   DimR Cc() const { return DimR{cols, cslot}; }
+  void base(int b, int region, int r, int c) {
+    buf = b;
+    rid = region;
+    nr0 = 0;
+    nr1 = r;
+    nc0 = 0;
+    nc1 = c;
+  }
   Mat sub(int r0, int nr, int c0, int nc) const {
     Mat s = *this;
     s.off = tr ? off + (int64_t)r0 * ld + c0 : off + (int64_t)c0 * ld + r0;
@@ -44,6 +54,17 @@ struct Mat {
     if (!(c0 == 0 && nc == cols)) s.cslot = -1;
     s.rows = nr;
     s.cols = nc;
+    if (!tr) {
+      s.nr0 = nr0 + r0;
+      s.nr1 = s.nr0 + nr;
+      s.nc0 = nc0 + c0;
+      s.nc1 = s.nc0 + nc;
+    } else {
+      s.nc0 = nc0 + r0;
+      s.nc1 = s.nc0 + nr;
+      s.nr0 = nr0 + c0;
+      s.nr1 = s.nr0 + nc;
+    }
     return s;
   }
   Mat T() const {
@@ -77,8 +98,17 @@ struct Recorder {
   // free lists per size class: (offset, buffer id)
   std::map<int, std::vector<std::pair<int64_t, int>>> freel;
   std::vector<int> init_ranks;   // initial values of every rank slot
-  // dependency state per buffer
-  std::vector<int> last_w, max_r;
+  // dependency state per buffer: access rectangles with their levels
+  struct Access {
+    int buf, rid, r0, r1, c0, c1;
+  };
+  struct Entry {
+    Access a;
+    int level;
+    bool w;
+  };
+  std::vector<std::vector<Entry>> ent;
+  std::vector<int> last_w, max_r;   // (kept for the whole-buffer fast path)
   // tapes
   std::vector<GemmD> gemm;
   std::vector<EwD> ew;
@@ -97,7 +127,58 @@ struct Recorder {
   int new_buf() {
     last_w.push_back(0);
     max_r.push_back(0);
+    ent.emplace_back();
     return nbuf++;
+  }
+  static Access whole(int buf) { return Access{buf, -1, 0, 1 << 30, 0, 1 << 30}; }
+  static Access acc(const Mat& m) { return Access{m.buf, m.rid, m.nr0, m.nr1, m.nc0, m.nc1}; }
+  static bool conflict(const Access& a, const Access& b) {
+    if (a.buf != b.buf) return false;
+    if (a.rid >= 0 && b.rid >= 0 && a.rid != b.rid) return false;
+    if (a.rid < 0 || b.rid < 0) return true;
+    return a.r0 < b.r1 && b.r0 < a.r1 && a.c0 < b.c1 && b.c0 < a.c1;
+  }
+  void collapse(int buf) {   // forget rectangles: whole-buffer write / read at the max levels
+    int mw = 0, mr = 0;
+    for (auto& e : ent[buf]) (e.w ? mw : mr) = std::max(e.w ? mw : mr, e.level);
+    ent[buf].clear();
+    ent[buf].push_back(Entry{whole(buf), mw, true});
+    if (mr > 0) ent[buf].push_back(Entry{whole(buf), mr, false});
+  }
+  void collapse_reuse(int buf) {   // chunk handed to a new owner: all history is a write
+    int mx = 0;
+    for (auto& e : ent[buf]) mx = std::max(mx, e.level);
+    ent[buf].clear();
+    ent[buf].push_back(Entry{whole(buf), mx, true});
+  }
+  void addA(int kind, int idx, const std::vector<Access>& rd, const std::vector<Access>& wr) {
+    int lvl = 0;
+    for (const Access& r : rd) {
+      if (r.buf < 0) continue;
+      for (const Entry& e : ent[r.buf])
+        if (e.w && conflict(e.a, r)) lvl = std::max(lvl, e.level);
+    }
+    for (const Access& w : wr) {
+      if (w.buf < 0) continue;
+      for (const Entry& e : ent[w.buf])
+        if (conflict(e.a, w)) lvl = std::max(lvl, e.level);
+    }
+    ++lvl;
+    if (serial) lvl = (int)tasks.size() + 1;
+    for (const Access& r : rd)
+      if (r.buf >= 0) ent[r.buf].push_back(Entry{r, lvl, false});
+    for (const Access& w : wr)
+      if (w.buf >= 0) ent[w.buf].push_back(Entry{w, lvl, true});
+    for (const Access& w : wr)
+      if (w.buf >= 0 && ent[w.buf].size() > 256) collapse(w.buf);
+    for (const Access& r : rd)
+      if (r.buf >= 0 && ent[r.buf].size() > 256) collapse(r.buf);
+    tasks.push_back(Task{kind, idx, lvl});
+  }
+  void accs_of(const Mat& m, std::vector<Access>& v) const {
+    v.push_back(acc(m));
+    if (m.rslot >= 0 && slot_owner[m.rslot] >= 0) v.push_back(whole(slot_owner[m.rslot]));
+    if (m.cslot >= 0 && slot_owner[m.cslot] >= 0) v.push_back(whole(slot_owner[m.cslot]));
   }
   std::vector<int> slot_owner;
   int new_slot(int v0, int owner = -1) {
@@ -115,6 +196,14 @@ struct Recorder {
     add(kind, idx, std::vector<int>(rd), std::vector<int>(wr));
   }
   void add(int kind, int idx, const std::vector<int>& rd, const std::vector<int>& wr) {
+    std::vector<Access> r, w;
+    for (int b : rd)
+      if (b >= 0) r.push_back(whole(b));
+    for (int b : wr)
+      if (b >= 0) w.push_back(whole(b));
+    addA(kind, idx, r, w);
+  }
+  void add_old(int kind, int idx, const std::vector<int>& rd, const std::vector<int>& wr) {
     int lvl = 0;
     for (int b : rd)
       if (b >= 0) lvl = std::max(lvl, last_w[b]);
@@ -138,7 +227,19 @@ struct Recorder {
     int cls;
     int buf;
   };
+  std::map<int, int> refc;          // live temporaries: buffer id -> references
+  std::map<int, Tmp> live;
+  void retain(int buf) {
+    auto it = refc.find(buf);
+    if (it != refc.end()) ++it->second;
+  }
   Tmp alloc(int64_t elems) {
+    Tmp t = alloc_raw(elems);
+    refc[t.buf] = 1;
+    live[t.buf] = t;
+    return t;
+  }
+  Tmp alloc_raw(int64_t elems) {
     int cls = 10;
     while (((int64_t)1 << cls) < elems) ++cls;
     auto& fl = freel[cls];
@@ -146,13 +247,23 @@ struct Recorder {
     if (!fl.empty() && pool_top + sz > pool_budget) {
       auto pr = fl.front();   // oldest freed chunk first
       fl.erase(fl.begin());
+      collapse_reuse(pr.second);   // new owner: every earlier access conflicts
       return Tmp{pr.first, cls, pr.second};
     }
     Tmp t{leaf_end + pool_top, cls, new_buf()};
     pool_top += sz;
     return t;
   }
-  void release(const Tmp& t) { freel[t.cls].push_back({t.off, t.buf}); }
+  void release(const Tmp& t) { release_buf(t.buf); }
+  void release_buf(int buf) {
+    auto it = refc.find(buf);
+    if (it == refc.end()) return;        // not a temporary (leaf storage)
+    if (--it->second > 0) return;
+    const Tmp& t = live[buf];
+    freel[t.cls].push_back({t.off, t.buf});
+    refc.erase(it);
+    live.erase(buf);
+  }
 
   Mat tmp_mat(int rows, int cols, int rslot, int cslot, std::vector<Tmp>& owned) {
     Tmp t = alloc(std::max<int64_t>((int64_t)rows * cols, 1));
@@ -164,7 +275,7 @@ struct Recorder {
     m.cols = cols;
     m.rslot = rslot;
     m.cslot = cslot;
-    m.buf = t.buf;
+    m.base(t.buf, 0, rows, cols);
     return m;
   }
   LR tmp_lr(int m, int n, int cap, std::vector<Tmp>& owned) {
@@ -179,13 +290,13 @@ struct Recorder {
     r.U.rows = m;
     r.U.cols = cap;
     r.U.cslot = r.slot;
-    r.U.buf = t.buf;
+    r.U.base(t.buf, 0, m, cap);
     r.Vt.off = t.off + (int64_t)m * cap;
     r.Vt.ld = n;
     r.Vt.rows = n;
     r.Vt.cols = cap;
     r.Vt.cslot = r.slot;
-    r.Vt.buf = t.buf;
+    r.Vt.base(t.buf, 1, n, cap);
     return r;
   }
 
@@ -200,11 +311,11 @@ struct Recorder {
     gemm.push_back(d);
     flops += 8.0 * A.rows * A.cols * B.cols;
     ++gemm_count;
-    std::vector<int> rd;
-    reads_of(A, rd);
-    reads_of(B, rd);
-    reads_of(C, rd);   // C's dims (and data when beta != 0)
-    add(OP_GEMM, (int)gemm.size() - 1, rd, {C.buf});
+    std::vector<Access> rd;
+    accs_of(A, rd);
+    accs_of(B, rd);
+    accs_of(C, rd);   // C's dims (and data when beta != 0)
+    addA(OP_GEMM, (int)gemm.size() - 1, rd, {acc(C)});
   }
   // Y = a X + b Y
   void op_ew(const Mat* X, const Mat& Y, zc a, zc b) {
@@ -218,10 +329,10 @@ struct Recorder {
     d.b = b;
     d.hasX = X != nullptr;
     ew.push_back(d);
-    std::vector<int> rd;
-    if (X) reads_of(*X, rd);
-    reads_of(Y, rd);
-    add(OP_EW, (int)ew.size() - 1, rd, {Y.buf});
+    std::vector<Access> rd;
+    if (X) accs_of(*X, rd);
+    accs_of(Y, rd);
+    addA(OP_EW, (int)ew.size() - 1, rd, {acc(Y)});
   }
   void op_trsm(const Mat& T, int64_t pivoff, int variant, const Mat& Y) {
     if (Y.cols == 0) return;
@@ -229,9 +340,9 @@ struct Recorder {
     trsm.push_back(d);
     flops += 4.0 * T.rows * T.rows * Y.cols;
     ++trsm_count;
-    std::vector<int> rd{T.buf};
-    reads_of(Y, rd);
-    add(OP_TRSM, (int)trsm.size() - 1, rd, {Y.buf});
+    std::vector<Access> rd{acc(T)};
+    accs_of(Y, rd);
+    addA(OP_TRSM, (int)trsm.size() - 1, rd, {acc(Y)});
   }
   void op_getrf(const Mat& A, int64_t pivoff, int leaf) {
     getrf.push_back(GetrfD{A.off, pivoff, A.rows, leaf});
@@ -241,7 +352,9 @@ struct Recorder {
   }
   // dst (rows x cap) <- concat(pieces)
   void op_concat(int64_t dst, int rows, int out_slot, int dstbuf, const std::vector<Piece>& ps,
-                 const std::vector<int>& srcbufs) {
+                 const std::vector<int>& srcbufs, int dst_rid = -1,
+                 const std::vector<Mat>* srcmats = nullptr) {
+    if ((int)ps.size() > MAX_PIECES) throw cbie_error(CBIE_EINVALID, "too many concat pieces");
     ConcatD d;
     d.dst = dst;
     d.rows = rows;
@@ -249,11 +362,18 @@ struct Recorder {
     d.np = (int)ps.size();
     for (int i = 0; i < d.np; ++i) d.p[i] = ps[i];
     cat.push_back(d);
-    std::vector<int> rd(srcbufs);
-    for (const Piece& p : ps) {
-      if (p.cols.slot >= 0) rd.push_back(slot_owner[p.cols.slot]);
+    std::vector<Access> rd;
+    if (srcmats) {
+      for (const Mat& m : *srcmats) accs_of(m, rd);
+    } else {
+      for (int b : srcbufs)
+        if (b >= 0) rd.push_back(whole(b));
     }
-    add(OP_CONCAT, (int)cat.size() - 1, rd, {dstbuf});
+    for (const Piece& p : ps)
+      if (p.cols.slot >= 0 && slot_owner[p.cols.slot] >= 0) rd.push_back(whole(slot_owner[p.cols.slot]));
+    // the out-slot belongs to the destination buffer: writes of both halves share it
+    Access w{dstbuf, dst_rid, 0, 1 << 30, 0, 1 << 30};
+    addA(OP_CONCAT, (int)cat.size() - 1, rd, {w});
   }
   void op_dlr(const Mat& P, const LR& o) {
     DenseLRDesc d;
@@ -312,6 +432,86 @@ struct Builder {
   const int C;
   Builder(Recorder& r, cbie_hlu& f) : R(r), F(f), T(f.tree), C(f.tree.C) {}
 
+  // Lazy low-rank updates: updates to a low-rank LEAF are queued and merged by ONE
+  // concatenation + recompression when the leaf is next read (or the queue fills),
+  // instead of one recompression per update as in hmatrix.py:542-546.  Identical
+  // in exact arithmetic; fewer truncations and dependency levels.
+  struct Pend {
+    std::vector<Mat> U, Vt;
+    std::vector<zc> sign;
+    int capsum = 0;
+  };
+  std::map<int, Pend> pend;   // leaf index -> queued updates
+  bool lazy = getenv("CBIE_LAZY") != nullptr;   // off by default (round 1: slower, see DESIGN)
+  int flushes = 0;
+
+  void queue_update(int li, const Mat& U, const Mat& Vt, zc sign) {
+    Pend& p = pend[li];
+    R.retain(U.buf);
+    R.retain(Vt.buf);
+    p.U.push_back(U);
+    p.Vt.push_back(Vt);
+    p.sign.push_back(sign);
+    p.capsum += U.cols;
+    if ((int)p.U.size() >= MAX_PIECES - 1) flush(li);
+  }
+  void flush(int li) {
+    auto it = pend.find(li);
+    if (it == pend.end()) return;
+    Pend p = std::move(it->second);
+    pend.erase(it);
+    if (p.U.empty()) return;
+    ++flushes;
+    const int id = T.leaves[li].node;
+    const LR Tg = lr_raw(id);
+    const int m = Tg.U.rows, n = Tg.Vt.rows;
+    const int kc = Tg.cap + p.capsum;
+    std::vector<Recorder::Tmp> own;
+    Recorder::Tmp t = R.alloc((int64_t)(m + n) * kc);
+    own.push_back(t);
+    const int ks = R.new_slot(0, t.buf);
+    std::vector<Piece> pu{Piece{Tg.U.view(), m, 0, Tg.U.Cc(), zmk(1, 0)}};
+    std::vector<Piece> pv{Piece{Tg.Vt.view(), n, 0, Tg.Vt.Cc(), zmk(1, 0)}};
+    std::vector<int> bu{Tg.buf}, bv{Tg.buf};
+    for (size_t i = 0; i < p.U.size(); ++i) {
+      pu.push_back(Piece{p.U[i].view(), p.U[i].rows, 0, p.U[i].Cc(), p.sign[i]});
+      pv.push_back(Piece{p.Vt[i].view(), p.Vt[i].rows, 0, p.Vt[i].Cc(), zmk(1, 0)});
+      bu.push_back(p.U[i].buf);
+      bv.push_back(p.Vt[i].buf);
+    }
+    std::vector<Mat> mu{Tg.U}, mv{Tg.Vt};
+    for (size_t i = 0; i < p.U.size(); ++i) {
+      mu.push_back(p.U[i]);
+      mv.push_back(p.Vt[i]);
+    }
+    R.op_concat(t.off, m, ks, t.buf, pu, bu, 0, &mu);
+    R.op_concat(t.off + (int64_t)m * kc, n, ks, t.buf, pv, bv, 1, &mv);
+    TruncDesc d;
+    d.in_u = t.off;
+    d.in_v = t.off + (int64_t)m * kc;
+    d.ldu = m;
+    d.ldv = n;
+    d.out_u = Tg.U.off;
+    d.out_v = Tg.Vt.off;
+    d.m = m;
+    d.n = n;
+    d.k = kc;
+    d.k_slot = ks;
+    d.cap = Tg.cap;
+    d.out_slot = Tg.slot;
+    d.skip_slot = -1;
+    R.op_trunc(d, std::min(kc, std::max(m, n)), t.buf, -1, Tg.buf);
+    R.flops += trunc_flops(m, n, std::min(kc, 64));
+    for (size_t i = 0; i < p.U.size(); ++i) {
+      R.release_buf(p.U[i].buf);
+      R.release_buf(p.Vt[i].buf);
+    }
+    for (auto& x : own) R.release(x);
+  }
+  void flush_all() {
+    while (!pend.empty()) flush(pend.begin()->first);
+  }
+
   const BNode& nd(int id) const { return T.nodes[id]; }
   int rows_of(int id) const { return T.dofs(nd(id).r); }
   int cols_of(int id) const { return T.dofs(nd(id).c); }
@@ -350,10 +550,14 @@ struct Builder {
     m.ld = L.m;
     m.rows = L.m;
     m.cols = L.n;
-    m.buf = nd(id).leaf;
+    m.base(nd(id).leaf, 0, L.m, L.n);
     return m;
   }
-  LR lr(int id) const {
+  LR lr(int id) {
+    if (!pend.empty()) flush(nd(id).leaf);
+    return lr_raw(id);
+  }
+  LR lr_raw(int id) const {
     const int li = nd(id).leaf;
     const LeafInfo& L = T.leaves[li];
     LR r;
@@ -365,13 +569,13 @@ struct Builder {
     r.U.rows = L.m;
     r.U.cols = L.cap;
     r.U.cslot = li;
-    r.U.buf = li;
+    r.U.base(li, 0, L.m, L.cap);
     r.Vt.off = L.off_v;
     r.Vt.ld = L.n;
     r.Vt.rows = L.n;
     r.Vt.cols = L.cap;
     r.Vt.cslot = li;
-    r.Vt.buf = li;
+    r.Vt.base(li, 1, L.n, L.cap);
     return r;
   }
   int64_t piv(int id) const { return F.pivoff[nd(id).leaf]; }
@@ -450,8 +654,9 @@ struct Builder {
                           Piece{U.view(), U.rows, 0, U.Cc(), sign}};
     std::vector<Piece> pv{Piece{Tg.Vt.view(), n, 0, Tg.Vt.Cc(), zmk(1, 0)},
                           Piece{Vt.view(), Vt.rows, 0, Vt.Cc(), zmk(1, 0)}};
-    R.op_concat(t.off, m, ks, t.buf, pu, {Tg.buf, U.buf});
-    R.op_concat(t.off + (int64_t)m * kc, n, ks, t.buf, pv, {Tg.buf, Vt.buf});
+    std::vector<Mat> mu{Tg.U, U}, mv{Tg.Vt, Vt};
+    R.op_concat(t.off, m, ks, t.buf, pu, {Tg.buf, U.buf}, 0, &mu);
+    R.op_concat(t.off + (int64_t)m * kc, n, ks, t.buf, pv, {Tg.buf, Vt.buf}, 1, &mv);
     TruncDesc d;
     d.in_u = t.off;
     d.in_v = t.off + (int64_t)m * kc;
@@ -489,7 +694,8 @@ struct Builder {
     if (kind(id) == BLK_DENSE) {
       R.op_gemm(U, Vt.T(), D(id), sign, zmk(1, 0));
     } else if (kind(id) == BLK_LR) {
-      add_lr_to(lr(id), U, Vt, sign);
+      if (lazy) queue_update(nd(id).leaf, U, Vt, sign);
+      else add_lr_to(lr(id), U, Vt, sign);
     } else {
       const BNode& b = nd(id);
       for (int a = 0; a < b.nr; ++a)
@@ -505,7 +711,8 @@ struct Builder {
     } else if (kind(id) == BLK_LR) {
       std::vector<Recorder::Tmp> own;
       LR o = dense_to_lr(P, own);
-      add_lr_to(lr(id), o.U, o.Vt, zmk(1, 0));
+      if (lazy) queue_update(nd(id).leaf, o.U, o.Vt, zmk(1, 0));
+      else add_lr_to(lr(id), o.U, o.Vt, zmk(1, 0));
       for (auto& t : own) R.release(t);
     } else {
       const BNode& b = nd(id);
@@ -611,8 +818,13 @@ struct Builder {
       bu.push_back(parts[i].buf);
     }
     if (parts.size() > 4) throw cbie_error(CBIE_EINVALID, "more than 4 product parts");
-    R.op_concat(t.off, m, ks, t.buf, pu, bu);
-    R.op_concat(t.off + (int64_t)m * kc, n, ks, t.buf, pv, bu);
+    std::vector<Mat> mu, mv;
+    for (auto& q : parts) {
+      mu.push_back(q.U);
+      mv.push_back(q.Vt);
+    }
+    R.op_concat(t.off, m, ks, t.buf, pu, bu, 0, &mu);
+    R.op_concat(t.off + (int64_t)m * kc, n, ks, t.buf, pv, bu, 1, &mv);
     LR o = R.tmp_lr(m, n, std::min(m, n), own);
     TruncDesc d;
     d.in_u = t.off;
@@ -1004,6 +1216,8 @@ static void hlu_factor_impl(cbie_hlu* F) {
   }
   Builder B(R, *F);
   B.factor(T.root_node);
+  B.flush_all();
+  F->stat["lazy_flushes"] = B.flushes;
   auto t1 = std::chrono::steady_clock::now();
   F->stat["record_ms"] = std::chrono::duration<double, std::milli>(t1 - t0).count();
   // device state: arena = copy of the leaf storage + temporaries

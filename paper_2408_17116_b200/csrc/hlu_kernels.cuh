@@ -111,14 +111,15 @@ struct Piece {
   DimR cols;
   zc scale;
 };
+constexpr int MAX_PIECES = 16;
 struct ConcatD {
   int64_t dst;
   int rows, out_slot, np;
-  Piece p[4];
+  Piece p[MAX_PIECES];
 };
 __global__ void k_concat(zc* __restrict__ ar, int* __restrict__ ranks, const ConcatD* __restrict__ ds) {
   const ConcatD d = ds[blockIdx.y];
-  int c0[5];
+  int c0[MAX_PIECES + 1];
   c0[0] = 0;
   for (int q = 0; q < d.np; ++q) c0[q + 1] = c0[q] + dimv(d.p[q].cols, ranks);
   const int tot = c0[d.np];
