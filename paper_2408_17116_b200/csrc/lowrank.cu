@@ -59,7 +59,7 @@ __device__ __forceinline__ void cta_gemm_small(zc* C, int ldc, const zc* A, int 
 __device__ bool rand_truncate(const TruncDesc& d, zc* arena, int* ranks, int k, zc* sc,
                               int64_t scper, double tol, zc* rdv, double* kapv, double* sig,
                               int* order, zc* Ms, zc* Ws, double* red, int* flag,
-                              unsigned long long* overflow) {
+                              unsigned long long* overflow, zc* gsm) {
   const int m = d.m, n = d.n;
   const zc* U = arena + d.in_u;
   const zc* Vt = arena + d.in_v;
@@ -75,8 +75,8 @@ __device__ bool rand_truncate(const TruncDesc& d, zc* arena, int* ranks, int k, 
       Om[e] = zmk(hash_u((uint32_t)(e % n), (uint32_t)(e / n), 2 * attempt),
                   hash_u((uint32_t)(e % n), (uint32_t)(e / n), 2 * attempt + 1));
     __syncthreads();
-    cta_gemm_small(T, k, Vt, d.ldv, Om, n, k, n, l, 1);   // T = Vt^T Om      (k x l)
-    cta_gemm_small(Y, m, U, d.ldu, T, k, m, k, l, 0);     // Y = U T          (m x l)
+    cta_gemm_tiled(T, k, Vt, d.ldv, 1, Om, n, k, n, l, gsm);   // T = Vt^T Om      (k x l)
+    cta_gemm_tiled(Y, m, U, d.ldu, 0, T, k, m, k, l, gsm);     // Y = U T          (m x l)
     // no power iteration: without re-orthonormalisation (A A^H)^q A Omega loses the
     // singular directions below eps^(1/(2q+1)) s0, which the truncation needs; a
     // 16-column oversampling margin is used instead
@@ -96,10 +96,10 @@ __device__ bool rand_truncate(const TruncDesc& d, zc* arena, int* ranks, int k, 
     __syncthreads();
     cta_apply_q(Y, m, l, m, kapv, Q, l, m);
     // T = U^H Q (k x l);  Bt = Vt T (n x l)  [B = Q^H U V, Bt = B^T = Vt (U^T conj Q) = Vt conj(T)]
-    cta_gemm_small(T, k, U, d.ldu, Q, m, k, m, l, 2);
+    cta_gemm_tiled(T, k, U, d.ldu, 2, Q, m, k, m, l, gsm);
     for (int64_t e = threadIdx.x; e < (int64_t)k * l; e += LR_NT) T[e] = zconj(T[e]);
     __syncthreads();
-    cta_gemm_small(Z, n, Vt, d.ldv, T, k, n, k, l, 0);    // Z = Bt (n x l)
+    cta_gemm_tiled(Z, n, Vt, d.ldv, 0, T, k, n, k, l, gsm);    // Z = Bt (n x l)
     // exact SVD of B = R2^T Q2^T:  QR(Bt) = Q2 R2, core M = R2^T (l x l)
     cta_qr(Z, n, l, n, rdv, kapv, red);
     for (int e = threadIdx.x; e < l * l; e += LR_NT) {
@@ -191,7 +191,7 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
     zc* Ws = Ms + SMEM_J * SMEM_J;
     zc* sc = scratch + (int64_t)blockIdx.x * scratch_per;
     if (rand_truncate(d, arena, ranks, k, sc, scratch_per, tol, rd1, kap1, sig, order, Ms, Ws, red,
-                      &flag, overflow))
+                      &flag, overflow, Ws + SMEM_J * SMEM_J))
       return;
     __syncthreads();
   }
@@ -325,7 +325,8 @@ void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int
   const size_t need = (size_t)std::min(wave, nd) * per;
   if (scratch.n < need) scratch.alloc(need);
   const size_t smem = (size_t)kmax * (2 * sizeof(zc) + 3 * sizeof(double) + sizeof(int)) + 16 +
-                      (size_t)SMEM_J * SMEM_J * 2 * sizeof(zc);
+                      (size_t)SMEM_J * SMEM_J * 2 * sizeof(zc) +
+                      (size_t)TG_K * (TG_R + 1 + 65) * sizeof(zc);
   if (smem > 220 * 1024) throw cbie_error(CBIE_EINVALID, "truncation dimension too large");
   CK(cudaFuncSetAttribute(k_truncate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (int b0 = 0; b0 < nd; b0 += wave) {
@@ -436,6 +437,7 @@ __global__ void __launch_bounds__(LR_NT) k_dense_lr(zc* arena, int* ranks,
   extern __shared__ __align__(16) unsigned char smem_raw[];
   zc* rd = reinterpret_cast<zc*>(smem_raw);
   double* kap = reinterpret_cast<double*>(rd + d.cap);
+  zc* gsm = reinterpret_cast<zc*>((reinterpret_cast<uintptr_t>(kap + d.cap) + 15) & ~uintptr_t(15));
   double pf2 = 0.0;
   for (int64_t e = threadIdx.x; e < (int64_t)m * n; e += LR_NT)
     pf2 += zabs2(P[(e / m) * ld + e % m]);
@@ -449,33 +451,18 @@ __global__ void __launch_bounds__(LR_NT) k_dense_lr(zc* arena, int* ranks,
   for (int attempt = 0;; ++attempt) {
     const bool exact = 2 * l > full;
     if (exact) l = full;
-    // Y = P * Omega   (exact: Y = P's first l = min(m,n) columns span... use P itself)
     if (exact && l == n) {
       for (int64_t e = threadIdx.x; e < (int64_t)m * l; e += LR_NT)
         Y[e] = P[(e / m) * ld + e % m];
     } else {
-      for (int64_t e = threadIdx.x; e < (int64_t)m * l; e += LR_NT) {
-        const int i = (int)(e % m), c = (int)(e / m);
-        zc s = zmk(0.0, 0.0);
-        for (int j = 0; j < n; ++j)
-          zfma(s, P[(int64_t)j * ld + i], zmk(hash_unit(j, c, 2 * attempt), hash_unit(j, c, 2 * attempt + 1)));
-        Y[e] = s;
-      }
+      zc* Om = Z;   // Omega (n x l) staged in the Z region, then Z reused below
+      for (int64_t e = threadIdx.x; e < (int64_t)n * l; e += LR_NT)
+        Om[e] = zmk(hash_unit((uint32_t)(e % n), (uint32_t)(e / n), 2 * attempt),
+                    hash_unit((uint32_t)(e % n), (uint32_t)(e / n), 2 * attempt + 1));
       __syncthreads();
-      // one power iteration: Z = P^H Y, Y = P Z
-      for (int64_t e = threadIdx.x; e < (int64_t)n * l; e += LR_NT) {
-        const int j = (int)(e % n), c = (int)(e / n);
-        zc s = zmk(0.0, 0.0);
-        for (int i = 0; i < m; ++i) zfma(s, zconj(P[(int64_t)j * ld + i]), Y[(int64_t)c * m + i]);
-        Z[e] = s;
-      }
-      __syncthreads();
-      for (int64_t e = threadIdx.x; e < (int64_t)m * l; e += LR_NT) {
-        const int i = (int)(e % m), c = (int)(e / m);
-        zc s = zmk(0.0, 0.0);
-        for (int j = 0; j < n; ++j) zfma(s, P[(int64_t)j * ld + i], Z[(int64_t)c * n + j]);
-        Y[e] = s;
-      }
+      cta_gemm_tiled(Y, m, P, ld, 0, Om, n, m, n, l, gsm);   // Y = P Omega
+      cta_gemm_tiled(Z, n, P, ld, 2, Y, m, n, m, l, gsm);    // Z = P^H Y
+      cta_gemm_tiled(Y, m, P, ld, 0, Z, n, m, n, l, gsm);    // Y = P Z
     }
     __syncthreads();
     cta_qr(Y, m, l, m, rd, kap, red);
@@ -487,14 +474,13 @@ __global__ void __launch_bounds__(LR_NT) k_dense_lr(zc* arena, int* ranks,
     }
     __syncthreads();
     cta_apply_q(Y, m, lq, m, kap, U, lq, m);
-    // Vt = P^T conj(Q)  (B = Q^H P, Vt = B^T)
+    // Vt = P^T conj(Q)  (B = Q^H P, Vt = B^T):  Vt = conj(P^H Q)
+    cta_gemm_tiled(Vt, n, P, ld, 2, U, m, n, m, lq, gsm);
     double bf2 = 0.0;
     for (int64_t e = threadIdx.x; e < (int64_t)n * lq; e += LR_NT) {
-      const int j = (int)(e % n), c = (int)(e / n);
-      zc s = zmk(0.0, 0.0);
-      for (int i = 0; i < m; ++i) zfma(s, P[(int64_t)j * ld + i], zconj(U[(int64_t)c * m + i]));
-      Vt[e] = s;
-      bf2 += zabs2(s);
+      const zc v = zconj(Vt[e]);
+      Vt[e] = v;
+      bf2 += zabs2(v);
     }
     bf2 = block_sum(bf2, red);
     double rowmax = 0.0;
@@ -529,7 +515,8 @@ void launch_dense_lr(zc* arena, int* ranks, const DenseLRDesc* d_desc, int nd, i
   const int wave = (int)std::max<int64_t>(1, ((int64_t)1 << 30) / (per * (int64_t)sizeof(zc)));
   const size_t need = (size_t)std::min(wave, nd) * per;
   if (scratch.n < need) scratch.alloc(need);
-  const size_t smem = (size_t)max_cap * (sizeof(zc) + sizeof(double));
+  const size_t smem = (size_t)max_cap * (sizeof(zc) + sizeof(double)) + 32 +
+                      (size_t)TG_K * (TG_R + 1 + 65) * sizeof(zc);
   CK(cudaFuncSetAttribute(k_dense_lr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (int b0 = 0; b0 < nd; b0 += wave) {
     int nb = std::min(wave, nd - b0);

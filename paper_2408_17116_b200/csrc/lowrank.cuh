@@ -250,3 +250,75 @@ __device__ __forceinline__ int cta_herm_jacobi(zc* G, zc* W, int q, double* cs_c
   }
   return sweep;
 }
+
+// CTA-tiled small GEMM: C (rows x l, col-major ldc) = op(A) (rows x kk) * B (kk x l, ldb),
+// l <= 64.  op: 0 A (col-major, lda), 1 A^T, 2 A^H, 3 conj(A).  Staging tiles of
+// 64 rows x 32 k of op(A) and 32 x l of B in shared memory (sm >= 2*32*65 zc).
+constexpr int TG_R = 64, TG_K = 32;
+__device__ __forceinline__ void cta_gemm_tiled64(zc* C, int ldc, const zc* A, int lda, int mode,
+                                                 const zc* B, int ldb, int rows, int kk, int l,
+                                                 zc* sm);
+// any l: column blocks of 64
+__device__ __forceinline__ void cta_gemm_tiled(zc* C, int ldc, const zc* A, int lda, int mode,
+                                               const zc* B, int ldb, int rows, int kk, int l,
+                                               zc* sm) {
+  for (int c0 = 0; c0 < l; c0 += 64)
+    cta_gemm_tiled64(C + (int64_t)c0 * ldc, ldc, A, lda, mode, B + (int64_t)c0 * ldb, ldb, rows, kk,
+                     min(64, l - c0), sm);
+}
+__device__ __forceinline__ void cta_gemm_tiled64(zc* C, int ldc, const zc* A, int lda, int mode,
+                                                 const zc* B, int ldb, int rows, int kk, int l,
+                                                 zc* sm) {
+  zc* As = sm;                       // [TG_K][TG_R + 1]
+  zc* Bs = sm + TG_K * (TG_R + 1);   // [TG_K][64 + 1]
+  const int tr = threadIdx.x % TG_R, tg = threadIdx.x / TG_R;   // 8 column groups
+  constexpr int NG = LR_NT / TG_R;
+  for (int r0 = 0; r0 < rows; r0 += TG_R) {
+    zc acc[64 / NG];
+#pragma unroll
+    for (int q = 0; q < 64 / NG; ++q) acc[q] = zmk(0.0, 0.0);
+    for (int k0 = 0; k0 < kk; k0 += TG_K) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < TG_K * TG_R; e += LR_NT) {
+        int i, a;
+        if (mode == 1 || mode == 2) {   // contiguous along k for a fixed row
+          a = e % TG_K;
+          i = e / TG_K;
+        } else {
+          i = e % TG_R;
+          a = e / TG_R;
+        }
+        const int gi = r0 + i, ga = k0 + a;
+        zc v = zmk(0.0, 0.0);
+        if (gi < rows && ga < kk) {
+          if (mode == 0) v = A[(int64_t)ga * lda + gi];
+          else if (mode == 1) v = A[(int64_t)gi * lda + ga];
+          else if (mode == 2) v = zconj(A[(int64_t)gi * lda + ga]);
+          else v = zconj(A[(int64_t)ga * lda + gi]);
+        }
+        As[a * (TG_R + 1) + i] = v;
+      }
+      for (int e = threadIdx.x; e < TG_K * l; e += LR_NT) {
+        const int a = e % TG_K, c = e / TG_K;
+        Bs[a * 65 + c] = (k0 + a < kk) ? B[(int64_t)c * ldb + k0 + a] : zmk(0.0, 0.0);
+      }
+      __syncthreads();
+      const int kmax = min(TG_K, kk - k0);
+      for (int a = 0; a < kmax; ++a) {
+        const zc av = As[a * (TG_R + 1) + tr];
+#pragma unroll
+        for (int q = 0; q < 64 / NG; ++q) {
+          const int c = tg + NG * q;
+          if (c < l) zfma(acc[q], av, Bs[a * 65 + c]);
+        }
+      }
+    }
+    if (r0 + tr < rows)
+#pragma unroll
+      for (int q = 0; q < 64 / NG; ++q) {
+        const int c = tg + NG * q;
+        if (c < l) C[(int64_t)c * ldc + r0 + tr] = acc[q];
+      }
+  }
+  __syncthreads();
+}
