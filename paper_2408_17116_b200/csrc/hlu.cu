@@ -1249,11 +1249,16 @@ static void hlu_factor_impl(cbie_hlu* F) {
   F->stat["levels"] = ex.levels;
   F->stat["trunc_kernel_ms"] = ex.trunc_kernel_ms;
   if (getenv("CBIE_PROFILE")) {
-    unsigned long long h[6] = {0, 0, 0, 0, 0, 0};
+    unsigned long long h[14] = {};
     trunc_prof_read(h);
     const char* nm[4] = {"qr", "core", "svd", "apply"};
     for (int i = 0; i < 4; ++i) F->stat[std::string("trunc_cyc_") + nm[i]] = h[4] ? (double)h[i] / h[4] : 0;
     F->stat["trunc_mean_sweeps"] = h[4] ? (double)h[5] / h[4] : 0;
+    const char* pn[4] = {"rand_ok", "rand_fail", "exact_smem", "exact_global"};
+    for (int i = 0; i < 4; ++i) {
+      F->stat[std::string("trunc_n_") + pn[i]] = (double)h[6 + 2 * i];
+      F->stat[std::string("trunc_cyc_") + pn[i]] = h[6 + 2 * i] ? (double)h[7 + 2 * i] / h[6 + 2 * i] : 0;
+    }
   }
   F->stat["trunc_launches"] = ex.trunc_launches;
   {

@@ -15,7 +15,7 @@ constexpr int SMEM_J = 64;   // cores up to 64 x 64 run the Jacobi SVD in shared
 __device__ int prof_onesided_flag_dev = 0;
 
 constexpr int KEXACT = 64;    // concatenated ranks above this use the randomized path
-constexpr int RL0 = 32;       // initial sketch size
+constexpr int RL0 = 48;       // initial sketch size (accepts ranks <= 32 in one attempt)
 
 __device__ __forceinline__ double hash_u(uint32_t a, uint32_t b, uint32_t c) {
   uint32_t h = a * 0x9E3779B1u ^ (b + 0x7F4A7C15u) * 0x85EBCA77u ^ (c + 0x165667B1u) * 0xC2B2AE3Du;
@@ -190,9 +190,14 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
     Ms = reinterpret_cast<zc*>((reinterpret_cast<uintptr_t>(Ms) + 15) & ~uintptr_t(15));
     zc* Ws = Ms + SMEM_J * SMEM_J;
     zc* sc = scratch + (int64_t)blockIdx.x * scratch_per;
-    if (rand_truncate(d, arena, ranks, k, sc, scratch_per, tol, rd1, kap1, sig, order, Ms, Ws, red,
-                      &flag, overflow, Ws + SMEM_J * SMEM_J))
-      return;
+    const long long tr0 = clock64();
+    const bool ok = rand_truncate(d, arena, ranks, k, sc, scratch_per, tol, rd1, kap1, sig, order, Ms,
+                                  Ws, red, &flag, overflow, Ws + SMEM_J * SMEM_J);
+    if (prof && threadIdx.x == 0) {
+      atomicAdd(prof + (ok ? 6 : 8), 1ull);
+      atomicAdd(prof + (ok ? 7 : 9), (unsigned long long)(clock64() - tr0));
+    }
+    if (ok) return;
     __syncthreads();
   }
   zc* U = arena + d.in_u;
@@ -224,21 +229,55 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
   __syncthreads();
   long long tc2 = clock64();
   int sweeps = 0;
-  if (kk1 <= SMEM_J && kk2 <= SMEM_J) {
-    // one-sided Jacobi with M and W resident in shared memory
-    zc* Ms = reinterpret_cast<zc*>(order + KS);
+  bool precond = false;
+  zc* Ms = nullptr;
+  zc* Bs = nullptr;
+  zc* Js = nullptr;
+  double* kapM = nullptr;
+  if (kk1 <= SMEM_J && kk2 <= SMEM_J && kk1 >= kk2 && !ident) {
+    // QR-preconditioned one-sided Jacobi (M = Q_M R, Jacobi on R^H), all in shared
+    // memory: converges in a few sweeps instead of ~11.
+    precond = true;
+    Ms = reinterpret_cast<zc*>(order + KS);
     Ms = reinterpret_cast<zc*>((reinterpret_cast<uintptr_t>(Ms) + 15) & ~uintptr_t(15));
-    zc* Ws = Ms + SMEM_J * SMEM_J;
+    Bs = Ms + SMEM_J * SMEM_J;
+    Js = Bs + SMEM_J * SMEM_J;
+    zc* rdM = Js + SMEM_J * SMEM_J;
+    kapM = reinterpret_cast<double*>(rdM + SMEM_J);
     for (int e = threadIdx.x; e < kk1 * kk2; e += LR_NT) Ms[e] = M[e];
     __syncthreads();
-    sweeps = cta_jacobi(Ms, kk1, kk2, kk1, Ws, kk2, &flag, red);
+    cta_qr(Ms, kk1, kk2, kk1, rdM, kapM, red);
+    // A = R^H (kk2 x kk2): A[i][j] = conj(R[j][i]), R upper (diag rdM, strict upper in Ms)
+    for (int e = threadIdx.x; e < kk2 * kk2; e += LR_NT) {
+      const int i = e % kk2, j = e / kk2;
+      zc v = zmk(0.0, 0.0);
+      if (i == j) v = zconj(rdM[i]);
+      else if (i > j) v = zconj(Ms[i * kk1 + j]);
+      Bs[j * kk2 + i] = v;
+    }
+    __syncthreads();
+    sweeps = cta_jacobi_hw(Bs, kk2, kk2, kk2, Js, kk2, &flag, red);
     for (int c = threadIdx.x; c < kk2; c += LR_NT) {
       double sq = 0.0;
-      for (int i = 0; i < kk1; ++i) sq += zabs2(Ms[c * kk1 + i]);
+      for (int i = 0; i < kk2; ++i) sq += zabs2(Bs[c * kk2 + i]);
       sig[c] = sqrt(sq);
     }
-    for (int e = threadIdx.x; e < kk1 * kk2; e += LR_NT) M[e] = Ms[e];
-    for (int e = threadIdx.x; e < kk2 * kk2; e += LR_NT) W[e] = Ws[e];
+    __syncthreads();
+  } else if (kk1 <= SMEM_J && kk2 <= SMEM_J) {
+    // one-sided Jacobi with M and W resident in shared memory
+    zc* Mss = reinterpret_cast<zc*>(order + KS);
+    Mss = reinterpret_cast<zc*>((reinterpret_cast<uintptr_t>(Mss) + 15) & ~uintptr_t(15));
+    zc* Wss = Mss + SMEM_J * SMEM_J;
+    for (int e = threadIdx.x; e < kk1 * kk2; e += LR_NT) Mss[e] = M[e];
+    __syncthreads();
+    sweeps = cta_jacobi_hw(Mss, kk1, kk2, kk1, Wss, kk2, &flag, red);
+    for (int c = threadIdx.x; c < kk2; c += LR_NT) {
+      double sq = 0.0;
+      for (int i = 0; i < kk1; ++i) sq += zabs2(Mss[c * kk1 + i]);
+      sig[c] = sqrt(sq);
+    }
+    for (int e = threadIdx.x; e < kk1 * kk2; e += LR_NT) M[e] = Mss[e];
+    for (int e = threadIdx.x; e < kk2 * kk2; e += LR_NT) W[e] = Wss[e];
     __syncthreads();
   } else {
     sweeps = cta_jacobi(M, kk1, kk2, kk1, W, kk2, &flag, red);
@@ -269,17 +308,32 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
     if (threadIdx.x == 0) atomicAdd(overflow, 1ull);
     r = d.cap;
   }
-  // U' = Q1 [ (M W)[:, order[:r]] ; 0 ]
   zc* Uo = arena + d.out_u;
   zc* Vo = arena + d.out_v;
-  for (int e = threadIdx.x; e < m * r; e += LR_NT) {
-    const int i = e % m, l = e / m;
-    Uo[(int64_t)l * m + i] = i < kk1 ? M[(int64_t)order[l] * kk1 + i] : zmk(0.0, 0.0);
-  }
-  // Vt' = Q2 [ conj(W[:, order[:r]]) ; 0 ]
-  for (int e = threadIdx.x; e < n * r; e += LR_NT) {
-    const int j = e % n, l = e / n;
-    Vo[(int64_t)l * n + j] = j < kk2 ? zconj(W[(int64_t)order[l] * kk2 + j]) : zmk(0.0, 0.0);
+  if (precond) {
+    // U' = Q1 Q_M [J_r Sigma_r; 0],  Vt' = Q2 [conj(B_r) / sigma; 0]
+    for (int e = threadIdx.x; e < m * r; e += LR_NT) {
+      const int i = e % m, l = e / m;
+      Uo[(int64_t)l * m + i] = i < kk2 ? zscale(Js[order[l] * kk2 + i], sig[order[l]]) : zmk(0.0, 0.0);
+    }
+    for (int e = threadIdx.x; e < n * r; e += LR_NT) {
+      const int j = e % n, l = e / n;
+      Vo[(int64_t)l * n + j] =
+          j < kk2 ? zscale(zconj(Bs[order[l] * kk2 + j]), 1.0 / sig[order[l]]) : zmk(0.0, 0.0);
+    }
+    __syncthreads();
+    cta_apply_q(Ms, kk1, kk2, kk1, kapM, Uo, r, m);   // Q_M on the top kk1 rows
+  } else {
+    // U' = Q1 [ (M W)[:, order[:r]] ; 0 ]
+    for (int e = threadIdx.x; e < m * r; e += LR_NT) {
+      const int i = e % m, l = e / m;
+      Uo[(int64_t)l * m + i] = i < kk1 ? M[(int64_t)order[l] * kk1 + i] : zmk(0.0, 0.0);
+    }
+    // Vt' = Q2 [ conj(W[:, order[:r]]) ; 0 ]
+    for (int e = threadIdx.x; e < n * r; e += LR_NT) {
+      const int j = e % n, l = e / n;
+      Vo[(int64_t)l * n + j] = j < kk2 ? zconj(W[(int64_t)order[l] * kk2 + j]) : zmk(0.0, 0.0);
+    }
   }
   __syncthreads();
   cta_apply_q(U, m, kk1, ldu, kap1, Uo, r, m);
@@ -294,6 +348,9 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
       atomicAdd(prof + 3, (unsigned long long)(tc4 - tc3));
       atomicAdd(prof + 4, 1ull);
       atomicAdd(prof + 5, (unsigned long long)sweeps);
+      const bool sm = kk1 <= SMEM_J && kk2 <= SMEM_J;
+      atomicAdd(prof + (sm ? 10 : 12), 1ull);
+      atomicAdd(prof + (sm ? 11 : 13), (unsigned long long)(tc4 - tc0));
     }
   }
 }
@@ -304,13 +361,13 @@ unsigned long long* g_trunc_prof = nullptr;   // debug cycle counters (CBIE_PROF
 
 void trunc_prof_enable(bool on, int onesided) {
   if (on && !g_trunc_prof) {
-    cudaMalloc(&g_trunc_prof, 8 * sizeof(unsigned long long));
-    cudaMemset(g_trunc_prof, 0, 8 * sizeof(unsigned long long));
+    cudaMalloc(&g_trunc_prof, 16 * sizeof(unsigned long long));
+    cudaMemset(g_trunc_prof, 0, 16 * sizeof(unsigned long long));
   }
   cudaMemcpyToSymbol(prof_onesided_flag_dev, &onesided, sizeof(int));
 }
 void trunc_prof_read(unsigned long long* h) {
-  if (g_trunc_prof) cudaMemcpy(h, g_trunc_prof, 6 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  if (g_trunc_prof) cudaMemcpy(h, g_trunc_prof, 14 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
 }
 
 void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
@@ -324,9 +381,11 @@ void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int
   const int wave = (int)std::max<int64_t>(1, ((int64_t)1 << 30) / (per * (int64_t)sizeof(zc)));
   const size_t need = (size_t)std::min(wave, nd) * per;
   if (scratch.n < need) scratch.alloc(need);
+  // exact path: Ms, Bs, Js (3 x 64^2) + rdM/kapM; randomized path: Ms, Ws + GEMM tiles
   const size_t smem = (size_t)kmax * (2 * sizeof(zc) + 3 * sizeof(double) + sizeof(int)) + 16 +
-                      (size_t)SMEM_J * SMEM_J * 2 * sizeof(zc) +
-                      (size_t)TG_K * (TG_R + 1 + 65) * sizeof(zc);
+                      std::max((size_t)SMEM_J * SMEM_J * 3 * sizeof(zc) + SMEM_J * (sizeof(zc) + sizeof(double)),
+                               (size_t)SMEM_J * SMEM_J * 2 * sizeof(zc) +
+                                   (size_t)TG_K * (TG_R + 1 + 65) * sizeof(zc));
   if (smem > 220 * 1024) throw cbie_error(CBIE_EINVALID, "truncation dimension too large");
   CK(cudaFuncSetAttribute(k_truncate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (int b0 = 0; b0 < nd; b0 += wave) {

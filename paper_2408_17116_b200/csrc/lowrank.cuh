@@ -322,3 +322,83 @@ __device__ __forceinline__ void cta_gemm_tiled64(zc* C, int ldc, const zc* A, in
   }
   __syncthreads();
 }
+
+__device__ __forceinline__ double hw_sum(double v) {
+#pragma unroll
+  for (int o = 8; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// One-sided Jacobi with one HALF-warp per column pair (32 pairs in flight per
+// round with 512 threads); same rotation and skip rules as cta_jacobi.
+__device__ __forceinline__ int cta_jacobi_hw(zc* M, int p, int q, int ldm, zc* W, int ldw, int* flag,
+                                             double* red) {
+  const int hw = threadIdx.x >> 4, hl = threadIdx.x & 15;
+  constexpr int NHW = LR_NT / 16;
+  double f2 = 0.0;
+  for (int e = threadIdx.x; e < p * q; e += LR_NT) f2 += zabs2(M[(int64_t)(e / p) * ldm + e % p]);
+  f2 = block_sum(f2, red);
+  const double floor2 = 1e-24 * f2;
+  for (int e = threadIdx.x; e < q * q; e += LR_NT) {
+    int i = e % q, j = e / q;
+    W[(int64_t)j * ldw + i] = zmk(i == j ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+  if (q < 2) return 0;
+  const int qe = q + (q & 1);
+  int sweep = 0;
+  for (; sweep < 40; ++sweep) {
+    if (threadIdx.x == 0) *flag = 0;
+    __syncthreads();
+    for (int r = 0; r < qe - 1; ++r) {
+      // warp-uniform trip count: both half-warps of a warp shuffle together
+      for (int base = 0; base < qe / 2; base += NHW) {
+        const int pi = base + hw;
+        const int pa = pi, pb = qe - 1 - pi;
+        const int a = pa == 0 ? 0 : ((pa - 1 + r) % (qe - 1)) + 1;
+        const int b = pb == 0 ? 0 : ((pb - 1 + r) % (qe - 1)) + 1;
+        const bool valid = pi < qe / 2 && a < q && b < q;
+        zc* x = M + (int64_t)(valid ? a : 0) * ldm;
+        zc* y = M + (int64_t)(valid ? b : 0) * ldm;
+        double al = 0.0, be = 0.0, gr = 0.0, gi = 0.0;
+        if (valid)
+          for (int i = hl; i < p; i += 16) {
+            const zc xi = x[i], yi = y[i];
+            al += zabs2(xi);
+            be += zabs2(yi);
+            gr += xi.x * yi.x + xi.y * yi.y;
+            gi += xi.x * yi.y - xi.y * yi.x;
+          }
+        al = hw_sum(al);
+        be = hw_sum(be);
+        gr = hw_sum(gr);
+        gi = hw_sum(gi);
+        if (!valid) continue;
+        const double g = sqrt(gr * gr + gi * gi);
+        if (!(g > 1e-14 * sqrt(al * be)) || g == 0.0 || fmin(al, be) < floor2) continue;
+        const double zeta = (be - al) / (2.0 * g);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        const double ig = 1.0 / g;
+        const zc se = zmk(gr * ig * sn, gi * ig * sn), sec = zmk(gr * ig * sn, -gi * ig * sn);
+        for (int i = hl; i < p; i += 16) {
+          const zc xi = x[i], yi = y[i];
+          x[i] = zsub(zscale(xi, cs), zmul(sec, yi));
+          y[i] = zadd(zmul(se, xi), zscale(yi, cs));
+        }
+        zc* wx = W + (int64_t)a * ldw;
+        zc* wy = W + (int64_t)b * ldw;
+        for (int i = hl; i < q; i += 16) {
+          const zc xi = wx[i], yi = wy[i];
+          wx[i] = zsub(zscale(xi, cs), zmul(sec, yi));
+          wy[i] = zadd(zmul(se, xi), zscale(yi, cs));
+        }
+        if (hl == 0) *flag = 1;
+      }
+      __syncthreads();
+    }
+    if (*flag == 0) break;
+    __syncthreads();
+  }
+  return sweep;
+}
