@@ -311,7 +311,7 @@ __global__ void __launch_bounds__(256) k_getrf(zc* __restrict__ ar, int* __restr
     for (int o = 16; o > 0; o >>= 1) loc = fmax(loc, __shfl_xor_sync(0xffffffffu, loc, o));
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = loc;
     __syncthreads();
-    for (int w = 0; w < LR_NW; ++w) anorm = fmax(anorm, red[w]);
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) anorm = fmax(anorm, red[w]);
     __syncthreads();
   }
   bool zero_pivot = false;
@@ -343,7 +343,7 @@ __global__ void __launch_bounds__(256) k_getrf(zc* __restrict__ ar, int* __restr
     if (threadIdx.x == 0) {
       double B = s_v[0];
       int I = s_i[0];
-      for (int w = 1; w < LR_NW; ++w)
+      for (int w = 1; w < (int)(blockDim.x >> 5); ++w)
         if (s_v[w] > B || (s_v[w] == B && s_i[w] < I)) {
           B = s_v[w];
           I = s_i[w];

@@ -208,8 +208,16 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
   zc* W = M + (int64_t)kk1 * kk2;                         // kk2 x kk2
 
   const int ldu = d.ldu, ldv = d.ldv;
-  cta_qr(U, m, k, ldu, rd1, kap1, red);
-  if (!ident) cta_qr(Vt, n, k, ldv, rd2, kap2, red);
+  if (ident) {
+    cta_qr(U, m, k, ldu, rd1, kap1, red);
+  } else {
+    // the two QRs are independent: one per CTA half, named barriers 1 and 2
+    __shared__ double red2[LR_NW];
+    const int half = threadIdx.x / (LR_NT / 2);
+    if (half == 0) half_qr(U, m, k, ldu, rd1, kap1, red2, 1);
+    else half_qr(Vt, n, k, ldv, rd2, kap2, red2 + LR_NW / 2, 2);
+    __syncthreads();
+  }
   long long tc1 = clock64();
   // M = R1 R2^T (R2 = I for the dense mode)
   for (int e = threadIdx.x; e < kk1 * kk2; e += LR_NT) {
@@ -336,8 +344,14 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
     }
   }
   __syncthreads();
-  cta_apply_q(U, m, kk1, ldu, kap1, Uo, r, m);
-  if (!ident) cta_apply_q(Vt, n, kk2, ldv, kap2, Vo, r, n);
+  if (ident) {
+    cta_apply_q(U, m, kk1, ldu, kap1, Uo, r, m);
+  } else {
+    const int half = threadIdx.x / (LR_NT / 2);
+    if (half == 0) half_apply_q(U, m, kk1, ldu, kap1, Uo, r, m, 1);
+    else half_apply_q(Vt, n, kk2, ldv, kap2, Vo, r, n, 2);
+    __syncthreads();
+  }
   if (threadIdx.x == 0) {
     ranks[d.out_slot] = r;
     if (prof) {

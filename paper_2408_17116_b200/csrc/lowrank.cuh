@@ -402,3 +402,86 @@ __device__ __forceinline__ int cta_jacobi_hw(zc* M, int p, int q, int ldm, zc* W
   }
   return sweep;
 }
+
+// ---------------------------------------------------------------------------
+// Split-CTA variants: the two halves of the CTA (threads [0, NT/2) and
+// [NT/2, NT)) work on independent problems, synchronising with named barriers
+// (bar.sync id, NT/2) instead of __syncthreads.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ void half_bar(int id) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(LR_NT / 2) : "memory");
+}
+__device__ __forceinline__ double half_sum(double v, double* red, int id) {
+  constexpr int NWH = LR_NW / 2;
+  v = warp_sum(v);
+  const int w = (threadIdx.x >> 5) % NWH, l = threadIdx.x & 31;
+  half_bar(id);
+  if (l == 0) red[w] = v;
+  half_bar(id);
+  double t = 0.0;
+#pragma unroll
+  for (int i = 0; i < NWH; ++i) t += red[i];
+  return t;
+}
+// cta_qr for one half of the CTA; id = 1 + half index, red has LR_NW/2 doubles
+__device__ __forceinline__ void half_qr(zc* A, int m, int k, int ld, zc* rdiag, double* kappa,
+                                        double* red, int id) {
+  constexpr int NTH = LR_NT / 2, NWH = LR_NW / 2;
+  const int tid = threadIdx.x % NTH;
+  const int kk = min(m, k);
+  const int w = tid >> 5, lane = tid & 31;
+  for (int j = 0; j < kk; ++j) {
+    zc* x = A + (int64_t)j * ld;
+    double s = 0.0;
+    for (int i = j + tid; i < m; i += NTH) s += zabs2(x[i]);
+    s = half_sum(s, red, id);
+    const double nx = sqrt(s);
+    const zc alpha = x[j];
+    const double aa = sqrt(zabs2(alpha));
+    const zc ph = aa > 0.0 ? zmk(alpha.x / aa, alpha.y / aa) : zmk(1.0, 0.0);
+    double kap = 0.0;
+    half_bar(id);
+    if (nx > 0.0) {
+      kap = 1.0 / (nx * (nx + aa));
+      if (tid == 0) {
+        x[j] = zscale(ph, aa + nx);
+        rdiag[j] = zscale(ph, -nx);
+        kappa[j] = kap;
+      }
+    } else if (tid == 0) {
+      rdiag[j] = zmk(0.0, 0.0);
+      kappa[j] = 0.0;
+    }
+    half_bar(id);
+    if (kap != 0.0) {
+      for (int c = j + 1 + w; c < k; c += NWH) {
+        zc* y = A + (int64_t)c * ld;
+        zc d = zmk(0.0, 0.0);
+        for (int i = j + lane; i < m; i += 32) d = zadd(d, zcmul(x[i], y[i]));
+        d = zscale(warp_sum(d), kap);
+        for (int i = j + lane; i < m; i += 32) y[i] = zsub(y[i], zmul(d, x[i]));
+      }
+    }
+    half_bar(id);
+  }
+}
+__device__ __forceinline__ void half_apply_q(const zc* A, int m, int kk, int ld, const double* kappa,
+                                             zc* Z, int ncol, int ldz, int id) {
+  constexpr int NTH = LR_NT / 2, NWH = LR_NW / 2;
+  const int tid = threadIdx.x % NTH;
+  const int w = tid >> 5, lane = tid & 31;
+  for (int j = kk - 1; j >= 0; --j) {
+    const double kap = kappa[j];
+    if (kap != 0.0) {
+      const zc* x = A + (int64_t)j * ld;
+      for (int c = w; c < ncol; c += NWH) {
+        zc* y = Z + (int64_t)c * ldz;
+        zc d = zmk(0.0, 0.0);
+        for (int i = j + lane; i < m; i += 32) d = zadd(d, zcmul(x[i], y[i]));
+        d = zscale(warp_sum(d), kap);
+        for (int i = j + lane; i < m; i += 32) y[i] = zsub(y[i], zmul(d, x[i]));
+      }
+    }
+    half_bar(id);
+  }
+}

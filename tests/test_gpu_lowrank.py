@@ -14,7 +14,7 @@ def _lr(rng, m, n, r, decay=0.5):
     return U * (decay ** np.arange(r)), V
 
 
-@pytest.mark.parametrize("m,n,k", [(30, 40, 5), (192, 192, 40), (384, 384, 90), (192, 384, 150),
+@pytest.mark.parametrize("m,n,k", [(30, 40, 5), (192, 192, 40), (384, 384, 90), (192, 384, 150), (108, 108, 40), (108, 108, 80), (108, 108, 120), (108, 54, 70),
                                    (60, 50, 80)])
 def test_truncate_matches_numpy(m, n, k):
     from oracle.hcompress import truncate
