@@ -170,9 +170,9 @@ struct Recorder {
     for (const Access& w : wr)
       if (w.buf >= 0) ent[w.buf].push_back(Entry{w, lvl, true});
     for (const Access& w : wr)
-      if (w.buf >= 0 && ent[w.buf].size() > 256) collapse(w.buf);
+      if (w.buf >= 0 && ent[w.buf].size() > 24) collapse(w.buf);
     for (const Access& r : rd)
-      if (r.buf >= 0 && ent[r.buf].size() > 256) collapse(r.buf);
+      if (r.buf >= 0 && ent[r.buf].size() > 24) collapse(r.buf);
     tasks.push_back(Task{kind, idx, lvl});
   }
   void accs_of(const Mat& m, std::vector<Access>& v) const {
