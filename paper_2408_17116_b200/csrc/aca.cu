@@ -379,9 +379,33 @@ static void hmatrix_build(cbie_hmat* H, int n_leaf) {
       retry_idx.push_back((int)a);
       retry.push_back(aca[a]);
     }
-  DBuf<zc> retry_arena;
   if (!retry.empty()) {
-    throw cbie_error(CBIE_EINVALID, "ACA rank above 128 (capacity retry not implemented)");
+    // grow the arena (device-to-device copy) and rerun those blocks with the full
+    // budget as scratch capacity: the reference's ACA has no capacity limit
+    int64_t extra = 0;
+    for (auto& d : retry) extra += (int64_t)(d.m + d.n) * (d.budget + 1);
+    DBuf<zc> bigger;
+    bigger.alloc(H->arena.n + extra);
+    CK(cudaMemcpyAsync(bigger.p, H->arena.p, sizeof(zc) * H->arena.n, cudaMemcpyDeviceToDevice, s));
+    int64_t o = (int64_t)H->arena.n;
+    for (size_t q = 0; q < retry.size(); ++q) {
+      AcaDesc& d = retry[q];
+      d.kmax = d.budget;
+      d.off_u = o;
+      o += (int64_t)d.m * (d.kmax + 1);
+      d.off_v = o;
+      o += (int64_t)d.n * (d.kmax + 1);
+      aca[retry_idx[q]] = d;
+    }
+    std::swap(bigger.p, H->arena.p);
+    std::swap(bigger.n, H->arena.n);
+    DBuf<int> d_st2;
+    d_st2.alloc(retry.size());
+    launch_aca(H, retry, H->arena.p, d_st2.p);
+    std::vector<int> st2(retry.size());
+    CK(cudaMemcpy(st2.data(), d_st2.p, sizeof(int) * retry.size(), cudaMemcpyDeviceToHost));
+    for (size_t q = 0; q < retry.size(); ++q) status[retry_idx[q]] = st2[q];
+    H->stat["aca_retries"] = (double)retry.size();
   }
   const double aca_ms = tm.stop_ms(s);
   // ---- recompression of converged blocks ----
@@ -407,6 +431,7 @@ static void hmatrix_build(cbie_hmat* H, int n_leaf) {
     d.out_slot = aca_leaf[a];
     td.push_back(d);
     kmax = std::max(kmax, std::min(aca[a].kmax + 1, std::max(L.m, L.n)));
+    if (kmax > 384) kmax = 384;
   }
   DBuf<TruncDesc> dtd;
   dtd.upload(td, s);

@@ -15,6 +15,7 @@ constexpr int SMEM_J = 64;   // cores up to 64 x 64 run the Jacobi SVD in shared
 __device__ int prof_onesided_flag_dev = 0;
 
 constexpr int KEXACT = 64;    // concatenated ranks above this use the randomized path
+constexpr int RLMAX = 192;    // largest sketch (cores above SMEM_J run in global scratch)
 constexpr int RL0 = 48;       // initial sketch size (accepts ranks <= 32 in one attempt)
 
 __device__ __forceinline__ double hash_u(uint32_t a, uint32_t b, uint32_t c) {
@@ -63,12 +64,14 @@ __device__ bool rand_truncate(const TruncDesc& d, zc* arena, int* ranks, int k, 
   const int m = d.m, n = d.n;
   const zc* U = arena + d.in_u;
   const zc* Vt = arena + d.in_v;
-  const int lmax = min(SMEM_J, min(m, n));
+  const int lmax = min(RLMAX, min(min(m, n), k));
   int l = min(RL0, lmax);
-  zc* Y = sc;                         // m x lmax  (becomes Q)
-  zc* Z = Y + (int64_t)m * SMEM_J;    // n x lmax  (becomes Bt, then its reflectors)
-  zc* T = Z + (int64_t)n * SMEM_J;    // k x lmax
-  zc* Om = T + (int64_t)k * SMEM_J;   // n x lmax  (Omega, then Q2 output staging)
+  zc* Y = sc;                         // m x RLMAX (becomes Q's reflectors)
+  zc* Z = Y + (int64_t)m * RLMAX;     // n x RLMAX (becomes Bt, then its reflectors)
+  zc* T = Z + (int64_t)n * RLMAX;     // k x RLMAX
+  zc* Om = T + (int64_t)k * RLMAX;    // n x RLMAX (Omega)
+  zc* Mg = Om + (int64_t)(n + m) * RLMAX;   // RLMAX^2 core (global, for l > SMEM_J)
+  zc* Wg = Mg + (int64_t)RLMAX * RLMAX;
   (void)scper;
   for (int attempt = 0;; ++attempt) {
     for (int64_t e = threadIdx.x; e < (int64_t)n * l; e += LR_NT)
@@ -88,7 +91,7 @@ __device__ bool rand_truncate(const TruncDesc& d, zc* arena, int* ranks, int k, 
     }
     cta_qr(Y, m, l, m, rdv, kapv, red);
     // explicit Q (m x l) into Om (reuse, needs m <= n? use Z's region? ) -> stage in Om2
-    zc* Q = Om + (int64_t)n * SMEM_J;  // m x l (extra region)
+    zc* Q = Om + (int64_t)n * RLMAX;   // m x l (explicit Q)
     for (int64_t e = threadIdx.x; e < (int64_t)m * l; e += LR_NT) {
       const int i = (int)(e % m), c = (int)(e / m);
       Q[e] = zmk(i == c ? 1.0 : 0.0, 0.0);
@@ -102,18 +105,19 @@ __device__ bool rand_truncate(const TruncDesc& d, zc* arena, int* ranks, int k, 
     cta_gemm_tiled(Z, n, Vt, d.ldv, 0, T, k, n, k, l, gsm);    // Z = Bt (n x l)
     // exact SVD of B = R2^T Q2^T:  QR(Bt) = Q2 R2, core M = R2^T (l x l)
     cta_qr(Z, n, l, n, rdv, kapv, red);
+    zc* Mj = l <= SMEM_J ? Ms : Mg;
+    zc* Wj = l <= SMEM_J ? Ws : Wg;
     for (int e = threadIdx.x; e < l * l; e += LR_NT) {
       const int a = e % l, b = e / l;   // M[a][b] = R2[b][a]
-      Ms[e] = a == b ? rdv[a] : (a > b ? Z[(int64_t)a * n + b] : zmk(0.0, 0.0));
+      Mj[e] = a == b ? rdv[a] : (a > b ? Z[(int64_t)a * n + b] : zmk(0.0, 0.0));
     }
     __syncthreads();
-    cta_jacobi(Ms, l, l, l, Ws, l, flag, red);
+    cta_jacobi_hw(Mj, l, l, l, Wj, l, flag, red);
     for (int c = threadIdx.x; c < l; c += LR_NT) {
       double sq = 0.0;
-      for (int i = 0; i < l; ++i) sq += zabs2(Ms[c * l + i]);
+      for (int i = 0; i < l; ++i) sq += zabs2(Mj[c * l + i]);
       sig[c] = sqrt(sq);
-    }
-    __syncthreads();
+    }    __syncthreads();
     for (int c = threadIdx.x; c < l; c += LR_NT) {
       int pos = 0;
       for (int o = 0; o < l; ++o)
@@ -128,7 +132,7 @@ __device__ bool rand_truncate(const TruncDesc& d, zc* arena, int* ranks, int k, 
         if (sig[c] > tol * s0) ++r;
       r = max(r, 1);
     }
-    if (!(r <= l - 16)) {   // sketch too small: grow, or give up (exact path)
+    if (!(r <= l - 16) && l < min(min(m, n), k)) {   // sketch too small: grow or give up
       if (l >= lmax) return false;
       l = min(2 * l, lmax);
       __syncthreads();
@@ -143,7 +147,7 @@ __device__ bool rand_truncate(const TruncDesc& d, zc* arena, int* ranks, int k, 
     zc* Vo = arena + d.out_v;
     for (int64_t e = threadIdx.x; e < (int64_t)m * r; e += LR_NT) {
       const int i = (int)(e % m), c = (int)(e / m);
-      const zc* mc = Ms + order[c] * l;
+      const zc* mc = Mj + order[c] * l;
       zc s = zmk(0.0, 0.0);
       for (int a = 0; a < l; ++a) zfma(s, Q[(int64_t)a * m + i], mc[a]);
       Uo[e] = s;
@@ -151,7 +155,7 @@ __device__ bool rand_truncate(const TruncDesc& d, zc* arena, int* ranks, int k, 
     // Vt' = Q2 [conj(W[:, order[:r]]); 0]
     for (int64_t e = threadIdx.x; e < (int64_t)n * r; e += LR_NT) {
       const int j = (int)(e % n), c = (int)(e / n);
-      Vo[e] = j < l ? zconj(Ws[order[c] * l + j]) : zmk(0.0, 0.0);
+      Vo[e] = j < l ? zconj(Wj[order[c] * l + j]) : zmk(0.0, 0.0);
     }
     __syncthreads();
     cta_apply_q(Z, n, l, n, kapv, Vo, r, n);
@@ -170,12 +174,15 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
   __shared__ double red[LR_NW];
   __shared__ int flag;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  zc* rd1 = reinterpret_cast<zc*>(smem_raw);
+  // per-CTA vectors (reflector scalars, singular values, order) live at the end of
+  // the CTA's global scratch slot so the shared memory stays free for the cores
+  zc* rd1 = scratch + (int64_t)blockIdx.x * scratch_per + (scratch_per - 4 * (int64_t)KS);
   zc* rd2 = rd1 + KS;
   double* kap1 = reinterpret_cast<double*>(rd2 + KS);
   double* kap2 = kap1 + KS;
   double* sig = kap2 + KS;
   int* order = reinterpret_cast<int*>(sig + KS);
+  unsigned char* smem_base = smem_raw;
 
   const int m = d.m, n = d.n;
   if (d.skip_slot >= 0 && ranks[d.skip_slot] == 0) return;
@@ -186,8 +193,7 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
     return;
   }
   if (!ident && k > KEXACT && min(m, n) > 2 * RL0) {
-    zc* Ms = reinterpret_cast<zc*>(order + KS);
-    Ms = reinterpret_cast<zc*>((reinterpret_cast<uintptr_t>(Ms) + 15) & ~uintptr_t(15));
+    zc* Ms = reinterpret_cast<zc*>(smem_base);
     zc* Ws = Ms + SMEM_J * SMEM_J;
     zc* sc = scratch + (int64_t)blockIdx.x * scratch_per;
     const long long tr0 = clock64();
@@ -246,8 +252,7 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
     // QR-preconditioned one-sided Jacobi (M = Q_M R, Jacobi on R^H), all in shared
     // memory: converges in a few sweeps instead of ~11.
     precond = true;
-    Ms = reinterpret_cast<zc*>(order + KS);
-    Ms = reinterpret_cast<zc*>((reinterpret_cast<uintptr_t>(Ms) + 15) & ~uintptr_t(15));
+    Ms = reinterpret_cast<zc*>(smem_base);
     Bs = Ms + SMEM_J * SMEM_J;
     Js = Bs + SMEM_J * SMEM_J;
     zc* rdM = Js + SMEM_J * SMEM_J;
@@ -273,8 +278,7 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
     __syncthreads();
   } else if (kk1 <= SMEM_J && kk2 <= SMEM_J) {
     // one-sided Jacobi with M and W resident in shared memory
-    zc* Mss = reinterpret_cast<zc*>(order + KS);
-    Mss = reinterpret_cast<zc*>((reinterpret_cast<uintptr_t>(Mss) + 15) & ~uintptr_t(15));
+    zc* Mss = reinterpret_cast<zc*>(smem_base);
     zc* Wss = Mss + SMEM_J * SMEM_J;
     for (int e = threadIdx.x; e < kk1 * kk2; e += LR_NT) Mss[e] = M[e];
     __syncthreads();
@@ -388,19 +392,20 @@ void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int
                      unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, int kc_max,
                      int mn_max) {
   if (nd == 0) return;
-  kmax = std::max(std::max(kmax, 1), SMEM_J);
+  kmax = std::max(std::max(kmax, 1), RLMAX);
   const int64_t per = std::max<int64_t>((int64_t)kmax * kmax * 2,
-                                        (int64_t)SMEM_J * (4 * (int64_t)mn_max + kc_max + 1));
+                                        (int64_t)RLMAX * (4 * (int64_t)mn_max + kc_max + 1) +
+                                            2 * (int64_t)RLMAX * RLMAX) +
+                      4 * (int64_t)kmax;
   // waves keep the Jacobi scratch bounded (<= 1 GiB); the buffer is reused across calls
   const int wave = (int)std::max<int64_t>(1, ((int64_t)1 << 30) / (per * (int64_t)sizeof(zc)));
   const size_t need = (size_t)std::min(wave, nd) * per;
   if (scratch.n < need) scratch.alloc(need);
   // exact path: Ms, Bs, Js (3 x 64^2) + rdM/kapM; randomized path: Ms, Ws + GEMM tiles
-  const size_t smem = (size_t)kmax * (2 * sizeof(zc) + 3 * sizeof(double) + sizeof(int)) + 16 +
-                      std::max((size_t)SMEM_J * SMEM_J * 3 * sizeof(zc) + SMEM_J * (sizeof(zc) + sizeof(double)),
+  const size_t smem = std::max((size_t)SMEM_J * SMEM_J * 3 * sizeof(zc) + SMEM_J * (sizeof(zc) + sizeof(double)),
                                (size_t)SMEM_J * SMEM_J * 2 * sizeof(zc) +
                                    (size_t)TG_K * (TG_R + 1 + 65) * sizeof(zc));
-  if (smem > 220 * 1024) throw cbie_error(CBIE_EINVALID, "truncation dimension too large");
+  if (smem > 232448 - 2048) throw cbie_error(CBIE_EINVALID, "truncation dimension too large");
   CK(cudaFuncSetAttribute(k_truncate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (int b0 = 0; b0 < nd; b0 += wave) {
     int nb = std::min(wave, nd - b0);
