@@ -14,7 +14,8 @@ namespace {
 constexpr int SMEM_J = 64;   // cores up to 64 x 64 run the Jacobi SVD in shared memory
 __device__ int prof_onesided_flag_dev = 0;
 
-constexpr int KEXACT = 64;    // concatenated ranks above this use the randomized path
+constexpr int KEXACT = 64;    // cores up to this size run in shared memory
+constexpr int KRAND = 128;    // concatenated ranks above this use the randomized path
 constexpr int RLMAX = 192;    // largest sketch (cores above SMEM_J run in global scratch)
 constexpr int RL0 = 48;       // initial sketch size (accepts ranks <= 32 in one attempt)
 
@@ -65,7 +66,8 @@ __device__ bool rand_truncate(const TruncDesc& d, zc* arena, int* ranks, int k, 
   const zc* U = arena + d.in_u;
   const zc* Vt = arena + d.in_v;
   const int lmax = min(RLMAX, min(min(m, n), k));
-  int l = min(RL0, lmax);
+  // first sketch sized from k: a concatenation [U1 U2] typically keeps ~k/2
+  int l = min(lmax, max(RL0, ((k * 5 / 8 + 16 + 15) / 16) * 16));
   zc* Y = sc;                         // m x RLMAX (becomes Q's reflectors)
   zc* Z = Y + (int64_t)m * RLMAX;     // n x RLMAX (becomes Bt, then its reflectors)
   zc* T = Z + (int64_t)n * RLMAX;     // k x RLMAX
@@ -192,7 +194,7 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
     if (threadIdx.x == 0) ranks[d.out_slot] = 0;
     return;
   }
-  if (!ident && k > KEXACT && min(m, n) > 2 * RL0) {
+  if (!ident && k > KRAND && min(m, n) > 2 * RL0) {
     zc* Ms = reinterpret_cast<zc*>(smem_base);
     zc* Ws = Ms + SMEM_J * SMEM_J;
     zc* sc = scratch + (int64_t)blockIdx.x * scratch_per;
@@ -248,23 +250,36 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
   zc* Bs = nullptr;
   zc* Js = nullptr;
   double* kapM = nullptr;
-  if (kk1 <= SMEM_J && kk2 <= SMEM_J && kk1 >= kk2 && !ident) {
-    // QR-preconditioned one-sided Jacobi (M = Q_M R, Jacobi on R^H), all in shared
-    // memory: converges in a few sweeps instead of ~11.
+  if (kk1 >= kk2 && !ident) {
+    // QR-preconditioned one-sided Jacobi (M = Q_M R, Jacobi on R^H): a few sweeps
+    // instead of ~11.  Cores up to 64 x 64 live in shared memory, larger ones in
+    // the CTA's global scratch slot (after M and W).
     precond = true;
-    Ms = reinterpret_cast<zc*>(smem_base);
-    Bs = Ms + SMEM_J * SMEM_J;
-    Js = Bs + SMEM_J * SMEM_J;
-    zc* rdM = Js + SMEM_J * SMEM_J;
-    kapM = reinterpret_cast<double*>(rdM + SMEM_J);
+    const bool small = kk1 <= SMEM_J && kk2 <= SMEM_J;
+    if (small) {
+      Ms = reinterpret_cast<zc*>(smem_base);
+      Bs = Ms + SMEM_J * SMEM_J;
+      Js = Bs + SMEM_J * SMEM_J;
+    } else {
+      Ms = W + (int64_t)KS * KS;
+      Bs = Ms + (int64_t)KS * KS;
+      Js = Bs + (int64_t)KS * KS;
+    }
+    zc* rdQ = reinterpret_cast<zc*>(Js + (small ? SMEM_J * SMEM_J : (int64_t)KS * KS));
+    double* kpQ = reinterpret_cast<double*>(rdQ + KS);
+    if (small) {   // the small-core scalars stay in shared memory
+      rdQ = reinterpret_cast<zc*>(Js + SMEM_J * SMEM_J);
+      kpQ = reinterpret_cast<double*>(rdQ + SMEM_J);
+    }
+    kapM = kpQ;
     for (int e = threadIdx.x; e < kk1 * kk2; e += LR_NT) Ms[e] = M[e];
     __syncthreads();
-    cta_qr(Ms, kk1, kk2, kk1, rdM, kapM, red);
-    // A = R^H (kk2 x kk2): A[i][j] = conj(R[j][i]), R upper (diag rdM, strict upper in Ms)
+    cta_qr(Ms, kk1, kk2, kk1, rdQ, kapM, red);
+    // A = R^H (kk2 x kk2): A[i][j] = conj(R[j][i]), R upper (diag rdQ, strict upper in Ms)
     for (int e = threadIdx.x; e < kk2 * kk2; e += LR_NT) {
       const int i = e % kk2, j = e / kk2;
       zc v = zmk(0.0, 0.0);
-      if (i == j) v = zconj(rdM[i]);
+      if (i == j) v = zconj(rdQ[i]);
       else if (i > j) v = zconj(Ms[i * kk1 + j]);
       Bs[j * kk2 + i] = v;
     }
@@ -393,7 +408,7 @@ void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int
                      int mn_max) {
   if (nd == 0) return;
   kmax = std::max(std::max(kmax, 1), RLMAX);
-  const int64_t per = std::max<int64_t>((int64_t)kmax * kmax * 2,
+  const int64_t per = std::max<int64_t>((int64_t)kmax * kmax * 5 + 2 * (int64_t)kmax,
                                         (int64_t)RLMAX * (4 * (int64_t)mn_max + kc_max + 1) +
                                             2 * (int64_t)RLMAX * RLMAX) +
                       4 * (int64_t)kmax;
