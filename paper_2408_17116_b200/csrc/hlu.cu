@@ -1207,9 +1207,18 @@ static void hlu_factor_impl(cbie_hlu* F) {
   Recorder R;
   R.tol = F->tol;
   R.leaf_end = leaf_end;
-  // temporaries before chunk reuse (GiB, CBIE_POOL_GB overrides)
-  R.pool_budget = (int64_t)((getenv("CBIE_POOL_GB") ? atof(getenv("CBIE_POOL_GB")) : 8.0) *
-                            (double)(1ll << 30)) / (int64_t)sizeof(zc);
+  // temporaries before chunk reuse: most of the free HBM after the factor copy (a
+  // reused chunk orders its new owner after every earlier access, which costs
+  // parallelism), CBIE_POOL_GB overrides
+  {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    double gb = 0.7 * ((double)fr - (double)leaf_end * sizeof(zc)) / (double)(1ll << 30) - 4.0;
+    gb = std::max(4.0, std::min(gb, 120.0));
+    if (getenv("CBIE_POOL_GB")) gb = atof(getenv("CBIE_POOL_GB"));
+    R.pool_budget = (int64_t)(gb * (double)(1ll << 30)) / (int64_t)sizeof(zc);
+    F->stat["pool_budget_gb"] = gb;
+  }
   for (int li = 0; li < nleaf; ++li) {
     R.new_buf();
     R.new_slot(0, li);
@@ -1241,6 +1250,15 @@ static void hlu_factor_impl(cbie_hlu* F) {
   tm.start(s);
   Exec ex = execute(R, F->arena.p, F->ranks.p, F->piv.p, F->rcond.p, flag.p, ovf.p, scratch, F->tol, s);
   F->stat["factor_device_ms"] = tm.stop_ms(s);
+  {
+    // keep only the factor storage; the temporary pool is released
+    DBuf<zc> compact;
+    compact.alloc((size_t)leaf_end + 1);
+    CK(cudaMemcpyAsync(compact.p, F->arena.p, sizeof(zc) * leaf_end, cudaMemcpyDeviceToDevice, s));
+    CK(cudaStreamSynchronize(s));
+    std::swap(compact.p, F->arena.p);
+    std::swap(compact.n, F->arena.n);
+  }
   int hflag = 0;
   unsigned long long hovf = 0;
   CK(cudaMemcpy(&hflag, flag.p, sizeof(int), cudaMemcpyDeviceToHost));

@@ -119,3 +119,25 @@ def test_chebyshev_sample_patches_match_oracle():
                           ph.Form("mfie", ph.Medium.relative(1.0, 1.0, 1.0)))
     B = d.dense()
     assert np.abs(A - B).max() <= TOL * np.abs(B).max()
+
+
+def test_star_chart_frames_match_finite_differences():
+    """Config-4 star chart on the device: positions equal the host chart, tangents
+    equal central differences of the host chart."""
+    from paper_2408_17116_b200 import geometry as geo, kernels as ker
+    from paper_2408_17116_b200.assembly import GpuGenerator
+    coef, _ = geo.star_coefficients(2408)
+    patches = geo.star_patches(2.5, 0, (5, 5), coef)
+    spec = ker.FormulationSpec(ker.MFIE_PEC, ker.Medium.from_relative(1.0, 1.0, 1.0))
+    gen = GpuGenerator(patches, spec)
+    xu = geo.fejer_nodes(5)
+    uu, vv = np.tile(xu, 5), np.repeat(xu, 5)
+    h = 1e-6
+    for q, p in enumerate(patches):
+        ch = p.chart
+        sl = slice(q * 25, (q + 1) * 25)
+        assert np.abs(gen.pos[sl] - ch.positions(uu, vv)).max() < 1e-13
+        du = (ch.positions(uu + h, vv) - ch.positions(uu - h, vv)) / (2 * h)
+        dv = (ch.positions(uu, vv + h) - ch.positions(uu, vv - h)) / (2 * h)
+        assert np.abs(gen.a_u[sl] - du).max() < 1e-7
+        assert np.abs(gen.a_v[sl] - dv).max() < 1e-7
