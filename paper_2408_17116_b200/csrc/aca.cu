@@ -263,6 +263,27 @@ __global__ void k_gather_rows(const int32_t* __restrict__ rptr, const int64_t* _
 }  // namespace
 
 // ---------------------------------------------------------------------------
+// segment gather (staging -> arena)
+// ---------------------------------------------------------------------------
+__global__ void k_copy_segments(const CopySeg* __restrict__ segs, const zc* __restrict__ src,
+                                zc* __restrict__ dst) {
+  const CopySeg g = segs[blockIdx.x];
+  for (int64_t e = threadIdx.x; e < g.count; e += blockDim.x) dst[g.dst + e] = src[g.src + e];
+}
+
+void launch_copy_segments(const std::vector<CopySeg>& segs, const zc* src, zc* dst, cudaStream_t s) {
+  if (segs.empty()) return;
+  DBuf<CopySeg> d;
+  d.upload(segs, s);
+  for (size_t b0 = 0; b0 < segs.size(); b0 += 65535) {
+    const int nb = (int)std::min<size_t>(65535, segs.size() - b0);
+    k_copy_segments<<<nb, 256, 0, s>>>(d.p + b0, src, dst);
+    CKL();
+  }
+  CK(cudaStreamSynchronize(s));
+}
+
+// ---------------------------------------------------------------------------
 // build driver
 // ---------------------------------------------------------------------------
 static int aca_budget(int m, int n) { return std::max(1, std::min(m, n) / 2); }
@@ -306,48 +327,24 @@ static void hmatrix_build(cbie_hmat* H, int n_leaf) {
   H->stat["tree_ms"] = std::chrono::duration<double, std::milli>(t1 - t0).count();
   H->N = c->N;
   const int nleaf = (int)T.leaves.size();
-  // ---- storage plan: dense leaves m x n, LR leaves U m x cap + Vt n x cap ----
-  int64_t off = 0;
-  for (auto& L : T.leaves) {
+  // ---- storage: dense leaves first (m x n each); low-rank leaves are appended
+  // wave by wave with their EXACT ranks (U m x r, Vt n x r), so the arena holds
+  // sum (m+n) r instead of (m+n) * budget (config 5: ~20 GB instead of ~1.5 TB) ----
+  int64_t used = 0;
+  for (auto& L : T.leaves)
     if (L.kind == BLK_DENSE) {
-      L.off_d = off;
-      off += (int64_t)L.m * L.n;
-    } else {
-      L.cap = aca_budget(L.m, L.n);
-      L.off_u = off;
-      off += (int64_t)L.m * L.cap;
-      L.off_v = off;
-      off += (int64_t)L.n * L.cap;
+      L.off_d = used;
+      used += (int64_t)L.m * L.n;
     }
-  }
-  // ACA scratch (U m x (kmax+1), Vt n x (kmax+1)) behind the leaf storage
-  const int KCAP = 128;
-  std::vector<AcaDesc> aca;
+  int64_t lr_guess = 0;
+  for (auto& L : T.leaves)
+    if (L.kind == BLK_LR) lr_guess += (int64_t)(L.m + L.n) * 24;
+  H->arena.alloc(std::max<int64_t>(used + lr_guess, 1));
   std::vector<int> aca_leaf;
-  int64_t scratch0 = off;
-  for (int li = 0; li < nleaf; ++li) {
-    auto& L = T.leaves[li];
-    if (L.kind != BLK_LR) continue;
-    AcaDesc d;
-    const Cluster &R = T.cl[L.r], &Cc = T.cl[L.c];
-    d.r_lo = R.lo;
-    d.r_hi = R.hi;
-    d.c_lo = Cc.lo;
-    d.c_hi = Cc.hi;
-    d.m = L.m;
-    d.n = L.n;
-    d.budget = aca_budget(L.m, L.n);
-    d.kmax = std::min(d.budget, KCAP);
-    d.off_u = off;
-    off += (int64_t)L.m * (d.kmax + 1);
-    d.off_v = off;
-    off += (int64_t)L.n * (d.kmax + 1);
-    d.k_slot = nleaf + (int)aca.size();
-    aca.push_back(d);
-    aca_leaf.push_back(li);
-  }
-  H->arena.alloc(std::max<int64_t>(off, 1));
-  H->rank.alloc(nleaf + aca.size() + 1);
+  for (int li = 0; li < nleaf; ++li)
+    if (T.leaves[li].kind == BLK_LR) aca_leaf.push_back(li);
+  const int nadm = (int)aca_leaf.size();
+  H->rank.alloc(nleaf + nadm + 1);
   CK(cudaMemsetAsync(H->rank.p, 0, sizeof(int) * H->rank.n, s));
   H->d_pperm.upload(T.pperm, s);
   EvTimer tm;
@@ -363,117 +360,184 @@ static void hmatrix_build(cbie_hmat* H, int n_leaf) {
   dt.upload(tiles, s);
   launch_fill_tiles(c, dt.p, (int)tiles.size(), H->d_pperm.p, H->arena.p, 1, s);
   const double dense_ms = tm.stop_ms(s);
-  // ---- ACA ----
-  tm.start(s);
-  DBuf<int> d_status;
-  d_status.alloc(std::max<size_t>(aca.size(), 1));
-  launch_aca(H, aca, H->arena.p, d_status.p);
-  std::vector<int> status(aca.size());
-  if (!aca.empty())
-    CK(cudaMemcpy(status.data(), d_status.p, sizeof(int) * aca.size(), cudaMemcpyDeviceToHost));
-  // retry capacity misses with the full budget
-  std::vector<AcaDesc> retry;
-  std::vector<int> retry_idx;
-  for (size_t a = 0; a < aca.size(); ++a)
-    if (status[a] == 2) {
-      retry_idx.push_back((int)a);
-      retry.push_back(aca[a]);
-    }
-  if (!retry.empty()) {
-    // grow the arena (device-to-device copy) and rerun those blocks with the full
-    // budget as scratch capacity: the reference's ACA has no capacity limit
-    int64_t extra = 0;
-    for (auto& d : retry) extra += (int64_t)(d.m + d.n) * (d.budget + 1);
+  auto grow = [&](int64_t need) {
+    if (need <= (int64_t)H->arena.n) return;
     DBuf<zc> bigger;
-    bigger.alloc(H->arena.n + extra);
-    CK(cudaMemcpyAsync(bigger.p, H->arena.p, sizeof(zc) * H->arena.n, cudaMemcpyDeviceToDevice, s));
-    int64_t o = (int64_t)H->arena.n;
-    for (size_t q = 0; q < retry.size(); ++q) {
-      AcaDesc& d = retry[q];
-      d.kmax = d.budget;
-      d.off_u = o;
-      o += (int64_t)d.m * (d.kmax + 1);
-      d.off_v = o;
-      o += (int64_t)d.n * (d.kmax + 1);
-      aca[retry_idx[q]] = d;
-    }
+    bigger.alloc(std::max<int64_t>(need, (int64_t)(1.5 * (double)H->arena.n)));
+    CK(cudaMemcpyAsync(bigger.p, H->arena.p, sizeof(zc) * used, cudaMemcpyDeviceToDevice, s));
     std::swap(bigger.p, H->arena.p);
     std::swap(bigger.n, H->arena.n);
-    DBuf<int> d_st2;
-    d_st2.alloc(retry.size());
-    launch_aca(H, retry, H->arena.p, d_st2.p);
-    std::vector<int> st2(retry.size());
-    CK(cudaMemcpy(st2.data(), d_st2.p, sizeof(int) * retry.size(), cudaMemcpyDeviceToHost));
-    for (size_t q = 0; q < retry.size(); ++q) status[retry_idx[q]] = st2[q];
-    H->stat["aca_retries"] = (double)retry.size();
-  }
-  const double aca_ms = tm.stop_ms(s);
-  // ---- recompression of converged blocks ----
-  tm.start(s);
-  std::vector<TruncDesc> td;
-  int kmax = 1;
-  for (size_t a = 0; a < aca.size(); ++a) {
-    auto& L = T.leaves[aca_leaf[a]];
-    if (status[a] != 0) continue;
-    TruncDesc d;
-    d.in_u = aca[a].off_u;
-    d.in_v = aca[a].off_v;
-    d.ldu = L.m;
-    d.ldv = L.n;
-    d.skip_slot = -1;
-    d.out_u = L.off_u;
-    d.out_v = L.off_v;
-    d.m = L.m;
-    d.n = L.n;
-    d.k = 0;
-    d.k_slot = aca[a].k_slot;
-    d.cap = L.cap;
-    d.out_slot = aca_leaf[a];
-    td.push_back(d);
-    kmax = std::max(kmax, std::min(aca[a].kmax + 1, std::max(L.m, L.n)));
-    if (kmax > 384) kmax = 384;
-  }
-  DBuf<TruncDesc> dtd;
-  dtd.upload(td, s);
+  };
+  // ---- admissible leaves in waves: ACA -> recompression -> exact-rank append ----
+  const int KCAP = 128;
+  const int64_t wave_elems =
+      (int64_t)((getenv("CBIE_ACA_WAVE_GB") ? atof(getenv("CBIE_ACA_WAVE_GB")) : 8.0) *
+                (double)(1ll << 30)) / (int64_t)sizeof(zc);
+  DBuf<zc> scratch, staging, tscratch;
+  DBuf<int> d_status;
   DBuf<unsigned long long> ovf;
   ovf.alloc(1);
   CK(cudaMemsetAsync(ovf.p, 0, 8, s));
-  DBuf<zc> scratch;
-  int kcm = 1, mnm = 1;
-  for (auto& d : td) {
-    kcm = std::max(kcm, d.cap + 1);
-    mnm = std::max(mnm, std::max(d.m, d.n));
-  }
-  for (auto& a : aca) kcm = std::max(kcm, a.kmax + 1);
-  launch_truncate(H->arena.p, H->rank.p, dtd.p, (int)td.size(), kmax, H->tol, ovf.p, scratch, s,
-                  kcm, mnm);
-  const double trunc_ms = tm.stop_ms(s);
-  // ---- demotion: RankOverflow -> dense leaf (hmatrix.py:259-263) ----
-  std::vector<int> demote;
-  for (size_t a = 0; a < aca.size(); ++a)
-    if (status[a] == 1) demote.push_back(aca_leaf[a]);
-  H->demoted = (int)demote.size();
-  double demote_ms = 0;
-  if (!demote.empty()) {
-    // dense storage for demoted leaves reuses the (now free) ACA scratch region
-    int64_t o = scratch0;
-    std::vector<TileDesc> dtl;
-    for (int li : demote) {
-      auto& L = T.leaves[li];
-      L.kind = BLK_DENSE;
-      T.nodes[L.node].kind = BLK_DENSE;
-      L.off_d = o;
-      o += (int64_t)L.m * L.n;
+  double aca_ms = 0, trunc_ms = 0, demote_ms = 0;
+  int demoted = 0, retries = 0, waves = 0;
+  for (int w0 = 0; w0 < nadm;) {
+    // wave: consecutive admissible leaves whose ACA scratch fits
+    std::vector<AcaDesc> aca;
+    int64_t soff = 0;
+    int w1 = w0;
+    for (; w1 < nadm; ++w1) {
+      const auto& L = T.leaves[aca_leaf[w1]];
+      const int budget = aca_budget(L.m, L.n);
+      const int kmax = std::min(budget, KCAP);
+      const int64_t need = (int64_t)(L.m + L.n) * (kmax + 1);
+      if (w1 > w0 && soff + need > wave_elems) break;
+      AcaDesc d;
       const Cluster &R = T.cl[L.r], &Cc = T.cl[L.c];
-      dtl.push_back(TileDesc{L.off_d, R.lo, R.hi, Cc.lo, Cc.hi});
+      d.r_lo = R.lo;
+      d.r_hi = R.hi;
+      d.c_lo = Cc.lo;
+      d.c_hi = Cc.hi;
+      d.m = L.m;
+      d.n = L.n;
+      d.budget = budget;
+      d.kmax = kmax;
+      d.off_u = soff;
+      soff += (int64_t)L.m * (kmax + 1);
+      d.off_v = soff;
+      soff += (int64_t)L.n * (kmax + 1);
+      d.k_slot = nleaf + w1;
+      aca.push_back(d);
     }
-    if (o > (int64_t)H->arena.n) throw cbie_error(CBIE_EOOM, "demotion storage exceeds scratch");
-    tm.start(s);
-    DBuf<TileDesc> dd;
-    dd.upload(dtl, s);
-    launch_fill_tiles(c, dd.p, (int)dtl.size(), H->d_pperm.p, H->arena.p, 1, s);
-    demote_ms = tm.stop_ms(s);
+    ++waves;
+    EvTimer tw;
+    tw.start(s);
+    if ((int64_t)scratch.n < soff) scratch.alloc(soff);
+    d_status.alloc(std::max<size_t>(aca.size(), 1));
+    launch_aca(H, aca, scratch.p, d_status.p);
+    std::vector<int> status(aca.size());
+    CK(cudaMemcpy(status.data(), d_status.p, sizeof(int) * aca.size(), cudaMemcpyDeviceToHost));
+    // capacity misses: rerun with the full budget in a second scratch region
+    std::vector<AcaDesc> retry;
+    std::vector<int> retry_idx;
+    int64_t roff = soff;
+    for (size_t a = 0; a < aca.size(); ++a)
+      if (status[a] == 2) {
+        AcaDesc d = aca[a];
+        d.kmax = d.budget;
+        d.off_u = roff;
+        roff += (int64_t)d.m * (d.kmax + 1);
+        d.off_v = roff;
+        roff += (int64_t)d.n * (d.kmax + 1);
+        aca[a] = d;
+        retry.push_back(d);
+        retry_idx.push_back((int)a);
+      }
+    if (!retry.empty()) {
+      DBuf<zc> bigger;
+      bigger.alloc(roff);
+      CK(cudaMemcpyAsync(bigger.p, scratch.p, sizeof(zc) * soff, cudaMemcpyDeviceToDevice, s));
+      std::swap(bigger.p, scratch.p);
+      std::swap(bigger.n, scratch.n);
+      DBuf<int> st2;
+      st2.alloc(retry.size());
+      launch_aca(H, retry, scratch.p, st2.p);
+      std::vector<int> s2(retry.size());
+      CK(cudaMemcpy(s2.data(), st2.p, sizeof(int) * retry.size(), cudaMemcpyDeviceToHost));
+      for (size_t q = 0; q < retry.size(); ++q) status[retry_idx[q]] = s2[q];
+      retries += (int)retry.size();
+    }
+    aca_ms += tw.stop_ms(s);
+    // recompression into staging (capacity = the block's ACA capacity: r <= k)
+    tw.start(s);
+    std::vector<TruncDesc> td;
+    std::vector<int> td_block;
+    int64_t stoff = 0;
+    int kmax_t = 1, kcm = 1, mnm = 1;
+    for (size_t a = 0; a < aca.size(); ++a) {
+      if (status[a] != 0) continue;
+      const auto& d = aca[a];
+      TruncDesc t;
+      t.in_u = d.off_u;
+      t.in_v = d.off_v;
+      t.ldu = d.m;
+      t.ldv = d.n;
+      t.skip_slot = -1;
+      t.m = d.m;
+      t.n = d.n;
+      t.k = 0;
+      t.k_slot = d.k_slot;
+      t.cap = std::min(d.kmax + 1, std::min(d.m, d.n));
+      t.out_u = stoff;
+      stoff += (int64_t)d.m * t.cap;
+      t.out_v = stoff;
+      stoff += (int64_t)d.n * t.cap;
+      t.out_slot = aca_leaf[w0 + a];
+      td.push_back(t);
+      td_block.push_back((int)a);
+      kmax_t = std::max(kmax_t, std::min(d.kmax + 1, std::max(d.m, d.n)));
+      kcm = std::max(kcm, d.kmax + 1);
+      mnm = std::max(mnm, std::max(d.m, d.n));
+    }
+    kmax_t = std::min(kmax_t, 384);
+    if ((int64_t)staging.n < stoff) staging.alloc(std::max<int64_t>(stoff, 1));
+    DBuf<TruncDesc> dtd;
+    dtd.upload(td, s);
+    launch_truncate(scratch.p, H->rank.p, dtd.p, (int)td.size(), kmax_t, H->tol, ovf.p, tscratch, s,
+                    kcm, mnm, staging.p);
+    std::vector<int> rk(nleaf);
+    CK(cudaStreamSynchronize(s));   // ranks come from the (non-blocking) library stream
+    CK(cudaMemcpy(rk.data(), H->rank.p, sizeof(int) * nleaf, cudaMemcpyDeviceToHost));
+    // exact-rank append
+    std::vector<CopySeg> segs;
+    int64_t need = used;
+    for (size_t q = 0; q < td.size(); ++q) {
+      const int li = td[q].out_slot;
+      need += (int64_t)(td[q].m + td[q].n) * std::max(rk[li], 1);
+    }
+    grow(need);
+    for (size_t q = 0; q < td.size(); ++q) {
+      const int li = td[q].out_slot;
+      auto& L = T.leaves[li];
+      const int r = rk[li];
+      L.cap = std::max(r, 1);
+      L.off_u = used;
+      used += (int64_t)L.m * L.cap;
+      L.off_v = used;
+      used += (int64_t)L.n * L.cap;
+      if (r > 0) {
+        segs.push_back(CopySeg{td[q].out_u, L.off_u, (int64_t)L.m * r});
+        segs.push_back(CopySeg{td[q].out_v, L.off_v, (int64_t)L.n * r});
+      }
+    }
+    launch_copy_segments(segs, staging.p, H->arena.p, s);
+    trunc_ms += tw.stop_ms(s);
+    // demotion: RankOverflow -> dense leaf (hmatrix.py:259-263)
+    std::vector<TileDesc> dtl;
+    for (size_t a = 0; a < aca.size(); ++a)
+      if (status[a] == 1) {
+        auto& L = T.leaves[aca_leaf[w0 + a]];
+        L.kind = BLK_DENSE;
+        T.nodes[L.node].kind = BLK_DENSE;
+        L.cap = 0;
+        grow(used + (int64_t)L.m * L.n);
+        L.off_d = used;
+        used += (int64_t)L.m * L.n;
+        const Cluster &R = T.cl[L.r], &Cc = T.cl[L.c];
+        dtl.push_back(TileDesc{L.off_d, R.lo, R.hi, Cc.lo, Cc.hi});
+      }
+    if (!dtl.empty()) {
+      tw.start(s);
+      DBuf<TileDesc> dd;
+      dd.upload(dtl, s);
+      launch_fill_tiles(c, dd.p, (int)dtl.size(), H->d_pperm.p, H->arena.p, 1, s);
+      demote_ms += tw.stop_ms(s);
+      demoted += (int)dtl.size();
+    }
+    w0 = w1;
   }
+  H->demoted = demoted;
+  H->stat["aca_retries"] = retries;
+  H->stat["aca_waves"] = waves;
   unsigned long long hovf = 0;
   CK(cudaMemcpy(&hovf, ovf.p, 8, cudaMemcpyDeviceToHost));
   H->overflow = (int64_t)hovf;
@@ -490,13 +554,13 @@ static void hmatrix_build(cbie_hmat* H, int n_leaf) {
   H->stat["demote_fill_ms"] = demote_ms;
   H->stat["fill_ms"] = dense_ms + aca_ms + trunc_ms + demote_ms;
   H->stat["n_leaves"] = nleaf;
-  H->stat["n_dense"] = (double)tiles.size() + demote.size();
-  H->stat["n_lowrank"] = (double)(aca.size() - demote.size());
-  H->stat["demoted"] = (double)demote.size();
+  H->stat["n_dense"] = (double)tiles.size() + demoted;
+  H->stat["n_lowrank"] = (double)(nadm - demoted);
+  H->stat["demoted"] = (double)demoted;
   H->stat["trunc_overflow"] = (double)hovf;
   H->stat["stored_scalars"] = (double)stored;
   H->stat["compression_rate"] = 1.0 - (double)stored / ((double)H->N * (double)H->N);
-  H->stat["arena_bytes"] = (double)H->arena.n * sizeof(zc);
+  H->stat["arena_bytes"] = (double)used * sizeof(zc);
 }
 
 // ---------------------------------------------------------------------------

@@ -1189,11 +1189,29 @@ static void hlu_factor_impl(cbie_hlu* F) {
   F->tree = H->tree;
   Tree& T = F->tree;
   const int nleaf = (int)T.leaves.size();
-  // leaf storage region of H (everything below the first ACA scratch offset)
+  // factor storage: the H-matrix keeps exact ranks; the factors get room to grow
+  // (cap = min(budget, 2 r + 48); truncations clipped at cap are counted)
+  std::vector<CopySeg> segs;
   int64_t leaf_end = 0;
-  for (auto& L : T.leaves) {
-    if (L.kind == BLK_DENSE) leaf_end = std::max(leaf_end, L.off_d + (int64_t)L.m * L.n);
-    else leaf_end = std::max(leaf_end, L.off_v + (int64_t)L.n * L.cap);
+  for (int li = 0; li < nleaf; ++li) {
+    auto& L = T.leaves[li];
+    const auto& L0 = H->tree.leaves[li];
+    if (L.kind == BLK_DENSE) {
+      L.off_d = leaf_end;
+      leaf_end += (int64_t)L.m * L.n;
+      segs.push_back(CopySeg{L0.off_d, L.off_d, (int64_t)L.m * L.n});
+    } else {
+      const int r = H->h_rank[li];
+      L.cap = std::max(1, std::min(std::max(1, std::min(L.m, L.n) / 2), 2 * r + 48));
+      L.off_u = leaf_end;
+      leaf_end += (int64_t)L.m * L.cap;
+      L.off_v = leaf_end;
+      leaf_end += (int64_t)L.n * L.cap;
+      if (r > 0) {
+        segs.push_back(CopySeg{L0.off_u, L.off_u, (int64_t)L.m * r});
+        segs.push_back(CopySeg{L0.off_v, L.off_v, (int64_t)L.n * r});
+      }
+    }
   }
   // pivots for dense diagonal leaves
   F->pivoff.assign(nleaf, -1);
@@ -1231,7 +1249,7 @@ static void hlu_factor_impl(cbie_hlu* F) {
   F->stat["record_ms"] = std::chrono::duration<double, std::milli>(t1 - t0).count();
   // device state: arena = copy of the leaf storage + temporaries
   F->arena.alloc((size_t)(leaf_end + R.pool_top + 1));
-  CK(cudaMemcpyAsync(F->arena.p, H->arena.p, sizeof(zc) * leaf_end, cudaMemcpyDeviceToDevice, s));
+  launch_copy_segments(segs, H->arena.p, F->arena.p, s);
   std::vector<int> r0 = R.init_ranks;
   for (int li = 0; li < nleaf; ++li) r0[li] = H->h_rank[li];
   F->ranks.upload(r0, s);

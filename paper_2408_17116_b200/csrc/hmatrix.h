@@ -78,10 +78,17 @@ struct TruncDesc {
   int out_slot;                // ranks[out_slot] <- r
 };
 // kmax >= every min(m,k), min(n,k) (dense mode: min(m,n) and n) in the batch
-// kc_max / mn_max: largest concatenated capacity and max(m, n) (randomized-path scratch)
+// kc_max / mn_max: largest concatenated capacity and max(m, n) (randomized-path scratch);
+// arena_out (if non-null) receives the outputs (out_u / out_v offsets are relative to it)
 void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
                      unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s,
-                     int kc_max = 0, int mn_max = 0);
+                     int kc_max = 0, int mn_max = 0, zc* arena_out = nullptr);
+
+// contiguous segment copies src[src + i] -> dst[dst + i] (aca.cu)
+struct CopySeg {
+  int64_t src, dst, count;
+};
+void launch_copy_segments(const std::vector<CopySeg>& segs, const zc* src, zc* dst, cudaStream_t s);
 
 // lowrank.cu: dense block -> (Q, B) by an adaptive randomized range finder
 struct DenseLRDesc {

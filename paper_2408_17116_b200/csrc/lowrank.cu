@@ -58,7 +58,7 @@ __device__ __forceinline__ void cta_gemm_small(zc* C, int ldc, const zc* A, int 
 // adaptive range finder with one power iteration, exact SVD of the l x l core.
 // Accepts when the sketch shows >= 4 singular values below tol * s0, else
 // doubles l (<= SMEM_J).  Returns false if l would exceed SMEM_J.
-__device__ bool rand_truncate(const TruncDesc& d, zc* arena, int* ranks, int k, zc* sc,
+__device__ bool rand_truncate(const TruncDesc& d, zc* arena, zc* aout, int* ranks, int k, zc* sc,
                               int64_t scper, double tol, zc* rdv, double* kapv, double* sig,
                               int* order, zc* Ms, zc* Ws, double* red, int* flag,
                               unsigned long long* overflow, zc* gsm) {
@@ -145,8 +145,8 @@ __device__ bool rand_truncate(const TruncDesc& d, zc* arena, int* ranks, int k, 
       r = d.cap;
     }
     // U' = Q (M W)[:, order[:r]]   (m x r)
-    zc* Uo = arena + d.out_u;
-    zc* Vo = arena + d.out_v;
+    zc* Uo = aout + d.out_u;
+    zc* Vo = aout + d.out_v;
     for (int64_t e = threadIdx.x; e < (int64_t)m * r; e += LR_NT) {
       const int i = (int)(e % m), c = (int)(e / m);
       const zc* mc = Mj + order[c] * l;
@@ -166,7 +166,7 @@ __device__ bool rand_truncate(const TruncDesc& d, zc* arena, int* ranks, int k, 
   }
 }
 
-__global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
+__global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, zc* aout, int* ranks,
                                                     const TruncDesc* __restrict__ descs,
                                                     zc* scratch, int64_t scratch_per, int KS,
                                                     double tol, unsigned long long* overflow,
@@ -199,7 +199,7 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
     zc* Ws = Ms + SMEM_J * SMEM_J;
     zc* sc = scratch + (int64_t)blockIdx.x * scratch_per;
     const long long tr0 = clock64();
-    const bool ok = rand_truncate(d, arena, ranks, k, sc, scratch_per, tol, rd1, kap1, sig, order, Ms,
+    const bool ok = rand_truncate(d, arena, aout, ranks, k, sc, scratch_per, tol, rd1, kap1, sig, order, Ms,
                                   Ws, red, &flag, overflow, Ws + SMEM_J * SMEM_J);
     if (prof && threadIdx.x == 0) {
       atomicAdd(prof + (ok ? 6 : 8), 1ull);
@@ -335,8 +335,8 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, int* ranks,
     if (threadIdx.x == 0) atomicAdd(overflow, 1ull);
     r = d.cap;
   }
-  zc* Uo = arena + d.out_u;
-  zc* Vo = arena + d.out_v;
+  zc* Uo = aout + d.out_u;
+  zc* Vo = aout + d.out_v;
   if (precond) {
     // U' = Q1 Q_M [J_r Sigma_r; 0],  Vt' = Q2 [conj(B_r) / sigma; 0]
     for (int e = threadIdx.x; e < m * r; e += LR_NT) {
@@ -405,7 +405,8 @@ void trunc_prof_read(unsigned long long* h) {
 
 void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
                      unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, int kc_max,
-                     int mn_max) {
+                     int mn_max, zc* arena_out) {
+  if (!arena_out) arena_out = arena;
   if (nd == 0) return;
   kmax = std::max(std::max(kmax, 1), RLMAX);
   const int64_t per = std::max<int64_t>((int64_t)kmax * kmax * 5 + 2 * (int64_t)kmax,
@@ -424,7 +425,7 @@ void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int
   CK(cudaFuncSetAttribute(k_truncate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   for (int b0 = 0; b0 < nd; b0 += wave) {
     int nb = std::min(wave, nd - b0);
-    k_truncate<<<nb, LR_NT, smem, s>>>(arena, ranks, d_desc + b0, scratch.p, per, kmax, tol,
+    k_truncate<<<nb, LR_NT, smem, s>>>(arena, arena_out, ranks, d_desc + b0, scratch.p, per, kmax, tol,
                                        overflow, g_trunc_prof);
     CKL();
   }
