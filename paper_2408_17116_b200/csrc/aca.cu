@@ -336,10 +336,18 @@ static void hmatrix_build(cbie_hmat* H, int n_leaf) {
       L.off_d = used;
       used += (int64_t)L.m * L.n;
     }
-  int64_t lr_guess = 0;
+  // low-rank region: the capacity bound sum (m+n) min(budget, 128) when it fits in
+  // half of the free HBM, else half of the free HBM (grown on demand, rarely)
+  int64_t lr_bound = 0;
   for (auto& L : T.leaves)
-    if (L.kind == BLK_LR) lr_guess += (int64_t)(L.m + L.n) * 24;
-  H->arena.alloc(std::max<int64_t>(used + lr_guess, 1));
+    if (L.kind == BLK_LR) lr_bound += (int64_t)(L.m + L.n) * std::min(aca_budget(L.m, L.n), 128);
+  {
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    const int64_t avail = (int64_t)(0.5 * ((double)fr - (double)used * sizeof(zc))) / (int64_t)sizeof(zc);
+    const int64_t lr_alloc = std::max<int64_t>(std::min(lr_bound, avail), 1 << 20);
+    H->arena.alloc(std::max<int64_t>(used + lr_alloc, 1));
+  }
   std::vector<int> aca_leaf;
   for (int li = 0; li < nleaf; ++li)
     if (T.leaves[li].kind == BLK_LR) aca_leaf.push_back(li);
@@ -363,7 +371,7 @@ static void hmatrix_build(cbie_hmat* H, int n_leaf) {
   auto grow = [&](int64_t need) {
     if (need <= (int64_t)H->arena.n) return;
     DBuf<zc> bigger;
-    bigger.alloc(std::max<int64_t>(need, (int64_t)(1.5 * (double)H->arena.n)));
+    bigger.alloc(std::max<int64_t>(need, (int64_t)H->arena.n + ((int64_t)1 << 28)));
     CK(cudaMemcpyAsync(bigger.p, H->arena.p, sizeof(zc) * used, cudaMemcpyDeviceToDevice, s));
     std::swap(bigger.p, H->arena.p);
     std::swap(bigger.n, H->arena.n);
@@ -416,26 +424,31 @@ static void hmatrix_build(cbie_hmat* H, int n_leaf) {
     launch_aca(H, aca, scratch.p, d_status.p);
     std::vector<int> status(aca.size());
     CK(cudaMemcpy(status.data(), d_status.p, sizeof(int) * aca.size(), cudaMemcpyDeviceToHost));
-    // capacity misses: rerun with the full budget in a second scratch region
-    std::vector<AcaDesc> retry;
-    std::vector<int> retry_idx;
+    // capacity misses: rerun with twice the capacity (up to the budget) until every
+    // block converged or overflowed its budget (the reference ACA has no capacity)
     int64_t roff = soff;
-    for (size_t a = 0; a < aca.size(); ++a)
-      if (status[a] == 2) {
-        AcaDesc d = aca[a];
-        d.kmax = d.budget;
-        d.off_u = roff;
-        roff += (int64_t)d.m * (d.kmax + 1);
-        d.off_v = roff;
-        roff += (int64_t)d.n * (d.kmax + 1);
-        aca[a] = d;
-        retry.push_back(d);
-        retry_idx.push_back((int)a);
-      }
-    if (!retry.empty()) {
+    for (int round = 0; round < 16; ++round) {
+      std::vector<AcaDesc> retry;
+      std::vector<int> retry_idx;
+      int64_t base = roff;
+      for (size_t a = 0; a < aca.size(); ++a)
+        if (status[a] == 2) {
+          AcaDesc d = aca[a];
+          d.kmax = std::min(d.budget, 2 * d.kmax);
+          d.off_u = roff;
+          roff += (int64_t)d.m * (d.kmax + 1);
+          d.off_v = roff;
+          roff += (int64_t)d.n * (d.kmax + 1);
+          aca[a] = d;
+          retry.push_back(d);
+          retry_idx.push_back((int)a);
+        }
+      if (retry.empty()) break;
+      (void)base;
       DBuf<zc> bigger;
       bigger.alloc(roff);
-      CK(cudaMemcpyAsync(bigger.p, scratch.p, sizeof(zc) * soff, cudaMemcpyDeviceToDevice, s));
+      CK(cudaMemcpyAsync(bigger.p, scratch.p, sizeof(zc) * std::min<int64_t>(scratch.n, roff),
+                         cudaMemcpyDeviceToDevice, s));
       std::swap(bigger.p, scratch.p);
       std::swap(bigger.n, scratch.n);
       DBuf<int> st2;

@@ -141,7 +141,17 @@ struct DBuf {
     if (count == n && p) return;
     release();
     if (count == 0) return;
-    CK(cudaMalloc(&p, count * sizeof(T)));
+    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    if (e != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      throw cbie_error(e == cudaErrorMemoryAllocation ? CBIE_EOOM : CBIE_ECUDA,
+                       std::string("cudaMalloc of ") + std::to_string(count * sizeof(T) >> 20) +
+                           " MiB failed (" + cudaGetErrorString(e) + "; free " +
+                           std::to_string(fr >> 20) + " MiB)");
+    }
     n = count;
   }
   void upload(const T* h, size_t count, cudaStream_t s) {
