@@ -316,8 +316,11 @@ static void launch_aca(cbie_hmat* H, const std::vector<AcaDesc>& descs, zc* aren
   CK(cudaStreamSynchronize(s));
 }
 
+void hlu_trim_cache(bool force);
+
 static void hmatrix_build(cbie_hmat* H, int n_leaf) {
   cbie_ctx* c = H->ctx;
+  hlu_trim_cache(false);
   cudaStream_t s = c->stream;
   Tree& T = H->tree;
   auto t0 = std::chrono::steady_clock::now();

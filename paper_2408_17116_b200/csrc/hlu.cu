@@ -989,14 +989,15 @@ struct Exec {
   int64_t kind_tasks[OP_NKIND] = {};
 };
 
-Exec execute(Recorder& R, zc* arena, int* ranks, int* piv, double* rcond, int* flag,
-             unsigned long long* ovf, DBuf<zc>& trunc_scratch, double tol, cudaStream_t s) {
-  Exec ex;
-  std::vector<Task> ts = R.tasks;
-  std::stable_sort(ts.begin(), ts.end(), [](const Task& a, const Task& b) {
-    return a.level != b.level ? a.level < b.level : a.kind < b.kind;
-  });
-  // reorder descriptor arrays into launch order and upload once
+struct Grp {
+  int kind, start, count, level, kmax;
+};
+
+// A recorded tape turned into launch groups with device-resident descriptors.
+// Reusable for every factorisation with the same block structure / layout.
+struct Plan {
+  Recorder R;
+  std::vector<Grp> groups;
   std::vector<GemmD> g;
   std::vector<EwD> e;
   std::vector<ConcatD> c;
@@ -1004,10 +1005,31 @@ Exec execute(Recorder& R, zc* arena, int* ranks, int* piv, double* rcond, int* f
   std::vector<GetrfD> f;
   std::vector<TruncDesc> tr;
   std::vector<DenseLRDesc> dl;
-  struct Grp {
-    int kind, start, count, level, kmax;
-  };
-  std::vector<Grp> groups;
+  DBuf<GemmD> dg;
+  DBuf<EwD> de;
+  DBuf<ConcatD> dc;
+  DBuf<TrsmD> dt;
+  DBuf<GetrfD> df;
+  DBuf<TruncDesc> dtr;
+  DBuf<DenseLRDesc> ddl;
+  size_t trsm_smem = 0, getrf_smem = 0;
+};
+
+void make_plan(Plan& P, cudaStream_t s) {
+  Recorder& R = P.R;
+  std::vector<Task> ts = R.tasks;
+  std::stable_sort(ts.begin(), ts.end(), [](const Task& a, const Task& b) {
+    return a.level != b.level ? a.level < b.level : a.kind < b.kind;
+  });
+  // reorder descriptor arrays into launch order and upload once
+  auto& g = P.g;
+  auto& e = P.e;
+  auto& c = P.c;
+  auto& t = P.t;
+  auto& f = P.f;
+  auto& tr = P.tr;
+  auto& dl = P.dl;
+  auto& groups = P.groups;
   for (size_t i = 0; i < ts.size();) {
     size_t j = i;
     const int kind = ts[i].kind, lvl = ts[i].level;
@@ -1040,31 +1062,38 @@ Exec execute(Recorder& R, zc* arena, int* ranks, int* piv, double* rcond, int* f
     groups.push_back(gr);
     i = j;
   }
-  DBuf<GemmD> dg;
-  DBuf<EwD> de;
-  DBuf<ConcatD> dc;
-  DBuf<TrsmD> dt;
-  DBuf<GetrfD> df;
-  DBuf<TruncDesc> dtr;
-  DBuf<DenseLRDesc> ddl;
-  ddl.upload(dl, s);
-  DBuf<zc> dlr_scratch;
-  dg.upload(g, s);
-  de.upload(e, s);
-  dc.upload(c, s);
-  dt.upload(t, s);
-  df.upload(f, s);
-  dtr.upload(tr, s);
-  // launch geometry helpers
-  int gemm_tiles = 1;
-  for (auto& x : g) gemm_tiles = std::max(gemm_tiles, std::max(x.m.v, x.n.v));
+  P.ddl.upload(dl, s);
+  P.dg.upload(g, s);
+  P.de.upload(e, s);
+  P.dc.upload(c, s);
+  P.dt.upload(t, s);
+  P.df.upload(f, s);
+  P.dtr.upload(tr, s);
   int maxn_trsm = 1;
   for (auto& x : t) maxn_trsm = std::max(maxn_trsm, x.n);
   int maxn_getrf = 1;
   for (auto& x : f) maxn_getrf = std::max(maxn_getrf, x.n);
-  const size_t trsm_smem = (size_t)maxn_trsm * TS_COLS * sizeof(zc);
+  P.trsm_smem = (size_t)maxn_trsm * TS_COLS * sizeof(zc);
+  P.getrf_smem = (size_t)maxn_getrf * sizeof(zc);
+}
+
+Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag,
+              unsigned long long* ovf, DBuf<zc>& trunc_scratch, double tol, cudaStream_t s) {
+  Exec ex;
+  const auto& g = P.g;
+  const auto& t = P.t;
+  const auto& tr = P.tr;
+  const auto& dl = P.dl;
+  auto& dg = P.dg;
+  auto& de = P.de;
+  auto& dc = P.dc;
+  auto& dt = P.dt;
+  auto& df = P.df;
+  auto& dtr = P.dtr;
+  auto& ddl = P.ddl;
+  DBuf<zc> dlr_scratch;
+  const size_t trsm_smem = P.trsm_smem, getrf_smem = P.getrf_smem;
   CK(cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem));
-  const size_t getrf_smem = (size_t)maxn_getrf * sizeof(zc);
   int lvl = -1;
   const bool prof = getenv("CBIE_PROFILE") != nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -1073,7 +1102,7 @@ Exec execute(Recorder& R, zc* arena, int* ranks, int* piv, double* rcond, int* f
     cudaEventCreate(&e1);
   }
   std::vector<cudaEvent_t> tev;   // (start, stop) pairs around every truncation launch
-  for (auto& gr : groups) {
+  for (auto& gr : P.groups) {
     if (gr.level != lvl) {
       ++ex.levels;
       lvl = gr.level;
@@ -1163,7 +1192,6 @@ Exec execute(Recorder& R, zc* arena, int* ranks, int* piv, double* rcond, int* f
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   }
-  (void)gemm_tiles;
   CK(cudaStreamSynchronize(s));
   for (size_t i = 0; i + 1 < tev.size(); i += 2) {
     float ms = 0;
@@ -1176,8 +1204,45 @@ Exec execute(Recorder& R, zc* arena, int* ranks, int* piv, double* rcond, int* f
   return ex;
 }
 
+Exec execute(Recorder& R, zc* arena, int* ranks, int* piv, double* rcond, int* flag,
+             unsigned long long* ovf, DBuf<zc>& trunc_scratch, double tol, cudaStream_t s) {
+  Plan P;
+  P.R = std::move(R);
+  make_plan(P, s);
+  Exec ex = run_plan(P, arena, ranks, piv, rcond, flag, ovf, trunc_scratch, tol, s);
+  R = std::move(P.R);
+  return ex;
+}
+
+// one cached plan + workspace per process (bench steps and repeated solves on the
+// same mesh factor the same block structure)
+struct PlanCache {
+  uint64_t key = 0;
+  Plan plan;
+  DBuf<zc> work;
+  int64_t leaf_end = 0;
+};
+std::unique_ptr<PlanCache> g_plan_cache;
+
+uint64_t fnv(uint64_t h, int64_t v) {
+  for (int i = 0; i < 8; ++i) {
+    h ^= (uint64_t)((v >> (8 * i)) & 0xff);
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+
 }  // namespace
 
+
+// drop the cached H-LU workspace when HBM is needed elsewhere
+void hlu_trim_cache(bool force) {
+  if (!g_plan_cache) return;
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  // keep the plan (small); release the workspace only when HBM runs short
+  if (force || (double)fr < 0.25 * (double)tot) g_plan_cache->work.release();
+}
 
 // ---------------------------------------------------------------------------
 // factor / solve drivers
@@ -1221,35 +1286,57 @@ static void hlu_factor_impl(cbie_hlu* F) {
       F->pivoff[li] = npiv;
       npiv += T.leaves[li].m;
     }
+  // structure key: leaf layout + tolerance; a hit skips recording and descriptor upload
+  uint64_t key = 1469598103934665603ull;
+  key = fnv(key, nleaf);
+  for (const auto& L : T.leaves) {
+    key = fnv(key, L.kind * 1000003ll + L.m * 1009ll + L.n);
+    key = fnv(key, L.cap * 7919ll + T.cl[L.r].lo * 31ll + T.cl[L.c].lo);
+  }
+  key = fnv(key, (int64_t)(F->tol * 1e15));
+  const bool use_cache = getenv("CBIE_NO_PLAN_CACHE") == nullptr;
   auto t0 = std::chrono::steady_clock::now();
-  Recorder R;
-  R.tol = F->tol;
-  R.leaf_end = leaf_end;
-  // temporaries before chunk reuse: most of the free HBM after the factor copy (a
-  // reused chunk orders its new owner after every earlier access, which costs
-  // parallelism), CBIE_POOL_GB overrides
-  {
-    size_t fr = 0, tot = 0;
-    cudaMemGetInfo(&fr, &tot);
-    double gb = 0.7 * ((double)fr - (double)leaf_end * sizeof(zc)) / (double)(1ll << 30) - 4.0;
-    gb = std::max(4.0, std::min(gb, 120.0));
-    if (getenv("CBIE_POOL_GB")) gb = atof(getenv("CBIE_POOL_GB"));
-    R.pool_budget = (int64_t)(gb * (double)(1ll << 30)) / (int64_t)sizeof(zc);
-    F->stat["pool_budget_gb"] = gb;
+  if (!(use_cache && g_plan_cache && g_plan_cache->key == key)) {
+    g_plan_cache.reset();   // release the previous plan's workspace first
+    auto pc = std::make_unique<PlanCache>();
+    Recorder& R = pc->plan.R;
+    R.tol = F->tol;
+    R.leaf_end = leaf_end;
+    // temporaries before chunk reuse: most of the free HBM after the factor copy (a
+    // reused chunk orders its new owner after every earlier access, which costs
+    // parallelism), CBIE_POOL_GB overrides
+    {
+      size_t fr = 0, tot = 0;
+      cudaMemGetInfo(&fr, &tot);
+      double gb = 0.7 * ((double)fr - 2.0 * (double)leaf_end * sizeof(zc)) / (double)(1ll << 30) - 4.0;
+      gb = std::max(4.0, std::min(gb, 120.0));
+      if (getenv("CBIE_POOL_GB")) gb = atof(getenv("CBIE_POOL_GB"));
+      R.pool_budget = (int64_t)(gb * (double)(1ll << 30)) / (int64_t)sizeof(zc);
+    }
+    for (int li = 0; li < nleaf; ++li) {
+      R.new_buf();
+      R.new_slot(0, li);
+    }
+    Builder B(R, *F);
+    B.factor(T.root_node);
+    B.flush_all();
+    make_plan(pc->plan, s);
+    pc->key = key;
+    pc->leaf_end = leaf_end;
+    g_plan_cache = std::move(pc);
+    F->stat["plan_cached"] = 0;
+  } else {
+    F->stat["plan_cached"] = 1;
   }
-  for (int li = 0; li < nleaf; ++li) {
-    R.new_buf();
-    R.new_slot(0, li);
-  }
-  Builder B(R, *F);
-  B.factor(T.root_node);
-  B.flush_all();
-  F->stat["lazy_flushes"] = B.flushes;
+  Plan& PL = g_plan_cache->plan;
+  Recorder& R = PL.R;
+  F->stat["pool_budget_gb"] = (double)R.pool_budget * sizeof(zc) / (double)(1ll << 30);
   auto t1 = std::chrono::steady_clock::now();
   F->stat["record_ms"] = std::chrono::duration<double, std::milli>(t1 - t0).count();
-  // device state: arena = copy of the leaf storage + temporaries
-  F->arena.alloc((size_t)(leaf_end + R.pool_top + 1));
-  launch_copy_segments(segs, H->arena.p, F->arena.p, s);
+  // device state: workspace = copy of the leaf storage + temporaries (cached)
+  DBuf<zc>& work = g_plan_cache->work;
+  if ((int64_t)work.n < leaf_end + R.pool_top + 1) work.alloc((size_t)(leaf_end + R.pool_top + 1));
+  launch_copy_segments(segs, H->arena.p, work.p, s);
   std::vector<int> r0 = R.init_ranks;
   for (int li = 0; li < nleaf; ++li) r0[li] = H->h_rank[li];
   F->ranks.upload(r0, s);
@@ -1266,17 +1353,12 @@ static void hlu_factor_impl(cbie_hlu* F) {
   if (getenv("CBIE_PROFILE")) trunc_prof_enable(true, getenv("CBIE_ONESIDED") ? 1 : 0);
   EvTimer tm;
   tm.start(s);
-  Exec ex = execute(R, F->arena.p, F->ranks.p, F->piv.p, F->rcond.p, flag.p, ovf.p, scratch, F->tol, s);
+  Exec ex = run_plan(PL, work.p, F->ranks.p, F->piv.p, F->rcond.p, flag.p, ovf.p, scratch, F->tol, s);
   F->stat["factor_device_ms"] = tm.stop_ms(s);
-  {
-    // keep only the factor storage; the temporary pool is released
-    DBuf<zc> compact;
-    compact.alloc((size_t)leaf_end + 1);
-    CK(cudaMemcpyAsync(compact.p, F->arena.p, sizeof(zc) * leaf_end, cudaMemcpyDeviceToDevice, s));
-    CK(cudaStreamSynchronize(s));
-    std::swap(compact.p, F->arena.p);
-    std::swap(compact.n, F->arena.n);
-  }
+  // the factors keep only their storage; the workspace stays with the plan cache
+  F->arena.alloc((size_t)leaf_end + 1);
+  CK(cudaMemcpyAsync(F->arena.p, work.p, sizeof(zc) * leaf_end, cudaMemcpyDeviceToDevice, s));
+  CK(cudaStreamSynchronize(s));
   int hflag = 0;
   unsigned long long hovf = 0;
   CK(cudaMemcpy(&hflag, flag.p, sizeof(int), cudaMemcpyDeviceToHost));
