@@ -384,7 +384,8 @@ static void hmatrix_build(cbie_hmat* H, int n_leaf) {
   const int64_t wave_elems =
       (int64_t)((getenv("CBIE_ACA_WAVE_GB") ? atof(getenv("CBIE_ACA_WAVE_GB")) : 8.0) *
                 (double)(1ll << 30)) / (int64_t)sizeof(zc);
-  DBuf<zc> scratch, staging, tscratch;
+  DBuf<zc> scratch, staging;
+  TruncWork tscratch;
   DBuf<int> d_status;
   DBuf<unsigned long long> ovf;
   ovf.alloc(1);
@@ -499,7 +500,7 @@ static void hmatrix_build(cbie_hmat* H, int n_leaf) {
     DBuf<TruncDesc> dtd;
     dtd.upload(td, s);
     launch_truncate(scratch.p, H->rank.p, dtd.p, (int)td.size(), kmax_t, H->tol, ovf.p, tscratch, s,
-                    kcm, mnm, staging.p);
+                    kcm, mnm, staging.p, TRUNC_NO_DENSE);
     std::vector<int> rk(nleaf);
     CK(cudaStreamSynchronize(s));   // ranks come from the (non-blocking) library stream
     CK(cudaMemcpy(rk.data(), H->rank.p, sizeof(int) * nleaf, cudaMemcpyDeviceToHost));

@@ -991,6 +991,7 @@ struct Exec {
 
 struct Grp {
   int kind, start, count, level, kmax;
+  int split = 0;   // OP_TRUNC: descriptors [start, start + split) have max(m, n) <= 192
 };
 
 // A recorded tape turned into launch groups with device-resident descriptors.
@@ -1059,6 +1060,11 @@ void make_plan(Plan& P, cudaStream_t s) {
       }
     }
     gr.count = (int)(j - i);
+    if (kind == OP_TRUNC) {   // small blocks first: they and the large ones run on two streams
+      auto small = [](const TruncDesc& d) { return std::max(d.m, d.n) <= 192; };
+      std::stable_partition(tr.begin() + gr.start, tr.end(), small);
+      gr.split = (int)std::count_if(tr.begin() + gr.start, tr.end(), small);
+    }
     groups.push_back(gr);
     i = j;
   }
@@ -1078,8 +1084,14 @@ void make_plan(Plan& P, cudaStream_t s) {
 }
 
 Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag,
-              unsigned long long* ovf, DBuf<zc>& trunc_scratch, double tol, cudaStream_t s) {
+              unsigned long long* ovf, TruncWork* tw, double tol, cudaStream_t s) {
   Exec ex;
+  // second stream for the large-block half of split recompression groups
+  cudaStream_t s2 = nullptr;
+  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
+  CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
+  CK(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
+  CK(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming));
   const auto& g = P.g;
   const auto& t = P.t;
   const auto& tr = P.tr;
@@ -1165,14 +1177,27 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
         cudaEventCreate(&a);
         cudaEventCreate(&b);
         cudaEventRecord(a, s);
-        int kcm = 1, mnm = 1;
-        for (int i = 0; i < gr.count; ++i) {
-          const TruncDesc& td = tr[gr.start + i];
-          kcm = std::max(kcm, td.k);
-          mnm = std::max(mnm, std::max(td.m, td.n));
+        auto part = [&](int b, int e, TruncWork& w, cudaStream_t st) {
+          int kcm = 1, mnm = 1, dense = 0;
+          for (int i = b; i < e; ++i) {
+            const TruncDesc& td = tr[gr.start + i];
+            kcm = std::max(kcm, td.k);
+            mnm = std::max(mnm, std::max(td.m, td.n));
+            dense |= td.in_v < 0;
+          }
+          launch_truncate(arena, ranks, dtr.p + gr.start + b, e - b, gr.kmax, tol, ovf, w, st, kcm, mnm,
+                          nullptr, dense ? 0 : TRUNC_NO_DENSE);
+        };
+        if (gr.split > 0 && gr.split < gr.count) {
+          CK(cudaEventRecord(fork_ev, s));
+          CK(cudaStreamWaitEvent(s2, fork_ev, 0));
+          part(gr.split, gr.count, tw[1], s2);
+          part(0, gr.split, tw[0], s);
+          CK(cudaEventRecord(join_ev, s2));
+          CK(cudaStreamWaitEvent(s, join_ev, 0));
+        } else {
+          part(0, gr.count, tw[0], s);
         }
-        launch_truncate(arena, ranks, dtr.p + gr.start, gr.count, gr.kmax, tol, ovf, trunc_scratch, s,
-                        kcm, mnm);
         cudaEventRecord(b, s);
         tev.push_back(a);
         tev.push_back(b);
@@ -1186,6 +1211,24 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
       float ms = 0;
       cudaEventElapsedTime(&ms, e0, e1);
       ex.kind_ms[gr.kind] += ms;
+      if (gr.kind == OP_TRUNC && getenv("CBIE_TRUNC_DUMP")) {
+        // debug: per-launch size profile (k of every task after its inputs are final)
+        int kmx = 0, n64 = 0, n96 = 0, rmx = 0;
+        for (int i = 0; i < gr.count; ++i) {
+          const TruncDesc& td = tr[gr.start + i];
+          int k = td.k, r = 0;
+          if (td.k_slot >= 0) cudaMemcpy(&k, ranks + td.k_slot, sizeof(int), cudaMemcpyDeviceToHost);
+          cudaMemcpy(&r, ranks + td.out_slot, sizeof(int), cudaMemcpyDeviceToHost);
+          kmx = std::max(kmx, k);
+          rmx = std::max(rmx, r);
+          if (getenv("CBIE_TRUNC_DUMP")[0] == '2')
+            fprintf(stderr, "T %d %d %d %d %d %d\n", gr.level, td.m, td.n, k, r, td.in_v < 0);
+          n64 += k > 64;
+          n96 += k > 96;
+        }
+        fprintf(stderr, "TRUNC level=%d n=%d kmax=%d rmax=%d n_k>64=%d n_k>96=%d ms=%.3f\n", gr.level,
+                gr.count, kmx, rmx, n64, n96, ms);
+      }
     }
   }
   if (prof) {
@@ -1193,6 +1236,9 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
     cudaEventDestroy(e1);
   }
   CK(cudaStreamSynchronize(s));
+  cudaEventDestroy(fork_ev);
+  cudaEventDestroy(join_ev);
+  cudaStreamDestroy(s2);
   for (size_t i = 0; i + 1 < tev.size(); i += 2) {
     float ms = 0;
     cudaEventElapsedTime(&ms, tev[i], tev[i + 1]);
@@ -1205,11 +1251,11 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
 }
 
 Exec execute(Recorder& R, zc* arena, int* ranks, int* piv, double* rcond, int* flag,
-             unsigned long long* ovf, DBuf<zc>& trunc_scratch, double tol, cudaStream_t s) {
+             unsigned long long* ovf, TruncWork* tw, double tol, cudaStream_t s) {
   Plan P;
   P.R = std::move(R);
   make_plan(P, s);
-  Exec ex = run_plan(P, arena, ranks, piv, rcond, flag, ovf, trunc_scratch, tol, s);
+  Exec ex = run_plan(P, arena, ranks, piv, rcond, flag, ovf, tw, tol, s);
   R = std::move(P.R);
   return ex;
 }
@@ -1220,6 +1266,7 @@ struct PlanCache {
   uint64_t key = 0;
   Plan plan;
   DBuf<zc> work;
+  TruncWork tw[2];   // recompression workspaces of the two streams
   int64_t leaf_end = 0;
 };
 std::unique_ptr<PlanCache> g_plan_cache;
@@ -1241,7 +1288,11 @@ void hlu_trim_cache(bool force) {
   size_t fr = 0, tot = 0;
   cudaMemGetInfo(&fr, &tot);
   // keep the plan (small); release the workspace only when HBM runs short
-  if (force || (double)fr < 0.25 * (double)tot) g_plan_cache->work.release();
+  if (force || (double)fr < 0.25 * (double)tot) {
+    g_plan_cache->work.release();
+    g_plan_cache->tw[0].release();
+    g_plan_cache->tw[1].release();
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1349,11 +1400,10 @@ static void hlu_factor_impl(cbie_hlu* F) {
   DBuf<unsigned long long> ovf;
   ovf.alloc(1);
   CK(cudaMemsetAsync(ovf.p, 0, 8, s));
-  DBuf<zc> scratch;
   if (getenv("CBIE_PROFILE")) trunc_prof_enable(true, getenv("CBIE_ONESIDED") ? 1 : 0);
   EvTimer tm;
   tm.start(s);
-  Exec ex = run_plan(PL, work.p, F->ranks.p, F->piv.p, F->rcond.p, flag.p, ovf.p, scratch, F->tol, s);
+  Exec ex = run_plan(PL, work.p, F->ranks.p, F->piv.p, F->rcond.p, flag.p, ovf.p, g_plan_cache->tw, F->tol, s);
   F->stat["factor_device_ms"] = tm.stop_ms(s);
   // the factors keep only their storage; the workspace stays with the plan cache
   F->arena.alloc((size_t)leaf_end + 1);
@@ -1367,13 +1417,13 @@ static void hlu_factor_impl(cbie_hlu* F) {
   F->stat["levels"] = ex.levels;
   F->stat["trunc_kernel_ms"] = ex.trunc_kernel_ms;
   if (getenv("CBIE_PROFILE")) {
-    unsigned long long h[14] = {};
+    unsigned long long h[16] = {};
     trunc_prof_read(h);
     const char* nm[4] = {"qr", "core", "svd", "apply"};
     for (int i = 0; i < 4; ++i) F->stat[std::string("trunc_cyc_") + nm[i]] = h[4] ? (double)h[i] / h[4] : 0;
     F->stat["trunc_mean_sweeps"] = h[4] ? (double)h[5] / h[4] : 0;
-    const char* pn[4] = {"rand_ok", "rand_fail", "exact_smem", "exact_global"};
-    for (int i = 0; i < 4; ++i) {
+    const char* pn[5] = {"rand_ok", "rand_fail", "exact_smem", "exact_global", "blocked"};
+    for (int i = 0; i < 5; ++i) {
       F->stat[std::string("trunc_n_") + pn[i]] = (double)h[6 + 2 * i];
       F->stat[std::string("trunc_cyc_") + pn[i]] = h[6 + 2 * i] ? (double)h[7 + 2 * i] / h[6 + 2 * i] : 0;
     }
@@ -1491,8 +1541,8 @@ static void hlu_solve_impl(cbie_hlu* F, const zc* b, zc* x, int nrhs) {
   rc.alloc(1);
   DBuf<unsigned long long> ovf;
   ovf.alloc(1);
-  DBuf<zc> scratch;
-  execute(R, F->arena.p, ranks.p, F->piv.p, rc.p, flag.p, ovf.p, scratch, F->tol, s);
+  TruncWork tw[2];
+  execute(R, F->arena.p, ranks.p, F->piv.p, rc.p, flag.p, ovf.p, tw, F->tol, s);
   CK(cudaMemcpy(bp.data(), F->arena.p + X.off, sizeof(zc) * bp.size(), cudaMemcpyDeviceToHost));
   for (size_t p = 0; p < T.pperm.size(); ++p)
     for (int c = 0; c < C; ++c) {

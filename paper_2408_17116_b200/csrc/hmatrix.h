@@ -80,9 +80,27 @@ struct TruncDesc {
 // kmax >= every min(m,k), min(n,k) (dense mode: min(m,n) and n) in the batch
 // kc_max / mn_max: largest concatenated capacity and max(m, n) (randomized-path scratch);
 // arena_out (if non-null) receives the outputs (out_u / out_v offsets are relative to it)
+// flags & TRUNC_NO_DENSE: the caller guarantees no dense-mode (in_v < 0) descriptor, so
+// batches with mn_max <= 512 run the blocked kernel (trunc2.cu); problems whose device-side
+// rank exceeds 128 are deferred by it to the unblocked kernel (second launch)
+constexpr int TRUNC_NO_DENSE = 1;
+// per-stream workspace of the recompression launches (kept across calls)
+struct TruncWork {
+  DBuf<zc> scratch;    // per-CTA scratch of the blocked / unblocked kernels
+  DBuf<int> defer;     // problems the blocked kernel hands to the unblocked one
+  DBuf<zc> dscratch;   // scratch of the deferred launch
+  void release() {
+    scratch.release();
+    defer.release();
+    dscratch.release();
+  }
+};
 void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
-                     unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s,
-                     int kc_max = 0, int mn_max = 0, zc* arena_out = nullptr);
+                     unsigned long long* overflow, TruncWork& work, cudaStream_t s,
+                     int kc_max = 0, int mn_max = 0, zc* arena_out = nullptr, int flags = 0);
+bool launch_truncate_blocked(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, double tol,
+                             unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, int kc_max,
+                             int mn_max, zc* arena_out, int* defer);
 
 // contiguous segment copies src[src + i] -> dst[dst + i] (aca.cu)
 struct CopySeg {

@@ -166,16 +166,12 @@ __device__ bool rand_truncate(const TruncDesc& d, zc* arena, zc* aout, int* rank
   }
 }
 
-__global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, zc* aout, int* ranks,
-                                                    const TruncDesc* __restrict__ descs,
-                                                    zc* scratch, int64_t scratch_per, int KS,
-                                                    double tol, unsigned long long* overflow,
-                                                    unsigned long long* prof) {
-  const TruncDesc d = descs[blockIdx.x];
+__device__ void trunc_task(const TruncDesc d, zc* arena, zc* aout, int* ranks, zc* scratch,
+                           int64_t scratch_per, int KS, double tol, unsigned long long* overflow,
+                           unsigned long long* prof, unsigned char* smem_raw) {
   long long tc0 = clock64();
   __shared__ double red[LR_NW];
   __shared__ int flag;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
   // per-CTA vectors (reflector scalars, singular values, order) live at the end of
   // the CTA's global scratch slot so the shared memory stays free for the cores
   zc* rd1 = scratch + (int64_t)blockIdx.x * scratch_per + (scratch_per - 4 * (int64_t)KS);
@@ -388,6 +384,26 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, zc* aout, int* ra
   }
 }
 
+// idx == nullptr: CTA b handles descs[b].  Deferred mode (problems the blocked
+// kernel could not take): idx[0] = count, idx[1 + i] = descriptor index; the
+// CTAs stride over the list.
+__global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, zc* aout, int* ranks,
+                                                    const TruncDesc* __restrict__ descs,
+                                                    zc* scratch, int64_t scratch_per, int KS,
+                                                    double tol, unsigned long long* overflow,
+                                                    unsigned long long* prof, const int* idx) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  if (!idx) {
+    trunc_task(descs[blockIdx.x], arena, aout, ranks, scratch, scratch_per, KS, tol, overflow, prof, smem_raw);
+    return;
+  }
+  const int cnt = idx[0];
+  for (int i = blockIdx.x; i < cnt; i += gridDim.x) {
+    trunc_task(descs[idx[1 + i]], arena, aout, ranks, scratch, scratch_per, KS, tol, overflow, prof, smem_raw);
+    __syncthreads();
+  }
+}
+
 }  // namespace
 
 unsigned long long* g_trunc_prof = nullptr;   // debug cycle counters (CBIE_PROFILE)
@@ -400,20 +416,49 @@ void trunc_prof_enable(bool on, int onesided) {
   cudaMemcpyToSymbol(prof_onesided_flag_dev, &onesided, sizeof(int));
 }
 void trunc_prof_read(unsigned long long* h) {
-  if (g_trunc_prof) cudaMemcpy(h, g_trunc_prof, 14 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  if (g_trunc_prof) cudaMemcpy(h, g_trunc_prof, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
 }
 
 void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
-                     unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, int kc_max,
-                     int mn_max, zc* arena_out) {
+                     unsigned long long* overflow, TruncWork& work, cudaStream_t s, int kc_max,
+                     int mn_max, zc* arena_out, int flags) {
+  DBuf<zc>& scratch = work.scratch;
   if (!arena_out) arena_out = arena;
   if (nd == 0) return;
+  DBuf<int>& defer = work.defer;   // deferred-problem list of the blocked kernel
+  int* dfr = nullptr;
+  if (flags & TRUNC_NO_DENSE) {
+    if (kc_max > 128) {
+      if (defer.n < (size_t)nd + 1) defer.alloc(std::max<size_t>(nd + 1, 4096));
+      CK(cudaMemsetAsync(defer.p, 0, sizeof(int), s));
+      dfr = defer.p;
+    }
+    if (launch_truncate_blocked(arena, ranks, d_desc, nd, tol, overflow, scratch, s, kc_max, mn_max,
+                                arena_out, dfr)) {
+      if (!dfr) return;
+    } else {
+      dfr = nullptr;
+    }
+  }
   kmax = std::max(std::max(kmax, 1), RLMAX);
   const int64_t per = std::max<int64_t>((int64_t)kmax * kmax * 5 + 2 * (int64_t)kmax,
                                         (int64_t)RLMAX * (4 * (int64_t)mn_max + kc_max + 1) +
                                             2 * (int64_t)RLMAX * RLMAX) +
                       4 * (int64_t)kmax;
   // waves keep the Jacobi scratch bounded (<= 1 GiB); the buffer is reused across calls
+  if (dfr) {   // the blocked kernel's leftovers: a strided grid over the deferred list
+    DBuf<zc>& dscratch = work.dscratch;
+    const int grid = std::min(nd, 74);
+    if (dscratch.n < (size_t)grid * per) dscratch.alloc((size_t)grid * per);
+    const size_t smem = std::max((size_t)SMEM_J * SMEM_J * 3 * sizeof(zc) + SMEM_J * (sizeof(zc) + sizeof(double)),
+                                 (size_t)SMEM_J * SMEM_J * 2 * sizeof(zc) +
+                                     (size_t)TG_K * (TG_R + 1 + 65) * sizeof(zc));
+    CK(cudaFuncSetAttribute(k_truncate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_truncate<<<grid, LR_NT, smem, s>>>(arena, arena_out, ranks, d_desc, dscratch.p, per, kmax, tol, overflow,
+                                         g_trunc_prof, dfr);
+    CKL();
+    return;
+  }
   const int wave = (int)std::max<int64_t>(1, ((int64_t)1 << 30) / (per * (int64_t)sizeof(zc)));
   const size_t need = (size_t)std::min(wave, nd) * per;
   if (scratch.n < need) scratch.alloc(need);
@@ -426,7 +471,7 @@ void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int
   for (int b0 = 0; b0 < nd; b0 += wave) {
     int nb = std::min(wave, nd - b0);
     k_truncate<<<nb, LR_NT, smem, s>>>(arena, arena_out, ranks, d_desc + b0, scratch.p, per, kmax, tol,
-                                       overflow, g_trunc_prof);
+                                       overflow, g_trunc_prof, nullptr);
     CKL();
   }
 }
@@ -475,9 +520,10 @@ extern "C" int cbie_lowrank_truncate(cbie_ctx* c, const cbie_c128* U, int m, int
     DBuf<unsigned long long> ovf;
     ovf.alloc(1);
     CK(cudaMemsetAsync(ovf.p, 0, 8, s));
-    DBuf<zc> scratch;
+    TruncWork work;
     const int kmax = dense ? std::max(m, n) : std::min(k, std::max(m, n));
-    launch_truncate(ar.p, ranks.p, dd.p, 1, kmax, tol, ovf.p, scratch, s, k, std::max(m, n));
+    launch_truncate(ar.p, ranks.p, dd.p, 1, kmax, tol, ovf.p, work, s, k, std::max(m, n), nullptr,
+                    dense ? 0 : TRUNC_NO_DENSE);
     int rr = 0;
     CK(cudaMemcpyAsync(&rr, ranks.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     std::vector<zc> out((size_t)(m + n) * cap);

@@ -1,0 +1,601 @@
+// trunc2_impl.cuh — body of the blocked recompression kernel (see trunc2.cu),
+// included once per CTA shape: namespace T2NS, T2_NT threads, T2_ELEMS shared
+// complex elements, T2_MINB resident CTAs per SM.  No include guard on purpose.
+namespace {
+namespace T2NS {
+
+constexpr int NT = T2_NT;
+constexpr int NW = NT / 32;
+constexpr int KMAX = 128;      // largest concatenated rank handled here
+constexpr int MMAX = 384;      // largest block side
+constexpr int PWMAX = 32;      // widest panel
+constexpr int ELEMS = T2_ELEMS;  // dynamic shared region (zc): panels / core / Jacobi block
+constexpr double DELTA = 0.05; // pivoted-QR drop threshold relative to tol * s_0
+constexpr unsigned FULL = 0xffffffffu;
+
+// shared region layout for a QR / Q application on m rows:
+//   [panel: (m|1) x pw][Z chunk: (m|1) x CH][W: pw x CH][split partials: NT]
+__host__ __device__ inline int panel_width(int m) {
+  const int pw = (ELEMS - NT) / (2 * (m | 1));
+  return pw < 2 ? 2 : (pw > PWMAX ? PWMAX : pw);
+}
+__host__ __device__ inline int chunk_cols(int m, int pw) {
+  return (ELEMS - NT - (m | 1) * pw) / ((m | 1) + pw);
+}
+__host__ __device__ inline int64_t scratch_per(int kc) {
+  return 2 * (int64_t)(kc + PWMAX) * PWMAX + 4 * (int64_t)kc * kc + 64;
+}
+
+struct Smem {
+  zc rd1[KMAX], rd2[KMAX], rdM[KMAX];
+  zc u0[PWMAX];
+  double kap1[KMAX], kap2[KMAX];
+  double nrm[2][KMAX], sig[KMAX];   // column norms double-buffered across pivot steps
+  double sk[PWMAX];
+  int perm[KMAX], order[KMAX];
+  double red[NW];
+  int flag;
+};
+
+__device__ __forceinline__ double bsum(double v, double* red) {
+  v = warp_sum(v);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double t = 0.0;
+#pragma unroll
+  for (int i = 0; i < NW; ++i) t += red[i];
+  return t;
+}
+__device__ __forceinline__ double warp_max(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
+  return v;
+}
+
+// Householder QR of the panel P (mp x jn, ld ldp, shared) in place; the
+// reflector of column j is generated redundantly by every warp from column j
+// itself, so a column step needs a single barrier.  Conventions as cta_qr:
+// R strictly above the diagonal, rd[j] = R[j][j], reflector u_j in rows >= j
+// (head u0 on the diagonal), H_j = I - kap[j] u_j u_j^H.
+template <int RPL>
+__device__ void panel_factor(zc* P, int ldp, int mp, int jn, zc* rd, double* kap, Smem& S) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int j = 0; j < jn; ++j) {
+    zc x[RPL];
+    double s = 0.0;
+#pragma unroll
+    for (int t = 0; t < RPL; ++t) {
+      const int i = lane + 32 * t;
+      x[t] = (i >= j && i < mp) ? P[j * ldp + i] : zmk(0.0, 0.0);
+      s += zabs2(x[t]);
+    }
+    s = warp_sum(s);
+    const zc alpha = P[j * ldp + j];
+    const double nx = sqrt(s), aa = sqrt(zabs2(alpha));
+    const zc ph = aa > 0.0 ? zmk(alpha.x / aa, alpha.y / aa) : zmk(1.0, 0.0);
+    const double kp = nx > 0.0 ? 1.0 / (nx * (nx + aa)) : 0.0;
+    const zc u0 = nx > 0.0 ? zscale(ph, aa + nx) : alpha;
+#pragma unroll
+    for (int t = 0; t < RPL; ++t)
+      if (lane + 32 * t == j) x[t] = u0;
+    if (threadIdx.x == 0) {
+      rd[j] = nx > 0.0 ? zscale(ph, -nx) : zmk(0.0, 0.0);
+      kap[j] = kp;
+      S.u0[j] = u0;
+    }
+    if (kp != 0.0) {
+      for (int c = j + 1 + w; c < jn; c += NW) {
+        zc y[RPL];
+        zc d = zmk(0.0, 0.0);
+#pragma unroll
+        for (int t = 0; t < RPL; ++t) {
+          const int i = lane + 32 * t;
+          y[t] = (i >= j && i < mp) ? P[c * ldp + i] : zmk(0.0, 0.0);
+          d = zadd(d, zcmul(x[t], y[t]));
+        }
+        d = zscale(zmk(warp_sum(d.x), warp_sum(d.y)), kp);
+#pragma unroll
+        for (int t = 0; t < RPL; ++t) {
+          const int i = lane + 32 * t;
+          if (i >= j && i < mp) P[c * ldp + i] = zsub(y[t], zmul(d, x[t]));
+        }
+      }
+    }
+    __syncthreads();
+  }
+  for (int j = threadIdx.x; j < jn; j += NT) P[j * ldp + j] = S.u0[j];
+  __syncthreads();
+}
+
+// S (jn x jn, col-major ld lds, global) = unit-diagonal strict upper triangle of
+// Y^H Y, Y = [u_0 .. u_{jn-1}] diag(sqrt kap): Q_p = H_0 .. H_{jn-1} = I - Y S^{-1} Y^H.
+__device__ void build_S(const zc* P, int ldp, int mp, int jn, const double* kap, zc* Sg, int lds) {
+  for (int e = threadIdx.x; e < jn * jn; e += NT) {
+    const int a = e % jn, b = e / jn;
+    zc s = zmk(a == b ? 1.0 : 0.0, 0.0);
+    if (a < b && kap[a] != 0.0 && kap[b] != 0.0) {
+      zc acc = zmk(0.0, 0.0);
+      for (int i = b; i < mp; ++i) acc = zadd(acc, zcmul(P[a * ldp + i], P[b * ldp + i]));
+      s = zscale(acc, sqrt(kap[a] * kap[b]));
+    }
+    Sg[b * lds + a] = s;
+  }
+}
+
+// Z (mp x nz, ldz) <- (I - Y S^{-op} Y^H) Z, Y = P diag(sk) (column a of P holds
+// u_a in rows >= a).  adj: S^{-H} (Q_p^H, trailing update); else S^{-1} (Q_p).
+// Z is processed in chunks of CH columns staged in shared memory (Zs, ld
+// mp|1); W = Y^H Zs is computed one output per thread, with the row range
+// split over up to 8 threads (partials in Red) when the chunk has few outputs.
+__device__ void block_reflect(const zc* P, int ldp, int mp, int jn, const double* sk, const zc* Sg,
+                              int lds, zc* Z, int ldz, int nz, bool adj, zc* Zs, zc* Wsm, zc* Red,
+                              int CH) {
+  const int ldzs = mp | 1;
+  for (int c0 = 0; c0 < nz; c0 += CH) {
+    const int nc = min(CH, nz - c0);
+    for (int e = threadIdx.x; e < mp * nc; e += NT) {
+      const int c = e / mp, i = e - c * mp;
+      Zs[c * ldzs + i] = Z[(int64_t)(c0 + c) * ldz + i];
+    }
+    __syncthreads();
+    const int no = jn * nc;
+    const int ns = no >= NT ? 1 : min(8, NT / no);
+    for (int t = threadIdx.x; t < no * ns; t += NT) {
+      const int o = t % no, sp = t / no;
+      const int a = o % jn, c = o / jn;
+      const int i0 = (mp * sp) / ns, i1 = (mp * (sp + 1)) / ns;
+      const zc* pa = P + a * ldp;
+      const zc* zz = Zs + c * ldzs;
+      zc a0 = zmk(0.0, 0.0), a1 = zmk(0.0, 0.0);
+      int i = i0;
+      for (; i + 1 < i1; i += 2) {
+        const zc u0 = i >= a ? pa[i] : zmk(0.0, 0.0);
+        const zc u1 = i + 1 >= a ? pa[i + 1] : zmk(0.0, 0.0);
+        a0 = zadd(a0, zcmul(u0, zz[i]));
+        a1 = zadd(a1, zcmul(u1, zz[i + 1]));
+      }
+      if (i < i1 && i >= a) a0 = zadd(a0, zcmul(pa[i], zz[i]));
+      if (ns == 1) Wsm[o] = zadd(a0, a1);
+      else Red[sp * no + o] = zadd(a0, a1);
+    }
+    __syncthreads();
+    if (ns > 1) {
+      for (int o = threadIdx.x; o < no; o += NT) {
+        zc v = Red[o];
+        for (int sp = 1; sp < ns; ++sp) v = zadd(v, Red[sp * no + o]);
+        Wsm[o] = v;
+      }
+      __syncthreads();
+    }
+    for (int c = threadIdx.x; c < nc; c += NT) {
+      zc* wc = Wsm + c * jn;
+      for (int a = 0; a < jn; ++a) wc[a] = zscale(wc[a], sk[a]);
+      if (adj) {   // S^H is unit lower triangular: forward substitution
+        for (int a = 1; a < jn; ++a) {
+          zc v = wc[a];
+          for (int l = 0; l < a; ++l) v = zsub(v, zcmul(Sg[a * lds + l], wc[l]));
+          wc[a] = v;
+        }
+      } else {     // S is unit upper triangular: back substitution
+        for (int a = jn - 2; a >= 0; --a) {
+          zc v = wc[a];
+          for (int l = a + 1; l < jn; ++l) v = zsub(v, zmul(Sg[l * lds + a], wc[l]));
+          wc[a] = v;
+        }
+      }
+      for (int a = 0; a < jn; ++a) wc[a] = zscale(wc[a], sk[a]);
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < mp * nc; e += NT) {
+      const int c = e / mp, i = e - c * mp;
+      const int am = min(jn, i + 1);
+      const zc* wc = Wsm + c * jn;
+      zc s = zmk(0.0, 0.0);
+      for (int a = 0; a < am; ++a) zfma(s, P[a * ldp + i], wc[a]);
+      Z[(int64_t)(c0 + c) * ldz + i] = zsub(Zs[c * ldzs + i], s);
+    }
+    __syncthreads();
+  }
+}
+
+// Blocked Householder QR of A (m x k, ld, global) in place; S factors of the
+// panels into Sg (the panel starting at column p0 at Sg + p0 * pw, ld pw).
+template <int RPL>
+__device__ void blk_qr(zc* A, int m, int k, int ld, zc* rd, double* kap, zc* Sg, zc* sm, Smem& S) {
+  const int kk = min(m, k);
+  const int ldp = m | 1, pw = panel_width(m);
+  const int CH = chunk_cols(m, pw);
+  zc* P = sm;
+  zc* Zs = sm + ldp * pw;
+  zc* Wsm = Zs + ldp * CH;
+  zc* Red = Wsm + pw * CH;
+  for (int p0 = 0; p0 < kk; p0 += pw) {
+    const int mp = m - p0, jn = min(pw, kk - p0);
+    for (int e = threadIdx.x; e < jn * mp; e += NT) {
+      const int c = e / mp, i = e - c * mp;
+      P[c * ldp + i] = A[(int64_t)(p0 + c) * ld + p0 + i];
+    }
+    __syncthreads();
+    panel_factor<RPL>(P, ldp, mp, jn, rd + p0, kap + p0, S);
+    zc* Sp = Sg + (int64_t)p0 * pw;   // panel S factors: pw x pw, ld pw
+    build_S(P, ldp, mp, jn, kap + p0, Sp, pw);
+    for (int j = threadIdx.x; j < jn; j += NT) S.sk[j] = sqrt(kap[p0 + j]);
+    for (int e = threadIdx.x; e < jn * mp; e += NT) {
+      const int c = e / mp, i = e - c * mp;
+      A[(int64_t)(p0 + c) * ld + p0 + i] = P[c * ldp + i];
+    }
+    __syncthreads();
+    const int nt = k - p0 - jn;
+    if (nt > 0)
+      block_reflect(P, ldp, mp, jn, S.sk, Sp, pw, A + (int64_t)(p0 + jn) * ld + p0, ld, nt, true, Zs, Wsm,
+                    Red, CH);
+  }
+}
+
+// Z (m x nz, ldz) := Q Z, Q = H_0 .. H_{kk-1} from blk_qr (reflectors in A).
+__device__ void blk_apply_q(const zc* A, int m, int kk, int ld, const double* kap, const zc* Sg, zc* Z,
+                            int ldz, int nz, zc* sm, Smem& S) {
+  const int ldp = m | 1, pw = panel_width(m);
+  const int CH = chunk_cols(m, pw);
+  zc* P = sm;
+  zc* Zs = sm + ldp * pw;
+  zc* Wsm = Zs + ldp * CH;
+  zc* Red = Wsm + pw * CH;
+  const int np = (kk + pw - 1) / pw;
+  for (int pi = np - 1; pi >= 0; --pi) {
+    const int p0 = pi * pw, mp = m - p0, jn = min(pw, kk - p0);
+    for (int e = threadIdx.x; e < jn * mp; e += NT) {
+      const int c = e / mp, i = e - c * mp;
+      P[c * ldp + i] = A[(int64_t)(p0 + c) * ld + p0 + i];
+    }
+    for (int j = threadIdx.x; j < jn; j += NT) S.sk[j] = sqrt(kap[p0 + j]);
+    __syncthreads();
+    block_reflect(P, ldp, mp, jn, S.sk, Sg + (int64_t)p0 * pw, pw, Z + p0, ldz, nz, false, Zs, Wsm, Red,
+                  CH);
+  }
+}
+
+// Column-pivoted QR of M (p x q, ld; p <= KMAX) in place, stopped when the
+// trailing Frobenius^2 <= thr_rel2 * (largest column norm)^2.  On exit, for
+// a < kp: R[a][a] = S.rdM[a], R[a][b] = M[b * ld + a] (b > a); storage column
+// b holds original column S.perm[b].  Returns kp.
+__device__ int qrcp(zc* M, int p, int q, int ld, double thr_rel2, Smem& S) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = w; c < q; c += NW) {
+    double s = 0.0;
+    for (int i = lane; i < p; i += 32) s += zabs2(M[(int64_t)c * ld + i]);
+    s = warp_sum(s);
+    if (lane == 0) {
+      S.nrm[0][c] = s;
+      S.perm[c] = c;
+    }
+  }
+  __syncthreads();
+  double nmax = 0.0;
+  for (int c = lane; c < q; c += 32) nmax = fmax(nmax, S.nrm[0][c]);
+  nmax = warp_max(nmax);
+  const double thr2 = thr_rel2 * nmax;
+  const int kmax = min(p, q);
+  int j = 0;
+  for (; j < kmax; ++j) {
+    // every warp computes the same pivot and trailing norm (identical code and data)
+    // norms of step j live in buffer j & 1; the updates below write buffer
+    // (j + 1) & 1, so no warp can overwrite a norm another warp is still reading
+    const double* nr = S.nrm[j & 1];
+    double best = -1.0, tsum = 0.0;
+    int bi = q;
+    for (int c = j + lane; c < q; c += 32) {
+      const double v = nr[c];
+      tsum += v;
+      if (v > best) {
+        best = v;
+        bi = c;
+      }
+    }
+    tsum = warp_sum(tsum);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double ob = __shfl_xor_sync(FULL, best, o);
+      const int oi = __shfl_xor_sync(FULL, bi, o);
+      if (ob > best || (ob == best && oi < bi)) {
+        best = ob;
+        bi = oi;
+      }
+    }
+    if (!(tsum > thr2)) break;
+    if (bi != j) {
+      for (int i = threadIdx.x; i < p; i += NT) {
+        const zc t = M[(int64_t)j * ld + i];
+        M[(int64_t)j * ld + i] = M[(int64_t)bi * ld + i];
+        M[(int64_t)bi * ld + i] = t;
+      }
+      if (threadIdx.x == 0) {
+        const int t = S.perm[j];
+        S.perm[j] = S.perm[bi];
+        S.perm[bi] = t;
+      }
+      __syncthreads();
+    }
+    zc x[KMAX / 32];
+    double s = 0.0;
+#pragma unroll
+    for (int t = 0; t < KMAX / 32; ++t) {
+      const int i = lane + 32 * t;
+      x[t] = (i >= j && i < p) ? M[(int64_t)j * ld + i] : zmk(0.0, 0.0);
+      s += zabs2(x[t]);
+    }
+    s = warp_sum(s);
+    const zc alpha = M[(int64_t)j * ld + j];
+    const double nx = sqrt(s), aa = sqrt(zabs2(alpha));
+    const zc ph = aa > 0.0 ? zmk(alpha.x / aa, alpha.y / aa) : zmk(1.0, 0.0);
+    const double kp = nx > 0.0 ? 1.0 / (nx * (nx + aa)) : 0.0;
+    const zc u0 = nx > 0.0 ? zscale(ph, aa + nx) : alpha;
+#pragma unroll
+    for (int t = 0; t < KMAX / 32; ++t)
+      if (lane + 32 * t == j) x[t] = u0;
+    if (threadIdx.x == 0) S.rdM[j] = nx > 0.0 ? zscale(ph, -nx) : zmk(0.0, 0.0);
+    for (int c = j + 1 + w; c < q; c += NW) {
+      zc y[KMAX / 32];
+      zc d = zmk(0.0, 0.0);
+#pragma unroll
+      for (int t = 0; t < KMAX / 32; ++t) {
+        const int i = lane + 32 * t;
+        y[t] = (i >= j && i < p) ? M[(int64_t)c * ld + i] : zmk(0.0, 0.0);
+        d = zadd(d, zcmul(x[t], y[t]));
+      }
+      d = zscale(zmk(warp_sum(d.x), warp_sum(d.y)), kp);
+      double ns = 0.0;
+#pragma unroll
+      for (int t = 0; t < KMAX / 32; ++t) {
+        const int i = lane + 32 * t;
+        if (i >= j && i < p) {
+          const zc v = zsub(y[t], zmul(d, x[t]));
+          M[(int64_t)c * ld + i] = v;
+          if (i > j) ns += zabs2(v);
+        }
+      }
+      ns = warp_sum(ns);
+      if (lane == 0) S.nrm[(j + 1) & 1][c] = ns;
+    }
+    __syncthreads();
+  }
+  return j;
+}
+
+// One-sided Jacobi on the columns of A (p x q, ld), half-warp per pair, no
+// accumulated rotations.  Rotation and skip rules as cta_jacobi_hw.
+__device__ int jacobi_nw(zc* A, int p, int q, int ld, Smem& S) {
+  const int hw = threadIdx.x >> 4, hl = threadIdx.x & 15;
+  constexpr int NHW = NT / 16;
+  double f2 = 0.0;
+  for (int e = threadIdx.x; e < p * q; e += NT) f2 += zabs2(A[(int64_t)(e / p) * ld + e % p]);
+  f2 = bsum(f2, S.red);
+  const double floor2 = 1e-24 * f2;
+  if (q < 2) return 0;
+  const int qe = q + (q & 1);
+  int sweep = 0;
+  for (; sweep < 40; ++sweep) {
+    if (threadIdx.x == 0) S.flag = 0;
+    __syncthreads();
+    for (int r = 0; r < qe - 1; ++r) {
+      for (int base = 0; base < qe / 2; base += NHW) {
+        const int pi = base + hw;
+        const int pa = pi, pb = qe - 1 - pi;
+        const int a = pa == 0 ? 0 : ((pa - 1 + r) % (qe - 1)) + 1;
+        const int b = pb == 0 ? 0 : ((pb - 1 + r) % (qe - 1)) + 1;
+        const bool valid = pi < qe / 2 && a < q && b < q;
+        zc* x = A + (int64_t)(valid ? a : 0) * ld;
+        zc* y = A + (int64_t)(valid ? b : 0) * ld;
+        double al = 0.0, be = 0.0, gr = 0.0, gi = 0.0;
+        if (valid)
+          for (int i = hl; i < p; i += 16) {
+            const zc xi = x[i], yi = y[i];
+            al += zabs2(xi);
+            be += zabs2(yi);
+            gr += xi.x * yi.x + xi.y * yi.y;
+            gi += xi.x * yi.y - xi.y * yi.x;
+          }
+        al = hw_sum(al);
+        be = hw_sum(be);
+        gr = hw_sum(gr);
+        gi = hw_sum(gi);
+        if (!valid) continue;
+        const double g = sqrt(gr * gr + gi * gi);
+        if (!(g > 1e-14 * sqrt(al * be)) || g == 0.0 || fmin(al, be) < floor2) continue;
+        const double zeta = (be - al) / (2.0 * g);
+        const double t = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+        const double cs = 1.0 / sqrt(1.0 + t * t), sn = cs * t;
+        const double ig = 1.0 / g;
+        const zc se = zmk(gr * ig * sn, gi * ig * sn), sec = zmk(gr * ig * sn, -gi * ig * sn);
+        for (int i = hl; i < p; i += 16) {
+          const zc xi = x[i], yi = y[i];
+          x[i] = zsub(zscale(xi, cs), zmul(sec, yi));
+          y[i] = zadd(zmul(se, xi), zscale(yi, cs));
+        }
+        if (hl == 0) S.flag = 1;
+      }
+      __syncthreads();
+    }
+    if (S.flag == 0) break;
+    __syncthreads();
+  }
+  return sweep;
+}
+
+template <int RPL>
+__global__ void __launch_bounds__(NT, T2_MINB)
+    k_trunc2(zc* arena, zc* aout, int* ranks, const TruncDesc* __restrict__ descs, zc* scratch,
+             int64_t per, int kc, double tol, unsigned long long* overflow, unsigned long long* prof,
+             int* defer, int base) {
+  __shared__ Smem S;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  zc* sm = reinterpret_cast<zc*>(smraw);
+  const TruncDesc d = descs[blockIdx.x];
+  const long long tc0 = clock64();
+  if (d.skip_slot >= 0 && ranks[d.skip_slot] == 0) return;
+  const int k = d.k_slot >= 0 ? ranks[d.k_slot] : d.k;
+  const int m = d.m, n = d.n;
+  if (k <= 0 || m == 0 || n == 0) {
+    if (threadIdx.x == 0) ranks[d.out_slot] = 0;
+    return;
+  }
+  if (k > kc) {   // larger than this kernel's layout: handed to the unblocked kernel
+    if (threadIdx.x == 0) defer[1 + atomicAdd(defer, 1)] = base + blockIdx.x;
+    return;
+  }
+  zc* U = arena + d.in_u;
+  zc* Vt = arena + d.in_v;
+  const int kk1 = min(m, k), kk2 = min(n, k);
+  zc* sc = scratch + (int64_t)blockIdx.x * per;
+  zc* SgU = sc;
+  zc* SgV = SgU + (int64_t)(kc + PWMAX) * PWMAX;
+  zc* Mg = SgV + (int64_t)(kc + PWMAX) * PWMAX;   // kk1 x kk2 (kept for U' = M Vhat)
+  zc* M2 = Mg + (int64_t)kc * kc;                 // pivoted-QR workspace when M exceeds smem
+  zc* G = M2 + (int64_t)kc * kc;                  // R1^H staging / global Jacobi block
+  zc* Vh = G + (int64_t)kc * kc;                  // kk2 x r right singular vectors
+
+  blk_qr<RPL>(U, m, k, d.ldu, S.rd1, S.kap1, SgU, sm, S);
+  blk_qr<RPL>(Vt, n, k, d.ldv, S.rd2, S.kap2, SgV, sm, S);
+  const long long tc1 = clock64();
+  // M = R1 R2^T (R factors staged in shared memory when they fit)
+  if ((kk1 + kk2) * k <= ELEMS) {
+    zc* R1 = sm;                       // kk1 x k, ld kk1
+    zc* R2 = sm + kk1 * k;             // kk2 x k, ld kk2
+    for (int e = threadIdx.x; e < kk1 * k; e += NT) {
+      const int c = e / kk1, a = e - c * kk1;
+      R1[e] = c == a ? S.rd1[a] : (c > a ? U[(int64_t)c * d.ldu + a] : zmk(0.0, 0.0));
+    }
+    for (int e = threadIdx.x; e < kk2 * k; e += NT) {
+      const int c = e / kk2, b = e - c * kk2;
+      R2[e] = c == b ? S.rd2[b] : (c > b ? Vt[(int64_t)c * d.ldv + b] : zmk(0.0, 0.0));
+    }
+    __syncthreads();
+    for (int e = threadIdx.x; e < kk1 * kk2; e += NT) {
+      const int a = e % kk1, b = e / kk1;
+      zc s = zmk(0.0, 0.0);
+      for (int c = max(a, b); c < k; ++c) zfma(s, R1[c * kk1 + a], R2[c * kk2 + b]);
+      Mg[e] = s;
+    }
+  } else {
+    for (int e = threadIdx.x; e < kk1 * kk2; e += NT) {
+      const int a = e % kk1, b = e / kk1;
+      zc s = zmk(0.0, 0.0);
+      for (int c = max(a, b); c < k; ++c) {
+        const zc r1 = c == a ? S.rd1[a] : U[(int64_t)c * d.ldu + a];
+        const zc r2 = c == b ? S.rd2[b] : Vt[(int64_t)c * d.ldv + b];
+        zfma(s, r1, r2);
+      }
+      Mg[e] = s;
+    }
+  }
+  __syncthreads();
+  const bool m_sm = kk1 * kk2 <= ELEMS;
+  zc* Mq = m_sm ? sm : M2;
+  for (int e = threadIdx.x; e < kk1 * kk2; e += NT) Mq[e] = Mg[e];
+  __syncthreads();
+  const int kp = qrcp(Mq, kk1, kk2, kk1, (DELTA * tol) * (DELTA * tol), S);
+  // A = R1^H (kk2 x kp)
+  for (int e = threadIdx.x; e < kk2 * kp; e += NT) {
+    const int b = e % kk2, a = e / kk2;
+    G[e] = b > a ? zconj(Mq[(int64_t)b * kk1 + a]) : (b == a ? zconj(S.rdM[a]) : zmk(0.0, 0.0));
+  }
+  __syncthreads();
+  const bool a_sm = kk2 * kp <= ELEMS;
+  zc* Aj = a_sm ? sm : G;
+  if (a_sm) {
+    for (int e = threadIdx.x; e < kk2 * kp; e += NT) sm[e] = G[e];
+    __syncthreads();
+  }
+  const long long tc2 = clock64();
+  const int sweeps = jacobi_nw(Aj, kk2, kp, kk2, S);
+  for (int c = threadIdx.x; c < kp; c += NT) {
+    double sq = 0.0;
+    for (int i = 0; i < kk2; ++i) sq += zabs2(Aj[(int64_t)c * kk2 + i]);
+    S.sig[c] = sqrt(sq);
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < kp; c += NT) {
+    int pos = 0;
+    for (int o = 0; o < kp; ++o)
+      if (S.sig[o] > S.sig[c] || (S.sig[o] == S.sig[c] && o < c)) ++pos;
+    S.order[pos] = c;
+  }
+  __syncthreads();
+  const long long tc3 = clock64();
+  const double s0 = kp > 0 ? S.sig[S.order[0]] : 0.0;
+  int r = 0;
+  if (s0 > 0.0) {
+    for (int c = 0; c < kp; ++c)
+      if (S.sig[c] > tol * s0) ++r;
+    r = max(r, 1);
+  }
+  if (r > d.cap) {
+    if (threadIdx.x == 0) atomicAdd(overflow, 1ull);
+    r = d.cap;
+  }
+  // Vhat = P B_r / sigma_r  (kk2 x r)
+  for (int e = threadIdx.x; e < kk2 * r; e += NT) {
+    const int b = e % kk2, l = e / kk2;
+    const int c = S.order[l];
+    Vh[(int64_t)l * kk2 + S.perm[b]] = zscale(Aj[(int64_t)c * kk2 + b], 1.0 / S.sig[c]);
+  }
+  __syncthreads();
+  zc* Uo = aout + d.out_u;
+  zc* Vo = aout + d.out_v;
+  for (int e = threadIdx.x; e < n * r; e += NT) {
+    const int l = e / n, j = e - l * n;
+    Vo[(int64_t)l * n + j] = j < kk2 ? zconj(Vh[(int64_t)l * kk2 + j]) : zmk(0.0, 0.0);
+  }
+  for (int e = threadIdx.x; e < m * r; e += NT) {
+    const int l = e / m, i = e - l * m;
+    zc s = zmk(0.0, 0.0);
+    if (i < kk1) {
+      const zc* vh = Vh + (int64_t)l * kk2;
+      for (int b = 0; b < kk2; ++b) zfma(s, Mg[(int64_t)b * kk1 + i], vh[b]);
+    }
+    Uo[(int64_t)l * m + i] = s;
+  }
+  __syncthreads();
+  if (r > 0) {
+    blk_apply_q(U, m, kk1, d.ldu, S.kap1, SgU, Uo, m, r, sm, S);
+    blk_apply_q(Vt, n, kk2, d.ldv, S.kap2, SgV, Vo, n, r, sm, S);
+  }
+  if (threadIdx.x == 0) {
+    ranks[d.out_slot] = r;
+    if (prof) {
+      const long long tc4 = clock64();
+      atomicAdd(prof + 0, (unsigned long long)(tc1 - tc0));
+      atomicAdd(prof + 1, (unsigned long long)(tc2 - tc1));
+      atomicAdd(prof + 2, (unsigned long long)(tc3 - tc2));
+      atomicAdd(prof + 3, (unsigned long long)(tc4 - tc3));
+      atomicAdd(prof + 4, 1ull);
+      atomicAdd(prof + 5, (unsigned long long)sweeps);
+      atomicAdd(prof + 14, 1ull);
+      atomicAdd(prof + 15, (unsigned long long)(tc4 - tc0));
+    }
+  }
+}
+
+template <int RPL>
+void launch_rpl(zc* arena, zc* aout, int* ranks, const TruncDesc* d_desc, int nd, int kc, double tol,
+                unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, unsigned long long* prof,
+                int* defer) {
+  const int64_t per = scratch_per(kc);
+  const int wave = (int)std::max<int64_t>(1, ((int64_t)2 << 30) / (per * (int64_t)sizeof(zc)));
+  const size_t need = (size_t)std::min(wave, nd) * per;
+  if (scratch.n < need) scratch.alloc(need);
+  const int smem = ELEMS * (int)sizeof(zc);
+  CK(cudaFuncSetAttribute(k_trunc2<RPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  for (int b0 = 0; b0 < nd; b0 += wave) {
+    const int nb = std::min(wave, nd - b0);
+    k_trunc2<RPL><<<nb, NT, smem, s>>>(arena, aout, ranks, d_desc + b0, scratch.p, per, kc, tol, overflow,
+                                       prof, defer, b0);
+    CKL();
+  }
+}
+
+}  // namespace T2NS
+}  // namespace
+
