@@ -43,6 +43,32 @@ __host__ __device__ __forceinline__ void zfma(zc& acc, zc a, zc b) {
   acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
   acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
 }
+// Executed FP64 work of the H-LU kernels (SURVEY 8(d) flop convention): every task
+// adds its own algorithmic count once, with the ranks it actually saw on the device.
+// One counter per translation unit (static), read / reset by CBIE_FLOP_API below.
+static __device__ double g_tu_flops;
+__device__ __forceinline__ void flop_add(double f) { atomicAdd(&g_tu_flops, f); }
+__host__ __device__ inline double flops_qr(double m, double k) {   // thin QR incl. Q formation
+  return 16.0 * m * k * k - 16.0 * k * k * k / 3.0;
+}
+__host__ __device__ inline double flops_trunc(int m, int n, int k, bool dense) {
+  if (dense) {   // SVD with vectors of a dense m x n block (R-SVD x 4 for complex)
+    const double a = m > n ? m : n, b = m > n ? n : m;
+    return 4.0 * (4.0 * a * b * b + 22.0 * b * b * b);
+  }
+  const double kk = (double)min(min(m, n), k);
+  return flops_qr(m, min(m, k)) + flops_qr(n, min(n, k)) + 112.0 * kk * kk * kk;
+}
+#define CBIE_FLOP_API(name)                                                         \
+  double name##_flops_read() {                                                      \
+    double v = 0.0;                                                                 \
+    cudaMemcpyFromSymbol(&v, g_tu_flops, sizeof(double));                           \
+    return v;                                                                       \
+  }                                                                                 \
+  void name##_flops_reset() {                                                       \
+    const double z = 0.0;                                                           \
+    cudaMemcpyToSymbol(g_tu_flops, &z, sizeof(double));                             \
+  }
 // e^{-j k R} for complex k (Im k <= 0 for physical media)
 __device__ __forceinline__ zc zexp_mjkR(zc k, double R) {
   double s, c;

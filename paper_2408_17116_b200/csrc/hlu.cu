@@ -19,9 +19,15 @@
 #include "hmatrix.h"
 
 std::string stats_to_json(const std::map<std::string, double>& m);
+double trunc2_flops_read();
+void trunc2_flops_reset();
+double lowrank_flops_read();
+void lowrank_flops_reset();
 void trunc_prof_enable(bool on, int onesided);
 void trunc_prof_read(unsigned long long* h);
 void hmat_apply(cbie_hmat* H, const zc* d_xp, zc* d_yp, int nrhs, cudaStream_t s);
+
+CBIE_FLOP_API(hlu)
 
 namespace {
 
@@ -1014,6 +1020,7 @@ struct Plan {
   DBuf<TruncDesc> dtr;
   DBuf<DenseLRDesc> ddl;
   size_t trsm_smem = 0, getrf_smem = 0;
+  int maxn_lu = 0;   // largest diagonal leaf (getrf / trsm)
 };
 
 void make_plan(Plan& P, cudaStream_t s) {
@@ -1081,6 +1088,7 @@ void make_plan(Plan& P, cudaStream_t s) {
   for (auto& x : f) maxn_getrf = std::max(maxn_getrf, x.n);
   P.trsm_smem = (size_t)maxn_trsm * TS_COLS * sizeof(zc);
   P.getrf_smem = (size_t)maxn_getrf * sizeof(zc);
+  P.maxn_lu = std::max(maxn_trsm, maxn_getrf);
 }
 
 Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag,
@@ -1106,6 +1114,23 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
   DBuf<zc> dlr_scratch;
   const size_t trsm_smem = P.trsm_smem, getrf_smem = P.getrf_smem;
   CK(cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem));
+  // blocked diagonal-leaf kernels (dense_lu.cuh) unless a leaf exceeds LU_NMAX
+  const bool blk_lu = getenv("CBIE_LU_UNBLOCKED") == nullptr && P.maxn_lu <= LU_NMAX;
+  const size_t blk_smem = ((size_t)std::max(P.maxn_lu, 1) + LU_QC) * LU_NB * sizeof(zc);
+  const size_t trsm_blk_smem = (size_t)std::max(P.maxn_lu, 1) * LU_NB * sizeof(zc);
+  // rcond estimates run on a side stream (nothing downstream consumes them)
+  cudaStream_t s3 = nullptr;
+  cudaEvent_t rc_ev = nullptr;
+  DBuf<double> anorm;
+  if (blk_lu) {
+    CK(cudaFuncSetAttribute(k_trsm_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_blk_smem));
+    CK(cudaFuncSetAttribute(k_getrf_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)blk_smem));
+    CK(cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&rc_ev, cudaEventDisableTiming));
+    int nl = 1;
+    for (auto& x : P.f) nl = std::max(nl, x.leaf + 1);
+    anorm.alloc(nl);
+  }
   int lvl = -1;
   const bool prof = getenv("CBIE_PROFILE") != nullptr;
   cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -1155,12 +1180,23 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
         for (int i = 0; i < gr.count; ++i) cmax = std::max(cmax, ceil_div(t[gr.start + i].p.v, TS_COLS));
         for (int b0 = 0; b0 < gr.count; b0 += 65535) {
           int nb = std::min(65535, gr.count - b0);
-          k_trsm<<<dim3(cmax, nb), 256, trsm_smem, s>>>(arena, ranks, piv, dt.p + gr.start + b0);
+          if (blk_lu)
+            k_trsm_blk<<<dim3(ceil_div((int64_t)cmax * TS_COLS, LU_NB), nb), LU_NT, trsm_blk_smem, s>>>(
+                arena, ranks, piv, dt.p + gr.start + b0);
+          else
+            k_trsm<<<dim3(cmax, nb), 256, trsm_smem, s>>>(arena, ranks, piv, dt.p + gr.start + b0);
         }
         break;
       }
       case OP_GETRF:
-        k_getrf<<<gr.count, 256, getrf_smem, s>>>(arena, piv, df.p + gr.start, rcond, flag);
+        if (blk_lu) {
+          k_getrf_blk<<<gr.count, LU_NT, blk_smem, s>>>(arena, piv, df.p + gr.start, anorm.p);
+          CK(cudaEventRecord(rc_ev, s));
+          CK(cudaStreamWaitEvent(s3, rc_ev, 0));
+          k_rcond_blk<<<gr.count, LU_NT, (size_t)P.maxn_lu * sizeof(zc), s3>>>(arena, piv, df.p + gr.start,
+                                                                               anorm.p, rcond, flag);
+        } else
+          k_getrf<<<gr.count, 256, getrf_smem, s>>>(arena, piv, df.p + gr.start, rcond, flag);
         break;
       case OP_DLR: {
         int mm = 1, nn = 1, cc = 1;
@@ -1235,7 +1271,15 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   }
+  if (s3) {
+    CK(cudaEventRecord(rc_ev, s3));
+    CK(cudaStreamWaitEvent(s, rc_ev, 0));
+  }
   CK(cudaStreamSynchronize(s));
+  if (s3) {
+    cudaEventDestroy(rc_ev);
+    cudaStreamDestroy(s3);
+  }
   cudaEventDestroy(fork_ev);
   cudaEventDestroy(join_ev);
   cudaStreamDestroy(s2);
@@ -1401,6 +1445,10 @@ static void hlu_factor_impl(cbie_hlu* F) {
   ovf.alloc(1);
   CK(cudaMemsetAsync(ovf.p, 0, 8, s));
   if (getenv("CBIE_PROFILE")) trunc_prof_enable(true, getenv("CBIE_ONESIDED") ? 1 : 0);
+  CK(cudaStreamSynchronize(s));
+  hlu_flops_reset();
+  trunc2_flops_reset();
+  lowrank_flops_reset();
   EvTimer tm;
   tm.start(s);
   Exec ex = run_plan(PL, work.p, F->ranks.p, F->piv.p, F->rcond.p, flag.p, ovf.p, g_plan_cache->tw, F->tol, s);
@@ -1472,7 +1520,9 @@ static void hlu_factor_impl(cbie_hlu* F) {
   }
   F->stat["launches"] = ex.launches;
   F->stat["tasks"] = (double)R.tasks.size();
-  F->stat["flops"] = R.flops;
+  // executed FP64 work, counted by the kernels with the device-side ranks
+  F->stat["flops"] = hlu_flops_read() + trunc2_flops_read() + lowrank_flops_read();
+  F->stat["flops_recorded_capacity"] = R.flops;
   F->stat["n_truncations"] = (double)R.trunc_count;
   F->stat["n_gemm"] = (double)R.gemm_count;
   F->stat["n_trsm"] = (double)R.trsm_count;

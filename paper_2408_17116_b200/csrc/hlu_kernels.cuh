@@ -39,6 +39,7 @@ __global__ void __launch_bounds__(256) k_gemm(zc* __restrict__ ar, const int* __
   const GemmD d = ds[blockIdx.z];
   const int m = dimv(d.m, ranks), n = dimv(d.n, ranks), k = dimv(d.k, ranks);
   const int i0 = blockIdx.x * GT, j0 = blockIdx.y * GT;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) flop_add(8.0 * m * n * k);
   if (i0 >= m || j0 >= n) return;
   __shared__ zc sA[GK][GT + 1];
   __shared__ zc sB[GK][GT + 1];
@@ -157,6 +158,7 @@ __global__ void __launch_bounds__(256) k_trsm(zc* __restrict__ ar, const int* __
                                               const TrsmD* __restrict__ ds) {
   const TrsmD d = ds[blockIdx.y];
   const int p = dimv(d.p, ranks), n = d.n;
+  if (blockIdx.x == 0 && threadIdx.x == 0) flop_add(4.0 * n * n * p);
   const int c0 = blockIdx.x * TS_COLS;
   if (c0 >= p) return;
   const int nc = min(TS_COLS, p - c0);
@@ -290,6 +292,7 @@ __global__ void __launch_bounds__(256) k_getrf(zc* __restrict__ ar, int* __restr
   const int n = d.n;
   zc* A = ar + d.A;
   int* piv = pivs + d.piv;
+  if (threadIdx.x == 0) flop_add(8.0 * n * (double)n * n / 3.0);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   zc* x = reinterpret_cast<zc*>(smem_raw);   // [n] estimator vector
   __shared__ double red[LR_NW];
@@ -435,3 +438,4 @@ __global__ void __launch_bounds__(256) k_getrf(zc* __restrict__ ar, int* __restr
     if (!(rcond >= 1e-14)) atomicOr(flag, 1);
   }
 }
+#include "dense_lu.cuh"

@@ -190,6 +190,7 @@ __device__ void trunc_task(const TruncDesc d, zc* arena, zc* aout, int* ranks, z
     if (threadIdx.x == 0) ranks[d.out_slot] = 0;
     return;
   }
+  if (threadIdx.x == 0) flop_add(flops_trunc(m, n, k, ident));
   if (!ident && k > KRAND && min(m, n) > 2 * RL0) {
     zc* Ms = reinterpret_cast<zc*>(smem_base);
     zc* Ws = Ms + SMEM_J * SMEM_J;
@@ -605,6 +606,9 @@ __global__ void __launch_bounds__(LR_NT) k_dense_lr(zc* arena, int* ranks,
       cta_gemm_tiled(Y, m, P, ld, 0, Z, n, m, n, l, gsm);    // Y = P Z
     }
     __syncthreads();
+    if (threadIdx.x == 0)   // range finder GEMMs, QR + Q formation, B = Q^H P
+      flop_add((exact && l == n ? 0.0 : 24.0 * m * (double)n * l) + flops_qr(m, min(m, l)) +
+               8.0 * m * (double)n * min(m, l));
     cta_qr(Y, m, l, m, rd, kap, red);
     const int lq = min(m, l);
     // Q = H_0..H_{lq-1} [I; 0] into U
@@ -664,3 +668,5 @@ void launch_dense_lr(zc* arena, int* ranks, const DenseLRDesc* d_desc, int nd, i
     CKL();
   }
 }
+
+CBIE_FLOP_API(lowrank)

@@ -60,3 +60,5 @@ bool launch_truncate_blocked(zc* arena, int* ranks, const TruncDesc* d_desc, int
     t2b::launch_rpl<12>(arena, arena_out, ranks, d_desc, nd, kc, tol, overflow, scratch, s, g_trunc_prof, defer);
   return true;
 }
+
+CBIE_FLOP_API(trunc2)

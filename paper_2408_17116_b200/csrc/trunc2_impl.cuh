@@ -445,6 +445,7 @@ __global__ void __launch_bounds__(NT, T2_MINB)
     if (threadIdx.x == 0) defer[1 + atomicAdd(defer, 1)] = base + blockIdx.x;
     return;
   }
+  if (threadIdx.x == 0) flop_add(flops_trunc(m, n, k, false));
   zc* U = arena + d.in_u;
   zc* Vt = arena + d.in_v;
   const int kk1 = min(m, k), kk2 = min(n, k);
