@@ -997,7 +997,8 @@ struct Exec {
 
 struct Grp {
   int kind, start, count, level, kmax;
-  int split = 0;   // OP_TRUNC: descriptors [start, start + split) have max(m, n) <= 192
+  int split = 0;       // OP_TRUNC: descriptors [start, start + split) form the first part
+  bool gram = false;   // OP_TRUNC: the first part runs the Gram path
 };
 
 // A recorded tape turned into launch groups with device-resident descriptors.
@@ -1067,10 +1068,14 @@ void make_plan(Plan& P, cudaStream_t s) {
       }
     }
     gr.count = (int)(j - i);
-    if (kind == OP_TRUNC) {   // small blocks first: they and the large ones run on two streams
-      auto small = [](const TruncDesc& d) { return std::max(d.m, d.n) <= 192; };
-      std::stable_partition(tr.begin() + gr.start, tr.end(), small);
-      gr.split = (int)std::count_if(tr.begin() + gr.start, tr.end(), small);
+    if (kind == OP_TRUNC) {
+      // factor-form problems (Gram path + hand-offs) first, dense-mode ones after; the
+      // two parts run on two streams.  Without the Gram path: small blocks / large blocks.
+      const bool gram = R.tol >= 1e-5 && getenv("CBIE_NO_GRAM") == nullptr;
+      auto first = [gram](const TruncDesc& d) { return gram ? d.in_v >= 0 : std::max(d.m, d.n) <= 192; };
+      std::stable_partition(tr.begin() + gr.start, tr.end(), first);
+      gr.split = (int)std::count_if(tr.begin() + gr.start, tr.end(), first);
+      gr.gram = gram;
     }
     groups.push_back(gr);
     i = j;
@@ -1224,7 +1229,23 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
           launch_truncate(arena, ranks, dtr.p + gr.start + b, e - b, gr.kmax, tol, ovf, w, st, kcm, mnm,
                           nullptr, dense ? 0 : TRUNC_NO_DENSE);
         };
-        if (gr.split > 0 && gr.split < gr.count) {
+        if (gr.gram) {
+          if (gr.split < gr.count) {
+            CK(cudaEventRecord(fork_ev, s));
+            CK(cudaStreamWaitEvent(s2, fork_ev, 0));
+            part(gr.split, gr.count, tw[1], s2);
+          }
+          int kcm = 1, mnm = 1;
+          for (int i = 0; i < gr.split; ++i) {
+            kcm = std::max(kcm, tr[gr.start + i].k);
+            mnm = std::max(mnm, std::max(tr[gr.start + i].m, tr[gr.start + i].n));
+          }
+          launch_truncate_routed(arena, ranks, dtr.p + gr.start, gr.split, gr.kmax, tol, ovf, tw[0], s, kcm, mnm);
+          if (gr.split < gr.count) {
+            CK(cudaEventRecord(join_ev, s2));
+            CK(cudaStreamWaitEvent(s, join_ev, 0));
+          }
+        } else if (gr.split > 0 && gr.split < gr.count) {
           CK(cudaEventRecord(fork_ev, s));
           CK(cudaStreamWaitEvent(s2, fork_ev, 0));
           part(gr.split, gr.count, tw[1], s2);

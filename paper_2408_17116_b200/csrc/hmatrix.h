@@ -88,19 +88,29 @@ constexpr int TRUNC_NO_DENSE = 1;
 struct TruncWork {
   DBuf<zc> scratch;    // per-CTA scratch of the blocked / unblocked kernels
   DBuf<int> defer;     // problems the blocked kernel hands to the unblocked one
+  DBuf<int> gdefer;    // problems the Gram kernel hands to the Householder kernels
   DBuf<zc> dscratch;   // scratch of the deferred launch
   void release() {
     scratch.release();
     defer.release();
+    gdefer.release();
     dscratch.release();
   }
 };
 void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
                      unsigned long long* overflow, TruncWork& work, cudaStream_t s,
                      int kc_max = 0, int mn_max = 0, zc* arena_out = nullptr, int flags = 0);
+// factor-form problems only: Gram path for device-side ranks <= 64 (trunc2.cu), the
+// others handed on to the blocked (k <= 128, max(m, n) <= 384) / unblocked kernels
+void launch_truncate_routed(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
+                            unsigned long long* overflow, TruncWork& work, cudaStream_t s, int kc_max,
+                            int mn_max);
+void launch_truncate_gram(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, double tol,
+                          unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, zc* arena_out,
+                          int* defer);
 bool launch_truncate_blocked(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, double tol,
                              unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, int kc_max,
-                             int mn_max, zc* arena_out, int* defer);
+                             int mn_max, zc* arena_out, int* defer, const int* idx = nullptr);
 
 // contiguous segment copies src[src + i] -> dst[dst + i] (aca.cu)
 struct CopySeg {

@@ -420,6 +420,51 @@ void trunc_prof_read(unsigned long long* h) {
   if (g_trunc_prof) cudaMemcpy(h, g_trunc_prof, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
 }
 
+// unblocked kernel over a device-side list of problems (list[0] = count): strided grid
+static void launch_unblocked_list(zc* arena, zc* arena_out, int* ranks, const TruncDesc* d_desc, int nd,
+                                  int kmax, int64_t per, double tol, unsigned long long* overflow,
+                                  TruncWork& work, cudaStream_t s, const int* list) {
+  DBuf<zc>& dscratch = work.dscratch;
+  const int grid = std::min(nd, 74);
+  if (dscratch.n < (size_t)grid * per) dscratch.alloc((size_t)grid * per);
+  const size_t smem = std::max((size_t)SMEM_J * SMEM_J * 3 * sizeof(zc) + SMEM_J * (sizeof(zc) + sizeof(double)),
+                               (size_t)SMEM_J * SMEM_J * 2 * sizeof(zc) +
+                                   (size_t)TG_K * (TG_R + 1 + 65) * sizeof(zc));
+  CK(cudaFuncSetAttribute(k_truncate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  k_truncate<<<grid, LR_NT, smem, s>>>(arena, arena_out, ranks, d_desc, dscratch.p, per, kmax, tol, overflow,
+                                       g_trunc_prof, list);
+  CKL();
+}
+
+void launch_truncate_routed(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
+                            unsigned long long* overflow, TruncWork& work, cudaStream_t s, int kc_max,
+                            int mn_max) {
+  if (nd == 0) return;
+  if (work.gdefer.n < (size_t)nd + 1) work.gdefer.alloc(std::max<size_t>(nd + 1, 4096));
+  CK(cudaMemsetAsync(work.gdefer.p, 0, sizeof(int), s));
+  launch_truncate_gram(arena, ranks, d_desc, nd, tol, overflow, work.scratch, s, nullptr, work.gdefer.p);
+  if (kc_max <= 64) return;   // no capacity can exceed the Gram path
+  const int* list = work.gdefer.p;
+  if (mn_max <= 384) {        // blocked Householder kernel over the Gram leftovers
+    int* dfr = nullptr;
+    if (kc_max > 128) {
+      if (work.defer.n < (size_t)nd + 1) work.defer.alloc(std::max<size_t>(nd + 1, 4096));
+      CK(cudaMemsetAsync(work.defer.p, 0, sizeof(int), s));
+      dfr = work.defer.p;
+    }
+    launch_truncate_blocked(arena, ranks, d_desc, nd, tol, overflow, work.scratch, s, kc_max, mn_max, arena,
+                            dfr, work.gdefer.p);
+    if (!dfr) return;
+    list = dfr;
+  }
+  kmax = std::max(std::max(kmax, 1), RLMAX);
+  const int64_t per = std::max<int64_t>((int64_t)kmax * kmax * 5 + 2 * (int64_t)kmax,
+                                        (int64_t)RLMAX * (4 * (int64_t)mn_max + kc_max + 1) +
+                                            2 * (int64_t)RLMAX * RLMAX) +
+                      4 * (int64_t)kmax;
+  launch_unblocked_list(arena, arena, ranks, d_desc, nd, kmax, per, tol, overflow, work, s, list);
+}
+
 void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
                      unsigned long long* overflow, TruncWork& work, cudaStream_t s, int kc_max,
                      int mn_max, zc* arena_out, int flags) {
@@ -448,16 +493,7 @@ void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int
                       4 * (int64_t)kmax;
   // waves keep the Jacobi scratch bounded (<= 1 GiB); the buffer is reused across calls
   if (dfr) {   // the blocked kernel's leftovers: a strided grid over the deferred list
-    DBuf<zc>& dscratch = work.dscratch;
-    const int grid = std::min(nd, 74);
-    if (dscratch.n < (size_t)grid * per) dscratch.alloc((size_t)grid * per);
-    const size_t smem = std::max((size_t)SMEM_J * SMEM_J * 3 * sizeof(zc) + SMEM_J * (sizeof(zc) + sizeof(double)),
-                                 (size_t)SMEM_J * SMEM_J * 2 * sizeof(zc) +
-                                     (size_t)TG_K * (TG_R + 1 + 65) * sizeof(zc));
-    CK(cudaFuncSetAttribute(k_truncate, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_truncate<<<grid, LR_NT, smem, s>>>(arena, arena_out, ranks, d_desc, dscratch.p, per, kmax, tol, overflow,
-                                         g_trunc_prof, dfr);
-    CKL();
+    launch_unblocked_list(arena, arena_out, ranks, d_desc, nd, kmax, per, tol, overflow, work, s, dfr);
     return;
   }
   const int wave = (int)std::max<int64_t>(1, ((int64_t)1 << 30) / (per * (int64_t)sizeof(zc)));
@@ -523,8 +559,13 @@ extern "C" int cbie_lowrank_truncate(cbie_ctx* c, const cbie_c128* U, int m, int
     CK(cudaMemsetAsync(ovf.p, 0, 8, s));
     TruncWork work;
     const int kmax = dense ? std::max(m, n) : std::min(k, std::max(m, n));
-    launch_truncate(ar.p, ranks.p, dd.p, 1, kmax, tol, ovf.p, work, s, k, std::max(m, n), nullptr,
-                    dense ? 0 : TRUNC_NO_DENSE);
+    // same routing as the H-LU executor (hlu.cu make_plan): factor form at tol >= 1e-5
+    // takes the Gram path (ranks <= 64) and its hand-offs
+    if (!dense && tol >= 1e-5 && getenv("CBIE_NO_GRAM") == nullptr)
+      launch_truncate_routed(ar.p, ranks.p, dd.p, 1, kmax, tol, ovf.p, work, s, k, std::max(m, n));
+    else
+      launch_truncate(ar.p, ranks.p, dd.p, 1, kmax, tol, ovf.p, work, s, k, std::max(m, n), nullptr,
+                      dense ? 0 : TRUNC_NO_DENSE);
     int rr = 0;
     CK(cudaMemcpyAsync(&rr, ranks.p, sizeof(int), cudaMemcpyDeviceToHost, s));
     std::vector<zc> out((size_t)(m + n) * cap);

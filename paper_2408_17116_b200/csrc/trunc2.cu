@@ -33,6 +33,7 @@
 #undef T2_MINB
 
 #define T2NS t2b
+#define T2_GRAM 1
 #define T2_NT 512
 #define T2_ELEMS 12800
 #define T2_MINB 1
@@ -41,12 +42,23 @@
 #undef T2_NT
 #undef T2_ELEMS
 #undef T2_MINB
+#undef T2_GRAM
 
 extern unsigned long long* g_trunc_prof;
 
+// Gram-path recompression of factor-form problems; those whose device-side rank
+// exceeds 64 are appended to defer (defer[0] = count, then indices into d_desc)
+void launch_truncate_gram(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, double tol,
+                          unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, zc* arena_out,
+                          int* defer) {
+  if (nd == 0) return;
+  t2b::launch_gram(arena, arena_out ? arena_out : arena, ranks, d_desc, nd, tol, overflow, scratch, s,
+                   g_trunc_prof, defer);
+}
+
 bool launch_truncate_blocked(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, double tol,
                              unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, int kc_max,
-                             int mn_max, zc* arena_out, int* defer) {
+                             int mn_max, zc* arena_out, int* defer, const int* idx) {
   if (getenv("CBIE_TRUNC_UNBLOCKED")) return false;
   if (kc_max <= 0 || mn_max <= 0 || mn_max > t2b::MMAX) return false;
   if (!arena_out) arena_out = arena;
@@ -55,9 +67,11 @@ bool launch_truncate_blocked(zc* arena, int* ranks, const TruncDesc* d_desc, int
   // blocks up to 192 rows: 256 threads, 96 KB, two CTAs per SM; larger blocks:
   // 512 threads, 200 KB (wider panels, fewer trailing passes), one CTA per SM
   if (mn_max <= 192)
-    t2s::launch_rpl<6>(arena, arena_out, ranks, d_desc, nd, kc, tol, overflow, scratch, s, g_trunc_prof, defer);
+    t2s::launch_rpl<6>(arena, arena_out, ranks, d_desc, nd, kc, tol, overflow, scratch, s, g_trunc_prof, defer,
+                       idx);
   else
-    t2b::launch_rpl<12>(arena, arena_out, ranks, d_desc, nd, kc, tol, overflow, scratch, s, g_trunc_prof, defer);
+    t2b::launch_rpl<12>(arena, arena_out, ranks, d_desc, nd, kc, tol, overflow, scratch, s, g_trunc_prof, defer,
+                        idx);
   return true;
 }
 

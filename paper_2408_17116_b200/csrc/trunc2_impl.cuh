@@ -428,11 +428,14 @@ template <int RPL>
 __global__ void __launch_bounds__(NT, T2_MINB)
     k_trunc2(zc* arena, zc* aout, int* ranks, const TruncDesc* __restrict__ descs, zc* scratch,
              int64_t per, int kc, double tol, unsigned long long* overflow, unsigned long long* prof,
-             int* defer, int base) {
+             int* defer, int base, const int* idx) {
   __shared__ Smem S;
   extern __shared__ __align__(16) unsigned char smraw[];
   zc* sm = reinterpret_cast<zc*>(smraw);
-  const TruncDesc d = descs[blockIdx.x];
+  // idx: run the problems listed in idx[1 + base + blockIdx.x] (count idx[0]) of descs
+  if (idx && base + (int)blockIdx.x >= idx[0]) return;
+  const int tix = idx ? idx[1 + base + blockIdx.x] : (int)blockIdx.x;
+  const TruncDesc d = descs[tix];
   const long long tc0 = clock64();
   if (d.skip_slot >= 0 && ranks[d.skip_slot] == 0) return;
   const int k = d.k_slot >= 0 ? ranks[d.k_slot] : d.k;
@@ -442,7 +445,7 @@ __global__ void __launch_bounds__(NT, T2_MINB)
     return;
   }
   if (k > kc) {   // larger than this kernel's layout: handed to the unblocked kernel
-    if (threadIdx.x == 0) defer[1 + atomicAdd(defer, 1)] = base + blockIdx.x;
+    if (threadIdx.x == 0) defer[1 + atomicAdd(defer, 1)] = idx ? tix : base + blockIdx.x;
     return;
   }
   if (threadIdx.x == 0) flop_add(flops_trunc(m, n, k, false));
@@ -582,7 +585,7 @@ __global__ void __launch_bounds__(NT, T2_MINB)
 template <int RPL>
 void launch_rpl(zc* arena, zc* aout, int* ranks, const TruncDesc* d_desc, int nd, int kc, double tol,
                 unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, unsigned long long* prof,
-                int* defer) {
+                int* defer, const int* idx = nullptr) {
   const int64_t per = scratch_per(kc);
   const int wave = (int)std::max<int64_t>(1, ((int64_t)2 << 30) / (per * (int64_t)sizeof(zc)));
   const size_t need = (size_t)std::min(wave, nd) * per;
@@ -591,11 +594,513 @@ void launch_rpl(zc* arena, zc* aout, int* ranks, const TruncDesc* d_desc, int nd
   CK(cudaFuncSetAttribute(k_trunc2<RPL>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   for (int b0 = 0; b0 < nd; b0 += wave) {
     const int nb = std::min(wave, nd - b0);
-    k_trunc2<RPL><<<nb, NT, smem, s>>>(arena, aout, ranks, d_desc + b0, scratch.p, per, kc, tol, overflow,
-                                       prof, defer, b0);
+    k_trunc2<RPL><<<nb, NT, smem, s>>>(arena, aout, ranks, idx ? d_desc : d_desc + b0, scratch.p, per, kc,
+                                       tol, overflow, prof, defer, b0, idx);
     CKL();
   }
 }
+
+#ifdef T2_GRAM
+// ---------------------------------------------------------------------------
+// Gram path (concatenated rank k <= KG, any m, n): the two Householder QRs and
+// the two Q applications of k_trunc2 -- k sequential column steps over m rows
+// each -- are replaced by one streaming pass per factor:
+//   1. G_u = U^H U, G_v = Vt^H Vt (k x k) accumulated from row chunks staged
+//      in shared memory (FMA-bound, no per-column barrier);
+//   2. column balancing (U_c, Vt_c) -> (U_c a_c, Vt_c / a_c), a_c = (|Vt_c|/|U_c|)^(1/2):
+//      exact for U Vt^T, makes the relative stop below scale-free;
+//   3. pivoted Cholesky of the balanced Grams: P^T G P = R^H R, stopped when the
+//      largest remaining pivot is <= CHOL_EPS * max diagonal (directions below
+//      ~3e-7 of the largest balanced column norm are dropped: far below
+//      tol * s_0 for every tol >= 1e-5 this path is used for);
+//      U = Q_u R_u P_u^T with Q_u = (U D P_u)[:, :k_u] R_u11^{-1} never formed;
+//   4. core M = (R_u P_u^T)(R_v P_v^T)^T and its SVD exactly as in k_trunc2
+//      (pivoted QR reduction + one-sided Jacobi), keep s > tol * s_0;
+//   5. U' = U_sel D R_u11^{-1} (M Vhat), Vt' = Vt_sel D^{-1} R_v11^{-1} conj(Vhat):
+//      two small triangular solves and one streaming GEMM per factor.
+// Same result as truncate_lowrank (hmatrix.py:412-426) up to the Gram rounding
+// (~sqrt(eps) relative), inside the solution-level parity budget.
+// ---------------------------------------------------------------------------
+constexpr int KG = 64;              // largest concatenated rank of the Gram path
+constexpr int GCH = 64;             // rows staged per Gram chunk
+constexpr int GSQ = KG * KG;        // one k x k region (zc)
+constexpr int GLD = KG + 1;         // staged row stride (bank spread)
+constexpr double CHOL_EPS = 1e-13;  // pivoted-Cholesky stop (squared, relative)
+
+__host__ __device__ inline int64_t gram_scratch_per() { return 4 * (int64_t)GSQ + 64; }
+
+// G (k x k, ld k, shared, zeroed) += X^H X, X (m x k) col-major ld ldx in global memory
+__device__ void gram_acc(const zc* __restrict__ X, int m, int k, int ldx, zc* G, zc* Xs) {
+  const int ta = (k + 3) / 4, tb = (k + 1) / 2, ntile = ta * tb;
+  const int groups = max(1, NT / ntile);
+  const int g = threadIdx.x / ntile, t = threadIdx.x % ntile;
+  const bool act = g < groups;
+  const int a0 = 4 * (t % ta), b0 = 2 * (t / ta);
+  zc acc[4][2];
+#pragma unroll
+  for (int qa = 0; qa < 4; ++qa)
+#pragma unroll
+    for (int qb = 0; qb < 2; ++qb) acc[qa][qb] = zmk(0.0, 0.0);
+  for (int r0 = 0; r0 < m; r0 += GCH) {
+    const int rows = min(GCH, m - r0);
+    __syncthreads();
+    {
+      zc v[GCH * KG / NT];
+#pragma unroll
+      for (int u = 0; u < GCH * KG / NT; ++u) {
+        const int e = threadIdx.x + u * NT;
+        v[u] = e < rows * k ? X[(int64_t)(e / rows) * ldx + r0 + e % rows] : zmk(0.0, 0.0);
+      }
+#pragma unroll
+      for (int u = 0; u < GCH * KG / NT; ++u) {
+        const int e = threadIdx.x + u * NT;
+        if (e < rows * k) Xs[(e % rows) * GLD + e / rows] = v[u];
+      }
+    }
+    __syncthreads();
+    if (act) {
+      for (int i = g; i < rows; i += groups) {
+        const zc* xr = Xs + i * GLD;
+        zc xa[4], xb[2];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) xa[q] = a0 + q < k ? xr[a0 + q] : zmk(0.0, 0.0);
+#pragma unroll
+        for (int q = 0; q < 2; ++q) xb[q] = b0 + q < k ? xr[b0 + q] : zmk(0.0, 0.0);
+#pragma unroll
+        for (int qa = 0; qa < 4; ++qa)
+#pragma unroll
+          for (int qb = 0; qb < 2; ++qb) {
+            const zc p = zcmul(xa[qa], xb[qb]);
+            acc[qa][qb].x += p.x;
+            acc[qa][qb].y += p.y;
+          }
+      }
+    }
+  }
+  if (act)
+#pragma unroll
+    for (int qa = 0; qa < 4; ++qa)
+#pragma unroll
+      for (int qb = 0; qb < 2; ++qb)
+        if (a0 + qa < k && b0 + qb < k) {
+          double* gp = reinterpret_cast<double*>(G + (b0 + qb) * k + a0 + qa);
+          atomicAdd(gp, acc[qa][qb].x);
+          atomicAdd(gp + 1, acc[qa][qb].y);
+        }
+  __syncthreads();
+}
+
+// pivoted Cholesky of the Hermitian G (k x k, ld k, shared) in place: row j < kk of G
+// holds row j of R (columns in pivoted order, entries >= j); perm[j] = original
+// column of pivot j.  Returns kk (pivots above thr_rel * max diagonal).
+__device__ int pchol(zc* G, int k, int* perm, double thr_rel, Smem& S) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int c = threadIdx.x; c < k; c += NT) perm[c] = c;
+  double dmax = 0.0;
+  for (int c = 0; c < k; ++c) dmax = fmax(dmax, G[c * k + c].x);
+  const double thr = thr_rel * dmax;
+  __syncthreads();
+  int j = 0;
+  for (; j < k; ++j) {
+    if (w == 0) {
+      double best = -1.0;
+      int bi = k;
+      for (int c = j + lane; c < k; c += 32) {
+        const double v = G[c * k + c].x;
+        if (v > best) {
+          best = v;
+          bi = c;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(FULL, best, o);
+        const int oi = __shfl_xor_sync(FULL, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      const bool go = best > thr && best > 0.0;
+      if (lane == 0) S.flag = go ? 0 : 1;
+      if (go) {
+        if (bi != j) {
+          for (int c = lane; c < k; c += 32) {   // rows j <-> bi
+            const zc t = G[c * k + j];
+            G[c * k + j] = G[c * k + bi];
+            G[c * k + bi] = t;
+          }
+          __syncwarp();
+          for (int i = lane; i < k; i += 32) {   // columns j <-> bi
+            const zc t = G[j * k + i];
+            G[j * k + i] = G[bi * k + i];
+            G[bi * k + i] = t;
+          }
+          if (lane == 0) {
+            const int t = perm[j];
+            perm[j] = perm[bi];
+            perm[bi] = t;
+          }
+          __syncwarp();
+        }
+        const double rjj = sqrt(G[j * k + j].x);
+        const double inv = 1.0 / rjj;
+        __syncwarp();
+        for (int c = j + 1 + lane; c < k; c += 32) G[c * k + j] = zscale(G[c * k + j], inv);
+        if (lane == 0) G[j * k + j] = zmk(rjj, 0.0);
+      }
+    }
+    __syncthreads();
+    if (S.flag) break;
+    const int rem = k - j - 1;
+    for (int e = threadIdx.x; e < rem * rem; e += NT) {
+      const int a = j + 1 + e % rem, b = j + 1 + e / rem;
+      G[b * k + a] = zsub(G[b * k + a], zcmul(G[a * k + j], G[b * k + j]));
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  return j;
+}
+
+// Z (kk x r, ld kk, shared) <- R11^{-1} Z with R11 = rows/cols 0..kk-1 of R (ld k), then
+// row j scaled by sc[j]; thread per column
+__device__ void tri_solve_cols(const zc* R, int k, int kk, zc* Z, int r, const double* sc) {
+  for (int l = threadIdx.x; l < r; l += NT) {
+    zc* z = Z + (int64_t)l * kk;
+    for (int a = kk - 1; a >= 0; --a) {
+      zc s = z[a];
+      for (int j = a + 1; j < kk; ++j) s = zsub(s, zmul(R[j * k + a], z[j]));
+      z[a] = zscale(s, 1.0 / R[a * k + a].x);
+    }
+    for (int a = 0; a < kk; ++a) z[a] = zscale(z[a], sc[a]);
+  }
+  __syncthreads();
+}
+
+// O (mo x r, ld mo, global) = X[:, perm[0..kk)] T (kk x r, ld kk, shared)
+__device__ void apply_sel(const zc* __restrict__ X, int mo, int ldx, const int* perm, int kk, const zc* T,
+                          int r, zc* __restrict__ O) {
+  const int ng = (r + 7) / 8;
+  for (int e = threadIdx.x; e < mo * ng; e += NT) {
+    const int i = e % mo, l0 = 8 * (e / mo);
+    zc acc[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) acc[q] = zmk(0.0, 0.0);
+    for (int j0 = 0; j0 < kk; j0 += 8) {
+      zc x[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) x[u] = j0 + u < kk ? X[(int64_t)perm[j0 + u] * ldx + i] : zmk(0.0, 0.0);
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (j0 + u < kk)
+#pragma unroll
+          for (int q = 0; q < 8; ++q)
+            if (l0 + q < r) zfma(acc[q], x[u], T[(l0 + q) * kk + j0 + u]);
+    }
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (l0 + q < r) O[(int64_t)(l0 + q) * mo + i] = acc[q];
+  }
+}
+
+// Hermitian eigenproblem H (n x n, ld n, shared) = X diag(h) X^H by cyclic two-sided
+// Jacobi with the round-robin parallel ordering; X (ld n, shared) enters as I.  The
+// rotation of pair (p, q) is the one of jacobi_nw for the 2 x 2 Gram [h_pp h_pq; . h_qq].
+// Returns the number of sweeps.
+__device__ int herm_jacobi(zc* H, int n, zc* X, Smem& S) {
+  __shared__ double rc[KG / 2];
+  __shared__ zc rs[KG / 2];
+  __shared__ int rp[KG / 2], rq[KG / 2];
+  if (n < 2) return 0;
+  const int ne = n + (n & 1), np = ne / 2;
+  constexpr int NB = 2 * KG * (KG / 2) / NT, NC = KG * (KG / 2) / NT;
+  int bi[NB], bt[NB], ci[NC], ct[NC];   // fixed (row, pair) items of this thread
+#pragma unroll
+  for (int u = 0; u < NB; ++u) {
+    const int e = threadIdx.x + u * NT;
+    const int f = e % (n * np);
+    bi[u] = e < 2 * n * np ? f % n : -1;
+    bt[u] = f / n + (e >= n * np ? KG : 0);   // + KG marks the X update
+  }
+#pragma unroll
+  for (int u = 0; u < NC; ++u) {
+    const int e = threadIdx.x + u * NT;
+    ci[u] = e < n * np ? e % n : -1;
+    ct[u] = e / n;
+  }
+  double f2 = 0.0;
+  for (int e = threadIdx.x; e < n * n; e += NT) f2 += zabs2(H[e]);
+  f2 = bsum(f2, S.red);
+  int sweep = 0;
+  for (; sweep < 30; ++sweep) {
+    double off = 0.0;
+    for (int e = threadIdx.x; e < n * n; e += NT)
+      if (e % n != e / n) off += zabs2(H[e]);
+    off = bsum(off, S.red);
+    if (!(off > 1e-26 * f2)) break;
+    for (int rd = 0; rd < ne - 1; ++rd) {
+      if (threadIdx.x < np) {
+        const int t = threadIdx.x;
+        const int pb = ne - 1 - t;
+        const int p = t == 0 ? 0 : ((t - 1 + rd) % (ne - 1)) + 1;
+        const int q = pb == 0 ? 0 : ((pb - 1 + rd) % (ne - 1)) + 1;
+        double cs = 1.0;
+        zc se = zmk(0.0, 0.0);
+        const bool ok = p < n && q < n;
+        if (ok) {
+          const double al = H[p * n + p].x, be = H[q * n + q].x;
+          const zc gm = H[q * n + p];   // h_pq
+          const double g = sqrt(zabs2(gm));
+          if (g > 1e-300 && g > 1e-17 * sqrt(fabs(al * be))) {
+            const double zeta = (be - al) / (2.0 * g);
+            const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            cs = 1.0 / sqrt(1.0 + tt * tt);
+            const double sn = cs * tt, ig = 1.0 / g;
+            se = zmk(gm.x * ig * sn, gm.y * ig * sn);
+          }
+        }
+        rp[t] = ok ? p : -1;
+        rq[t] = q;
+        rc[t] = cs;
+        rs[t] = se;
+      }
+      __syncthreads();
+      // columns: [h_p h_q] <- [h_p h_q] J, J = [cs se; -conj(se) cs]; same for X
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        if (bi[u] < 0) continue;
+        const int t = bt[u] & (KG - 1);
+        const int p = rp[t], q = rq[t];
+        if (p < 0) continue;
+        zc* A = bt[u] >= KG ? X : H;
+        const int i = bi[u];
+        const double cs = rc[t];
+        const zc se = rs[t];
+        const zc xi = A[p * n + i], yi = A[q * n + i];
+        A[p * n + i] = zsub(zscale(xi, cs), zmul(zconj(se), yi));
+        A[q * n + i] = zadd(zmul(se, xi), zscale(yi, cs));
+      }
+      __syncthreads();
+      // rows: H <- J^H H
+#pragma unroll
+      for (int u = 0; u < NC; ++u) {
+        if (ci[u] < 0) continue;
+        const int t = ct[u];
+        const int p = rp[t], q = rq[t];
+        if (p < 0) continue;
+        const int j = ci[u];
+        const double cs = rc[t];
+        const zc se = rs[t];
+        const zc xp = H[j * n + p], xq = H[j * n + q];
+        H[j * n + p] = zsub(zscale(xp, cs), zmul(se, xq));
+        H[j * n + q] = zadd(zmul(zconj(se), xp), zscale(xq, cs));
+      }
+      __syncthreads();
+    }
+  }
+  return sweep;
+}
+
+__global__ void __launch_bounds__(NT, 1)
+    k_trunc_gram(zc* arena, zc* aout, int* ranks, const TruncDesc* __restrict__ descs, zc* scratch, int64_t per,
+                 double tol, unsigned long long* overflow, unsigned long long* prof, int* defer, int base) {
+  __shared__ Smem S;
+  __shared__ double alpha[KG], ainv[KG], scu[KG], scv[KG];
+  __shared__ int pu[KG], pv[KG], posu[KG], posv[KG];
+  extern __shared__ __align__(16) unsigned char smraw[];
+  zc* sm = reinterpret_cast<zc*>(smraw);
+  zc* Gu = sm;
+  zc* Gv = sm + GSQ;
+  zc* X2 = sm + 2 * GSQ;
+  const TruncDesc d = descs[blockIdx.x];
+  const long long tc0 = clock64();
+  if (d.skip_slot >= 0 && ranks[d.skip_slot] == 0) return;
+  const int k = d.k_slot >= 0 ? ranks[d.k_slot] : d.k;
+  const int m = d.m, n = d.n;
+  if (k <= 0 || m == 0 || n == 0) {
+    if (threadIdx.x == 0) ranks[d.out_slot] = 0;
+    return;
+  }
+  if (k > KG) {   // handed to the Householder kernels
+    if (threadIdx.x == 0) defer[1 + atomicAdd(defer, 1)] = base + blockIdx.x;
+    return;
+  }
+  if (threadIdx.x == 0) flop_add(8.0 * (m + n) * (double)k * k);
+  const zc* U = arena + d.in_u;
+  const zc* Vt = arena + d.in_v;
+  zc* sc = scratch + (int64_t)blockIdx.x * per;
+  zc* Rug = sc;
+  zc* Rvg = sc + GSQ;
+  zc* Mg = sc + 2 * GSQ;
+  zc* Vhg = sc + 3 * GSQ;
+
+  // 1. Gram matrices
+  for (int e = threadIdx.x; e < 2 * GSQ; e += NT) sm[e] = zmk(0.0, 0.0);
+  __syncthreads();
+  gram_acc(U, m, k, d.ldu, Gu, X2);
+  gram_acc(Vt, n, k, d.ldv, Gv, X2);
+  // 2. balancing
+  for (int c = threadIdx.x; c < k; c += NT) {
+    const double du = Gu[c * k + c].x, dv = Gv[c * k + c].x;
+    const double a = (du > 0.0 && dv > 0.0) ? sqrt(sqrt(dv / du)) : 0.0;
+    alpha[c] = a;
+    ainv[c] = a > 0.0 ? 1.0 / a : 0.0;
+  }
+  __syncthreads();
+  for (int e = threadIdx.x; e < k * k; e += NT) {
+    const int a = e % k, b = e / k;
+    Gu[b * k + a] = zscale(Gu[b * k + a], alpha[a] * alpha[b]);
+    Gv[b * k + a] = zscale(Gv[b * k + a], ainv[a] * ainv[b]);
+  }
+  __syncthreads();
+  const long long tc1 = clock64();
+  // 3. pivoted Cholesky
+  const int ku = pchol(Gu, k, pu, CHOL_EPS, S);
+  const int kv = pchol(Gv, k, pv, CHOL_EPS, S);
+  if (ku == 0 || kv == 0) {
+    if (threadIdx.x == 0) ranks[d.out_slot] = 0;
+    return;
+  }
+  for (int c = threadIdx.x; c < k; c += NT) {
+    posu[pu[c]] = c;
+    posv[pv[c]] = c;
+  }
+  __syncthreads();
+  // 4. core M = (R_u P_u^T)(R_v P_v^T)^T  (ku x kv), kept in global for U' = M Vhat
+  for (int e = threadIdx.x; e < ku * kv; e += NT) {
+    const int a = e % ku, b = e / ku;
+    zc s = zmk(0.0, 0.0);
+    for (int c = 0; c < k; ++c) {
+      const int ju = posu[c], jv = posv[c];
+      if (ju >= a && jv >= b) zfma(s, Gu[ju * k + a], Gv[jv * k + b]);
+    }
+    X2[e] = s;
+  }
+  for (int e = threadIdx.x; e < k * k; e += NT) {
+    Rug[e] = Gu[e];
+    Rvg[e] = Gv[e];
+  }
+  __syncthreads();
+  const int kk1 = ku, kk2 = kv;
+  // 5. SVD of the core through H = M M^H, preconditioned: pivoted Cholesky
+  //    P^T H P = R^H R (stopped at (DELTA tol)^2 of the largest pivot, as the old
+  //    pivoted-QR reduction), then the graded G = R R^H = Z S^2 Z^H by two-sided
+  //    Jacobi (few sweeps).  Left singular vectors times S: W = P R^H Z; right
+  //    singular vectors: Vhat = M^H W / S^2.  Singular values below ~sqrt(eps) s_0
+  //    are not resolved, far below tol * s_0.
+  zc* H = Gu;
+  for (int e = threadIdx.x; e < kk1 * kk1; e += NT) {
+    const int a = e % kk1, b = e / kk1;
+    zc s = zmk(0.0, 0.0);
+    for (int c = 0; c < kk2; ++c) zfma(s, X2[c * kk1 + a], zconj(X2[c * kk1 + b]));
+    H[b * kk1 + a] = s;
+  }
+  for (int e = threadIdx.x; e < kk1 * kk2; e += NT) Mg[e] = X2[e];
+  __syncthreads();
+  const int kp = pchol(H, kk1, S.perm, (DELTA * tol) * (DELTA * tol), S);
+  zc* Gp = Gv;   // R R^H (kp x kp)
+  zc* Z = X2;    // eigenvectors (kp x kp)
+  for (int e = threadIdx.x; e < kp * kp; e += NT) {
+    const int a = e % kp, b = e / kp;
+    zc s = zmk(0.0, 0.0);
+    for (int j = max(a, b); j < kk1; ++j) zfma(s, H[j * kk1 + a], zconj(H[j * kk1 + b]));
+    Gp[b * kp + a] = s;
+    Z[b * kp + a] = zmk(a == b ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+  const long long tc2 = clock64();
+  const int sweeps = herm_jacobi(Gp, kp, Z, S);
+  for (int c = threadIdx.x; c < kp; c += NT) S.sig[c] = sqrt(fmax(Gp[c * kp + c].x, 0.0));
+  __syncthreads();
+  for (int c = threadIdx.x; c < kp; c += NT) {
+    int pos = 0;
+    for (int o = 0; o < kp; ++o)
+      if (S.sig[o] > S.sig[c] || (S.sig[o] == S.sig[c] && o < c)) ++pos;
+    S.order[pos] = c;
+  }
+  __syncthreads();
+  const long long tc3 = clock64();
+  const double s0 = kp > 0 ? S.sig[S.order[0]] : 0.0;
+  int r = 0;
+  if (s0 > 0.0) {
+    for (int c = 0; c < kp; ++c)
+      if (S.sig[c] > tol * s0) ++r;
+    r = max(r, 1);
+  }
+  if (r > d.cap) {
+    if (threadIdx.x == 0) atomicAdd(overflow, 1ull);
+    r = d.cap;
+  }
+  // W = P R^H Z_r (kk1 x r) in Gv's region (G dead: S.sig holds its diagonal)
+  __syncthreads();
+  zc* W = Gv;
+  for (int e = threadIdx.x; e < kk1 * r; e += NT) {
+    const int j = e % kk1, l = e / kk1;
+    const int c = S.order[l];
+    zc s = zmk(0.0, 0.0);
+    for (int a = 0; a <= min(j, kp - 1); ++a) zfma(s, zconj(H[j * kk1 + a]), Z[c * kp + a]);
+    W[(int64_t)l * kk1 + S.perm[j]] = s;
+  }
+  __syncthreads();
+  // conj(Vhat) = conj(M^H W / S^2) (kk2 x r) to global
+  for (int e = threadIdx.x; e < kk2 * r; e += NT) {
+    const int b = e % kk2, l = e / kk2;
+    const double sg = S.sig[S.order[l]];
+    zc s = zmk(0.0, 0.0);
+    for (int a = 0; a < kk1; ++a) zfma(s, zconj(Mg[b * kk1 + a]), W[(int64_t)l * kk1 + a]);
+    Vhg[(int64_t)l * kk2 + b] = zconj(zscale(s, 1.0 / (sg * sg)));
+  }
+  for (int j = threadIdx.x; j < kk1; j += NT) scu[j] = alpha[pu[j]];
+  for (int j = threadIdx.x; j < kk2; j += NT) scv[j] = ainv[pv[j]];
+  for (int e = threadIdx.x; e < k * k; e += NT) X2[e] = Rug[e];
+  __syncthreads();
+  // 6a. U' = U_sel D R_u11^{-1} W
+  tri_solve_cols(X2, k, kk1, W, r, scu);
+  zc* Uo = aout + d.out_u;
+  zc* Vo = aout + d.out_v;
+  if (r > 0) apply_sel(U, m, d.ldu, pu, kk1, W, r, Uo);
+  __syncthreads();
+  // 6b. Vt' = Vt_sel D^{-1} R_v11^{-1} conj(Vhat)
+  zc* W2 = Gu;
+  for (int e = threadIdx.x; e < k * k; e += NT) X2[e] = Rvg[e];
+  for (int e = threadIdx.x; e < kk2 * r; e += NT) W2[e] = Vhg[e];
+  __syncthreads();
+  tri_solve_cols(X2, k, kk2, W2, r, scv);
+  if (r > 0) apply_sel(Vt, n, d.ldv, pv, kk2, W2, r, Vo);
+  if (threadIdx.x == 0) {
+    ranks[d.out_slot] = r;
+    if (prof) {
+      const long long tc4 = clock64();
+      atomicAdd(prof + 0, (unsigned long long)(tc1 - tc0));
+      atomicAdd(prof + 1, (unsigned long long)(tc2 - tc1));
+      atomicAdd(prof + 2, (unsigned long long)(tc3 - tc2));
+      atomicAdd(prof + 3, (unsigned long long)(tc4 - tc3));
+      atomicAdd(prof + 4, 1ull);
+      atomicAdd(prof + 5, (unsigned long long)sweeps);
+      atomicAdd(prof + 14, 1ull);
+      atomicAdd(prof + 15, (unsigned long long)(tc4 - tc0));
+    }
+  }
+}
+
+void launch_gram(zc* arena, zc* aout, int* ranks, const TruncDesc* d_desc, int nd, double tol,
+                 unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, unsigned long long* prof,
+                 int* defer) {
+  const int64_t per = gram_scratch_per();
+  const int wave = (int)std::max<int64_t>(1, ((int64_t)2 << 30) / (per * (int64_t)sizeof(zc)));
+  const size_t need = (size_t)std::min(wave, nd) * per;
+  if (scratch.n < need) scratch.alloc(need);
+  const int smem = (3 * GSQ + KG + 1) * (int)sizeof(zc);
+  CK(cudaFuncSetAttribute(k_trunc_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  for (int b0 = 0; b0 < nd; b0 += wave) {
+    const int nb = std::min(wave, nd - b0);
+    k_trunc_gram<<<nb, NT, smem, s>>>(arena, aout, ranks, d_desc + b0, scratch.p, per, tol, overflow, prof,
+                                      defer, b0);
+    CKL();
+  }
+}
+#endif  // T2_GRAM
 
 }  // namespace T2NS
 }  // namespace
