@@ -38,6 +38,22 @@ def _dist():
     return rank, world, local
 
 
+def _fp64_peak():
+    """FP64 denominator: best probe of profiles/fp64_peak_r01.jsonl (cuBLAS ZGEMM/DGEMM
+    8192^3 and a DFMA chain, measured on this pool's B200 by tools/fp64_peak.cu)."""
+    best = 0.0
+    try:
+        with open(os.path.join(ROOT, "profiles", "fp64_peak_r01.jsonl")) as f:
+            for line in f:
+                line = line.strip()
+                if line.startswith("{"):
+                    best = max(best, float(json.loads(line).get("tflops", 0.0)))
+    except OSError:
+        pass
+    return (best, "measured (profiles/fp64_peak_r01.jsonl, cuBLAS ZGEMM 8192^3)") if best > 0 else \
+        (37.0, "fallback (B200 FP64 nominal)")
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -192,20 +208,28 @@ def run_gpu(args):
     ms = _reduce_max(ms, world)
     value = world * N / (ms / 1e3)
 
-    # roofline: dominant kernel = batched recompression (k_truncate), HBM-bound by
-    # B_rc = 16 (m+n)(4k + r) bytes per truncation
+    # roofline: dominant kernel group = the H-LU recompressions (Gram-path / blocked
+    # truncation kernels, trunc2.cu), FP64-bound; achieved = FP64 flops they executed
+    # (counted on the device with the ranks they saw, SURVEY 8(d) convention) / their
+    # CUDA-event time on the launching streams
     peaks, peak_src = _peaks()
-    tb = sum(f["trunc_alg_bytes"] for f in fstats)
+    fp64_peak, fp64_src = _fp64_peak()
+    tf = sum(f.get("flops_trunc2", 0.0) for f in fstats)
     tms = sum(f["trunc_kernel_ms"] for f in fstats)
     tl = sum(f["trunc_launches"] for f in fstats)
-    achieved = tb / (tms / 1e3) / 1e9 if tms > 0 else 0.0
-    hbm = float(peaks.get("hbm_gbs", 6650.0))
+    tb = sum(f["trunc_alg_bytes"] for f in fstats)
+    achieved = tf / (tms / 1e3) / 1e12 if tms > 0 else 0.0
     flops = sum(f["flops"] for f in fstats) / args.steps
-    roof = {"bound": "hbm", "kernel": "k_truncate (batched QR+QR+Jacobi-SVD recompression)",
-            "achieved": achieved, "peak": hbm, "unit": "GB/s", "frac": achieved / hbm,
-            "peak_source": peak_src, "traffic": None,
-            "alg_bytes_per_launch": tb / max(tl, 1), "avg_launch_ms": tms / max(tl, 1),
-            "share_of_step": tms / args.steps / ms}
+    hlu_ms = statistics.mean(f["factor_device_ms"] for f in fstats)
+    roof = {"bound": "tensor", "kernel": "H-LU recompression (k_trunc_gram + k_trunc2, FP64; "
+            "B200 DMMA and DFMA share the FP64 peak)",
+            "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
+            "peak_source": fp64_src, "traffic": None,
+            "flops_per_launch": tf / max(tl, 1), "avg_launch_ms": tms / max(tl, 1),
+            "share_of_step": tms / args.steps / ms,
+            "hbm_alg_bytes_per_launch": tb / max(tl, 1),
+            "hlu_fp64_tflops": flops / (hlu_ms / 1e3) / 1e12,
+            "hlu_fp64_frac": flops / (hlu_ms / 1e3) / 1e12 / fp64_peak}
 
     # e2e through the public API with host buffers (geometry in, solution out)
     e2e = None
@@ -247,6 +271,8 @@ def run_gpu(args):
             "phases_ms": {"fill": statistics.mean(h["fill_ms"] for h in hstats),
                           "hlu": statistics.mean(f["factor_device_ms"] for f in fstats)},
             "fp64_flops_per_step": flops,
+            "fp64_flops_note": "H-LU FP64 flops executed on the device (gemm/trsm/getrf/recompression/"
+                               "dense->LR, ranks as seen by the kernels); the fill is not counted",
             "compression_rate": hstats[-1]["compression_rate"],
             "clocks": clk.summary()}
     if e2e:

@@ -1230,7 +1230,7 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
                           nullptr, dense ? 0 : TRUNC_NO_DENSE);
         };
         if (gr.gram) {
-          if (gr.split < gr.count) {
+          if (gr.split < gr.count) {   // dense-mode problems on the second stream
             CK(cudaEventRecord(fork_ev, s));
             CK(cudaStreamWaitEvent(s2, fork_ev, 0));
             part(gr.split, gr.count, tw[1], s2);
@@ -1240,7 +1240,8 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
             kcm = std::max(kcm, tr[gr.start + i].k);
             mnm = std::max(mnm, std::max(tr[gr.start + i].m, tr[gr.start + i].n));
           }
-          launch_truncate_routed(arena, ranks, dtr.p + gr.start, gr.split, gr.kmax, tol, ovf, tw[0], s, kcm, mnm);
+          launch_truncate_routed(arena, ranks, dtr.p + gr.start, gr.split, gr.kmax, tol, ovf, tw[0], s, kcm, mnm,
+                                 &tw[1], s2);
           if (gr.split < gr.count) {
             CK(cudaEventRecord(join_ev, s2));
             CK(cudaStreamWaitEvent(s, join_ev, 0));
@@ -1542,7 +1543,10 @@ static void hlu_factor_impl(cbie_hlu* F) {
   F->stat["launches"] = ex.launches;
   F->stat["tasks"] = (double)R.tasks.size();
   // executed FP64 work, counted by the kernels with the device-side ranks
-  F->stat["flops"] = hlu_flops_read() + trunc2_flops_read() + lowrank_flops_read();
+  F->stat["flops_dense"] = hlu_flops_read();        // gemm, trsm, getrf
+  F->stat["flops_trunc2"] = trunc2_flops_read();    // Gram / blocked recompression
+  F->stat["flops_lowrank"] = lowrank_flops_read();  // unblocked recompression, dense -> low rank
+  F->stat["flops"] = F->stat["flops_dense"] + F->stat["flops_trunc2"] + F->stat["flops_lowrank"];
   F->stat["flops_recorded_capacity"] = R.flops;
   F->stat["n_truncations"] = (double)R.trunc_count;
   F->stat["n_gemm"] = (double)R.gemm_count;

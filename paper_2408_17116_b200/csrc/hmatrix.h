@@ -102,12 +102,14 @@ void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int
                      int kc_max = 0, int mn_max = 0, zc* arena_out = nullptr, int flags = 0);
 // factor-form problems only: Gram path for device-side ranks <= 64 (trunc2.cu), the
 // others handed on to the blocked (k <= 128, max(m, n) <= 384) / unblocked kernels
+// With a second stream / workspace the Householder share runs concurrently with the
+// Gram kernel: a routing kernel splits the problems by their device-side rank first.
 void launch_truncate_routed(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
                             unsigned long long* overflow, TruncWork& work, cudaStream_t s, int kc_max,
-                            int mn_max);
+                            int mn_max, TruncWork* work2 = nullptr, cudaStream_t s2 = nullptr);
 void launch_truncate_gram(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, double tol,
                           unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, zc* arena_out,
-                          int* defer);
+                          int* defer, const int* idx = nullptr);
 bool launch_truncate_blocked(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, double tol,
                              unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, int kc_max,
                              int mn_max, zc* arena_out, int* defer, const int* idx = nullptr);

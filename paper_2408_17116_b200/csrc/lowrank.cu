@@ -436,33 +436,85 @@ static void launch_unblocked_list(zc* arena, zc* arena_out, int* ranks, const Tr
   CKL();
 }
 
+namespace {
+// split problems by device-side rank: k <= 64 (and no-ops) -> la, k > 64 -> lb
+__global__ void k_route(const int* __restrict__ ranks, const TruncDesc* __restrict__ ds, int nd, int* la, int* lb) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nd; i += gridDim.x * blockDim.x) {
+    const TruncDesc& d = ds[i];
+    const int k = d.k_slot >= 0 ? ranks[d.k_slot] : d.k;
+    const bool skip = d.skip_slot >= 0 && ranks[d.skip_slot] == 0;
+    if (skip || k <= 64) la[1 + atomicAdd(la, 1)] = i;
+    else lb[1 + atomicAdd(lb, 1)] = i;
+  }
+}
+}  // namespace
+
 void launch_truncate_routed(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
                             unsigned long long* overflow, TruncWork& work, cudaStream_t s, int kc_max,
-                            int mn_max) {
+                            int mn_max, TruncWork* work2, cudaStream_t s2) {
   if (nd == 0) return;
+  if (kc_max <= 64) {   // no capacity can exceed the Gram path
+    launch_truncate_gram(arena, ranks, d_desc, nd, tol, overflow, work.scratch, s, nullptr, nullptr);
+    return;
+  }
+  TruncWork& wb = work2 ? *work2 : work;
+  cudaStream_t sb = work2 && s2 ? s2 : s;
   if (work.gdefer.n < (size_t)nd + 1) work.gdefer.alloc(std::max<size_t>(nd + 1, 4096));
-  CK(cudaMemsetAsync(work.gdefer.p, 0, sizeof(int), s));
-  launch_truncate_gram(arena, ranks, d_desc, nd, tol, overflow, work.scratch, s, nullptr, work.gdefer.p);
-  if (kc_max <= 64) return;   // no capacity can exceed the Gram path
-  const int* list = work.gdefer.p;
-  if (mn_max <= 384) {        // blocked Householder kernel over the Gram leftovers
+  if (wb.gdefer.n < (size_t)nd + 1 || &wb == &work) {
+    if (&wb == &work) {
+      if (work.defer.n < 2 * (size_t)nd + 2) work.defer.alloc(std::max<size_t>(2 * nd + 2, 8192));
+    } else {
+      wb.gdefer.alloc(std::max<size_t>(nd + 1, 4096));
+    }
+  }
+  int* la = work.gdefer.p;
+  int* lb = &wb == &work ? work.defer.p + nd + 1 : wb.gdefer.p;
+  CK(cudaMemsetAsync(la, 0, sizeof(int), s));
+  CK(cudaMemsetAsync(lb, 0, sizeof(int), s));
+  k_route<<<std::min((nd + 255) / 256, 148), 256, 0, s>>>(ranks, d_desc, nd, la, lb);
+  CKL();
+  cudaEvent_t fork = nullptr, join = nullptr;
+  if (sb != s) {
+    CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    CK(cudaEventRecord(fork, s));
+    CK(cudaStreamWaitEvent(sb, fork, 0));
+  }
+  // ranks > 64: blocked Householder kernel (k <= 128, max(m, n) <= 384), then unblocked
+  const int* list = lb;
+  bool done = false;
+  if (mn_max <= 384) {
     int* dfr = nullptr;
     if (kc_max > 128) {
-      if (work.defer.n < (size_t)nd + 1) work.defer.alloc(std::max<size_t>(nd + 1, 4096));
-      CK(cudaMemsetAsync(work.defer.p, 0, sizeof(int), s));
-      dfr = work.defer.p;
+      if (&wb == &work) {
+        dfr = work.defer.p;   // first nd + 1 entries
+      } else {
+        if (wb.defer.n < (size_t)nd + 1) wb.defer.alloc(std::max<size_t>(nd + 1, 4096));
+        dfr = wb.defer.p;
+      }
+      CK(cudaMemsetAsync(dfr, 0, sizeof(int), sb));
     }
-    launch_truncate_blocked(arena, ranks, d_desc, nd, tol, overflow, work.scratch, s, kc_max, mn_max, arena,
-                            dfr, work.gdefer.p);
-    if (!dfr) return;
-    list = dfr;
+    launch_truncate_blocked(arena, ranks, d_desc, nd, tol, overflow, wb.scratch, sb, kc_max, mn_max, arena, dfr,
+                            lb);
+    if (!dfr) done = true;
+    else list = dfr;
   }
-  kmax = std::max(std::max(kmax, 1), RLMAX);
-  const int64_t per = std::max<int64_t>((int64_t)kmax * kmax * 5 + 2 * (int64_t)kmax,
-                                        (int64_t)RLMAX * (4 * (int64_t)mn_max + kc_max + 1) +
-                                            2 * (int64_t)RLMAX * RLMAX) +
-                      4 * (int64_t)kmax;
-  launch_unblocked_list(arena, arena, ranks, d_desc, nd, kmax, per, tol, overflow, work, s, list);
+  if (!done) {
+    kmax = std::max(std::max(kmax, 1), RLMAX);
+    const int64_t per = std::max<int64_t>((int64_t)kmax * kmax * 5 + 2 * (int64_t)kmax,
+                                          (int64_t)RLMAX * (4 * (int64_t)mn_max + kc_max + 1) +
+                                              2 * (int64_t)RLMAX * RLMAX) +
+                        4 * (int64_t)kmax;
+    launch_unblocked_list(arena, arena, ranks, d_desc, nd, kmax, per, tol, overflow, wb, sb, list);
+  }
+  // ranks <= 64: Gram kernel over its list (concurrently when sb != s)
+  launch_truncate_gram(arena, ranks, d_desc, nd, tol, overflow, work.scratch, s, nullptr, nullptr, la);
+  if (sb != s) {
+    CK(cudaEventRecord(join, sb));
+    CK(cudaStreamWaitEvent(s, join, 0));
+    cudaEventDestroy(fork);
+    cudaEventDestroy(join);
+  }
 }
 
 void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,

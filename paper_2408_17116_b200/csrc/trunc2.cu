@@ -50,10 +50,10 @@ extern unsigned long long* g_trunc_prof;
 // exceeds 64 are appended to defer (defer[0] = count, then indices into d_desc)
 void launch_truncate_gram(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, double tol,
                           unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, zc* arena_out,
-                          int* defer) {
+                          int* defer, const int* idx) {
   if (nd == 0) return;
   t2b::launch_gram(arena, arena_out ? arena_out : arena, ranks, d_desc, nd, tol, overflow, scratch, s,
-                   g_trunc_prof, defer);
+                   g_trunc_prof, defer, idx);
 }
 
 bool launch_truncate_blocked(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, double tol,

@@ -904,7 +904,8 @@ __device__ int herm_jacobi(zc* H, int n, zc* X, Smem& S) {
 
 __global__ void __launch_bounds__(NT, 1)
     k_trunc_gram(zc* arena, zc* aout, int* ranks, const TruncDesc* __restrict__ descs, zc* scratch, int64_t per,
-                 double tol, unsigned long long* overflow, unsigned long long* prof, int* defer, int base) {
+                 double tol, unsigned long long* overflow, unsigned long long* prof, int* defer, int base,
+                 const int* idx) {
   __shared__ Smem S;
   __shared__ double alpha[KG], ainv[KG], scu[KG], scv[KG];
   __shared__ int pu[KG], pv[KG], posu[KG], posv[KG];
@@ -913,7 +914,10 @@ __global__ void __launch_bounds__(NT, 1)
   zc* Gu = sm;
   zc* Gv = sm + GSQ;
   zc* X2 = sm + 2 * GSQ;
-  const TruncDesc d = descs[blockIdx.x];
+  // idx: run the problems listed in idx[1 + base + blockIdx.x] (count idx[0]) of descs
+  if (idx && base + (int)blockIdx.x >= idx[0]) return;
+  const int tix = idx ? idx[1 + base + blockIdx.x] : (int)blockIdx.x;
+  const TruncDesc d = descs[tix];
   const long long tc0 = clock64();
   if (d.skip_slot >= 0 && ranks[d.skip_slot] == 0) return;
   const int k = d.k_slot >= 0 ? ranks[d.k_slot] : d.k;
@@ -923,7 +927,7 @@ __global__ void __launch_bounds__(NT, 1)
     return;
   }
   if (k > KG) {   // handed to the Householder kernels
-    if (threadIdx.x == 0) defer[1 + atomicAdd(defer, 1)] = base + blockIdx.x;
+    if (threadIdx.x == 0) defer[1 + atomicAdd(defer, 1)] = idx ? tix : base + blockIdx.x;
     return;
   }
   if (threadIdx.x == 0) flop_add(8.0 * (m + n) * (double)k * k);
@@ -1069,6 +1073,9 @@ __global__ void __launch_bounds__(NT, 1)
   tri_solve_cols(X2, k, kk2, W2, r, scv);
   if (r > 0) apply_sel(Vt, n, d.ldv, pv, kk2, W2, r, Vo);
   if (threadIdx.x == 0) {
+    // applies, pivoted Choleskys, M and H products, Jacobi sweeps (Gram counted above)
+    flop_add(8.0 * ((double)m * kk1 + (double)n * kk2) * r + 16.0 * k * (double)k * k / 3.0 +
+             8.0 * kk1 * (double)kk2 * (k + kk1) + 32.0 * sweeps * (double)kp * kp * kp);
     ranks[d.out_slot] = r;
     if (prof) {
       const long long tc4 = clock64();
@@ -1086,7 +1093,7 @@ __global__ void __launch_bounds__(NT, 1)
 
 void launch_gram(zc* arena, zc* aout, int* ranks, const TruncDesc* d_desc, int nd, double tol,
                  unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, unsigned long long* prof,
-                 int* defer) {
+                 int* defer, const int* idx) {
   const int64_t per = gram_scratch_per();
   const int wave = (int)std::max<int64_t>(1, ((int64_t)2 << 30) / (per * (int64_t)sizeof(zc)));
   const size_t need = (size_t)std::min(wave, nd) * per;
@@ -1095,8 +1102,8 @@ void launch_gram(zc* arena, zc* aout, int* ranks, const TruncDesc* d_desc, int n
   CK(cudaFuncSetAttribute(k_trunc_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   for (int b0 = 0; b0 < nd; b0 += wave) {
     const int nb = std::min(wave, nd - b0);
-    k_trunc_gram<<<nb, NT, smem, s>>>(arena, aout, ranks, d_desc + b0, scratch.p, per, tol, overflow, prof,
-                                      defer, b0);
+    k_trunc_gram<<<nb, NT, smem, s>>>(arena, aout, ranks, idx ? d_desc : d_desc + b0, scratch.p, per, tol,
+                                      overflow, prof, defer, b0, idx);
     CKL();
   }
 }
