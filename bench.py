@@ -8,6 +8,8 @@ K3), H-matrix fill (dense leaves K2/K4, batched ACA K5, recompression K6) and
 the H-LU factorisation (K7-K10).  metric = unknowns/s = N / (fill + H-LU time).
 For N > 1 (torchrun) every rank factors its own replica of the problem
 (weak scaling, no data-path collective); value = N * ranks / max step time.
+Beside it, "fill_sharded" times the fill of ONE problem with its leaves sharded
+over the ranks plus the NCCL exchange of the shards (strong scaling of the fill).
 
 --impl reference times the CPU oracle (numpy restatement of the reference,
 oracle/) on a bounded sample of the same workload (see oracle/baseline.py).
@@ -231,6 +233,36 @@ def run_gpu(args):
             "hlu_fp64_tflops": flops / (hlu_ms / 1e3) / 1e12,
             "hlu_fp64_frac": flops / (hlu_ms / 1e3) / 1e12 / fp64_peak}
 
+    # N > 1: the fill of ONE problem sharded over the ranks (LPT leaf partition, no
+    # collective during the fill) + the NCCL exchange of the shards (csrc/shard.cu);
+    # max-over-ranks device time, reported beside the replica throughput
+    fill_shard = None
+    if world > 1:
+        from paper_2408_17116_b200 import dist as cdist
+        cdist.init_nccl(gen, rank, world)
+        HS = hm.HMatrix(gen, prob.n_leaf, prob.eta, prob.aca_tol, shard=(rank, world, True))   # warm-up
+        del HS
+        t_f, t_x = [], []
+        for _ in range(max(1, args.steps)):
+            _barrier(world)
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            HS = hm.HMatrix(gen, prob.n_leaf, prob.eta, prob.aca_tol, shard=(rank, world, True))
+            b.record(stream)
+            torch.cuda.synchronize()
+            t_f.append(a.elapsed_time(b))
+            t_x.append(HS.stats().get("exchange_ms", 0.0))
+            del HS
+        f_ms = _reduce_max(statistics.median(t_f), world)
+        x_ms = _reduce_max(statistics.median(t_x), world)
+        single = statistics.mean(h["fill_ms"] for h in hstats)
+        fill_shard = {"ms": f_ms, "exchange_ms": x_ms, "single_gpu_fill_ms": single,
+                      "leaves": "LPT partition of the block-tree leaves, ncclBroadcast of the shards",
+                      "speedup_vs_replica_fill": single / f_ms if f_ms > 0 else None}
+        cdist.finalize(gen)
+
     # e2e through the public API with host buffers (geometry in, solution out)
     e2e = None
     if not args.no_e2e:
@@ -277,6 +309,8 @@ def run_gpu(args):
             "clocks": clk.summary()}
     if e2e:
         line["e2e"] = e2e
+    if fill_shard:
+        line["fill_sharded"] = fill_shard
     if rank == 0 and world == 1 and not args.no_cpu:
         v, sec, desc, det = cpu_baseline_line(args.config, 1, 0, args.ref_level)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "sample": desc,

@@ -38,6 +38,7 @@ enum {
   CBIE_ECAP_EXCEEDED = 4,        /* errors.py:44  CapExceeded       */
   CBIE_ERANK_OVERFLOW = 5,       /* errors.py:36  RankOverflow      */
   CBIE_ECUDA = 10,
+  CBIE_ENCCL = 11,
   CBIE_EOOM = 12,
   CBIE_EINVALID = 13,
   CBIE_ESTATE = 14               /* call made before its prerequisites */
@@ -155,6 +156,32 @@ int cbie_hlu_solve(cbie_hlu* f, const cbie_c128* b, cbie_c128* x, int nrhs);
  * (hmatrix.py:605-609, k ignored). */
 int cbie_lowrank_truncate(cbie_ctx* ctx, const cbie_c128* U, int m, int k, const cbie_c128* V,
                           int n, double tol, int* r, cbie_c128* Uo, cbie_c128* Vo);
+
+/* ---- multi-GPU fill (one process per GPU, NCCL over NVLink / NVSwitch) ----
+ * The reference fills leaves with a thread pool over HMatrix._fill_leaf
+ * (hmatrix.py:207-224, 243-264); here each process fills the leaves it owns and
+ * the shards are exchanged with ncclBroadcast. */
+
+/* Deterministic LPT partition of n work items (leaves) over `world` owners by
+ * cost (largest first, each to the least-loaded owner, ties to the lowest rank).
+ * Host-only, no GPU needed. */
+void cbie_partition_lpt(const double* cost, int64_t n, int world, int* owner);
+
+/* ncclGetUniqueId into out (cap >= 128 bytes); rank 0 creates it, the caller
+ * distributes it (torch.distributed / any side channel). */
+int cbie_nccl_unique_id(char* out, int cap);
+
+/* NCCL communicator of this context (rank, world); cbie_dist_finalize drops it. */
+int cbie_dist_init(cbie_ctx* ctx, const char* nccl_id, int rank, int world);
+void cbie_dist_finalize(cbie_ctx* ctx);
+
+/* cbie_hmatrix_build with leaf sharding: this process fills the leaves the LPT
+ * partition gives `rank`; exchange != 0 broadcasts the shards (needs
+ * cbie_dist_init with the same rank / world) so every rank holds the complete
+ * H-matrix.  exchange == 0 leaves a partial H-matrix (cbie_hmatrix_leaf reports
+ * kind -1 for leaves owned elsewhere) -- used to check the shards on one GPU. */
+int cbie_hmatrix_build_shard(cbie_ctx* ctx, int n_leaf, double eta, double aca_tol, int rank,
+                             int world, int exchange, cbie_hmat** out);
 
 /* Timings (CUDA events), counts, flops, bytes as one JSON object.
  * which: 0 = context, 1 = hmatrix, 2 = hlu. */

@@ -55,6 +55,12 @@ _SIGS = {
     "cbie_lowrank_truncate": (ct.c_int, [P, P, ct.c_int, ct.c_int, P, ct.c_int, ct.c_double,
                                          ct.POINTER(ct.c_int), P, P]),
     "cbie_stats_json": (ct.c_int, [P, ct.c_int, ct.c_char_p, ct.c_size_t]),
+    "cbie_partition_lpt": (None, [P, ct.c_int64, ct.c_int, P]),
+    "cbie_nccl_unique_id": (ct.c_int, [ct.c_char_p, ct.c_int]),
+    "cbie_dist_init": (ct.c_int, [P, ct.c_char_p, ct.c_int, ct.c_int]),
+    "cbie_dist_finalize": (None, [P]),
+    "cbie_hmatrix_build_shard": (ct.c_int, [P, ct.c_int, ct.c_double, ct.c_double, ct.c_int, ct.c_int,
+                                            ct.c_int, ct.POINTER(P)]),
 }
 
 EXPORTED = tuple(_SIGS)

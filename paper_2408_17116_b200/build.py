@@ -59,7 +59,7 @@ def build(verbose: bool = False) -> str:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
     if (not os.path.exists(LIB)
             or max(os.path.getmtime(o) for o in objs) > os.path.getmtime(LIB)):
-        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs]
+        cmd = [NVCC, *ARCH, "-shared", "-o", LIB, *objs, "-lnccl"]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed:\n{r.stdout}\n{r.stderr}")

@@ -333,11 +333,17 @@ static void hmatrix_build(cbie_hmat* H, int n_leaf) {
   // ---- storage: dense leaves first (m x n each); low-rank leaves are appended
   // wave by wave with their EXACT ranks (U m x r, Vt n x r), so the arena holds
   // sum (m+n) r instead of (m+n) * budget (config 5: ~20 GB instead of ~1.5 TB) ----
+  // leaf ownership (single process: every leaf local); dense storage owner-major so
+  // each process's dense leaves are one contiguous range (shard exchange)
+  shard_assign(H);
   int64_t used = 0;
-  for (auto& L : T.leaves)
-    if (L.kind == BLK_DENSE) {
-      L.off_d = used;
-      used += (int64_t)L.m * L.n;
+  for (int o = 0; o < H->shard_world; ++o)
+    for (int li = 0; li < nleaf; ++li) {
+      auto& L = T.leaves[li];
+      if (L.kind == BLK_DENSE && (H->owner.empty() || H->owner[li] == o)) {
+        L.off_d = used;
+        used += (int64_t)L.m * L.n;
+      }
     }
   // low-rank region: the capacity bound sum (m+n) min(budget, 128) when it fits in
   // half of the free HBM, else half of the free HBM (grown on demand, rarely)
@@ -353,7 +359,14 @@ static void hmatrix_build(cbie_hmat* H, int n_leaf) {
   }
   std::vector<int> aca_leaf;
   for (int li = 0; li < nleaf; ++li)
-    if (T.leaves[li].kind == BLK_LR) aca_leaf.push_back(li);
+    if (T.leaves[li].kind == BLK_LR) {
+      if (H->owns(li)) {
+        aca_leaf.push_back(li);
+      } else {   // filled by another process
+        T.leaves[li].cap = 1;
+        T.leaves[li].off_u = T.leaves[li].off_v = -1;
+      }
+    }
   const int nadm = (int)aca_leaf.size();
   H->rank.alloc(nleaf + nadm + 1);
   CK(cudaMemsetAsync(H->rank.p, 0, sizeof(int) * H->rank.n, s));
@@ -362,11 +375,13 @@ static void hmatrix_build(cbie_hmat* H, int n_leaf) {
   tm.start(s);
   // ---- dense leaves ----
   std::vector<TileDesc> tiles;
-  for (auto& L : T.leaves)
-    if (L.kind == BLK_DENSE) {
+  for (int li = 0; li < nleaf; ++li) {
+    const auto& L = T.leaves[li];
+    if (L.kind == BLK_DENSE && H->owns(li)) {
       const Cluster &R = T.cl[L.r], &Cc = T.cl[L.c];
       tiles.push_back(TileDesc{L.off_d, R.lo, R.hi, Cc.lo, Cc.hi});
     }
+  }
   DBuf<TileDesc> dt;
   dt.upload(tiles, s);
   launch_fill_tiles(c, dt.p, (int)tiles.size(), H->d_pperm.p, H->arena.p, 1, s);
@@ -560,17 +575,21 @@ static void hmatrix_build(cbie_hmat* H, int n_leaf) {
   H->overflow = (int64_t)hovf;
   H->h_rank.resize(nleaf);
   CK(cudaMemcpy(H->h_rank.data(), H->rank.p, sizeof(int) * nleaf, cudaMemcpyDeviceToHost));
+  H->partial = H->shard_world > 1;
   int64_t stored = 0;
   for (int li = 0; li < nleaf; ++li) {
     auto& L = T.leaves[li];
+    if (!H->owns(li)) continue;
     stored += L.kind == BLK_DENSE ? (int64_t)L.m * L.n : (int64_t)H->h_rank[li] * (L.m + L.n);
   }
+  H->stat["arena_used"] = (double)used;
   H->stat["dense_fill_ms"] = dense_ms;
   H->stat["aca_ms"] = aca_ms;
   H->stat["recompress_ms"] = trunc_ms;
   H->stat["demote_fill_ms"] = demote_ms;
   H->stat["fill_ms"] = dense_ms + aca_ms + trunc_ms + demote_ms;
   H->stat["n_leaves"] = nleaf;
+  H->stat["n_local_leaves"] = (double)(tiles.size() + aca_leaf.size());
   H->stat["n_dense"] = (double)tiles.size() + demoted;
   H->stat["n_lowrank"] = (double)(nadm - demoted);
   H->stat["demoted"] = (double)demoted;
@@ -579,6 +598,8 @@ static void hmatrix_build(cbie_hmat* H, int n_leaf) {
   H->stat["compression_rate"] = 1.0 - (double)stored / ((double)H->N * (double)H->N);
   H->stat["arena_bytes"] = (double)used * sizeof(zc);
 }
+
+void hmatrix_build_entry(cbie_hmat* H, int n_leaf) { hmatrix_build(H, n_leaf); }
 
 // ---------------------------------------------------------------------------
 // matvec (HMatrix.matvec, hmatrix.py:267-274), deterministic
@@ -694,6 +715,11 @@ int cbie_hmatrix_leaf(cbie_hmat* h, int64_t leaf, int* kind, int* rank, cbie_c12
     if (leaf < 0 || leaf >= (int64_t)T.leaves.size()) throw cbie_error(CBIE_EINVALID, "leaf index");
     const auto& L = T.leaves[leaf];
     cudaSetDevice(h->ctx->device);
+    if (h->partial && !h->owns((int)leaf)) {   // filled by another shard, not exchanged yet
+      *kind = -1;
+      *rank = 0;
+      return CBIE_OK;
+    }
     *kind = L.kind == BLK_LR ? 1 : 0;
     const int m = L.m, n = L.n;
     if (L.kind == BLK_DENSE) {
@@ -731,6 +757,7 @@ int cbie_hmatrix_leaf(cbie_hmat* h, int64_t leaf, int* kind, int* rank, cbie_c12
 int cbie_hmatvec(cbie_hmat* h, const cbie_c128* x, cbie_c128* y, int nrhs) {
   try {
     cudaSetDevice(h->ctx->device);
+    if (h->partial) throw cbie_error(CBIE_ESTATE, "partial (sharded) H-matrix: exchange the shards first");
     cudaStream_t s = h->ctx->stream;
     const int64_t N = h->N;
     const int C = h->tree.C;

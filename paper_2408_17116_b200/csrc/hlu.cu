@@ -1633,6 +1633,7 @@ int cbie_hlu_factor(cbie_hmat* h, double trunc_tol, cbie_hlu** out) {
   try {
     cudaSetDevice(h->ctx->device);
     if (!(trunc_tol > 0.0 && trunc_tol < 1.0)) throw cbie_error(CBIE_EINVALID, "trunc_tol in (0,1)");
+    if (h->partial) throw cbie_error(CBIE_ESTATE, "partial (sharded) H-matrix: exchange the shards first");
     F = new cbie_hlu();
     F->H = h;
     F->tol = trunc_tol;

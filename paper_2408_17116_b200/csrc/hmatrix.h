@@ -61,7 +61,19 @@ struct cbie_hmat {
   int demoted = 0;
   int64_t overflow = 0;        // truncations clipped at capacity
   std::map<std::string, double> stat;
+  // leaf sharding (shard.cu): this process fills the leaves with owner[li] == shard_rank
+  int shard_rank = 0, shard_world = 1;
+  std::vector<int> owner;      // [nleaf], empty = every leaf local
+  std::vector<uint8_t> adm;    // [nleaf] admissible in the block tree (before demotion)
+  bool partial = false;        // true until the shards were exchanged
+  bool owns(int li) const { return owner.empty() || owner[li] == shard_rank; }
 };
+
+// shard.cu: LPT partition of the leaves over `world` processes by estimated fill cost
+void shard_assign(cbie_hmat* H);
+// shard.cu: exchange the shards over the context's NCCL communicator (every rank ends
+// up with the complete H-matrix, same layout on all ranks)
+void shard_exchange(cbie_hmat* H);
 
 // lowrank.cu: batched truncation  (hmatrix.py:412-426, 605-609)
 // inputs are col-major U (m x k) and Vt (n x k) = V^T; they are used as workspace.

@@ -1,0 +1,42 @@
+"""Multi-GPU plumbing of the H-matrix fill: one process per GPU,
+torch.distributed only to hand the NCCL unique id to every rank; the shard
+exchange itself is ncclBroadcast inside libcbie (csrc/shard.cu).
+
+The reference parallelises the fill with a ThreadPoolExecutor over leaves
+(hmatrix.py:217-219); here the leaves are partitioned over processes by the
+same deterministic LPT rule on every rank (partition_lpt)."""
+
+from __future__ import annotations
+
+import ctypes as ct
+
+import numpy as np
+
+from . import _ffi
+
+
+def partition_lpt(cost, world: int) -> np.ndarray:
+    """Owner of every work item: largest cost first, each to the least-loaded rank
+    (ties to the lowest rank).  Host-only (cbie_partition_lpt)."""
+    lib = _ffi.load()
+    c = np.ascontiguousarray(np.asarray(cost, dtype=np.float64))
+    owner = np.empty(c.shape[0], np.int32)
+    lib.cbie_partition_lpt(_ffi.ptr(c), int(c.shape[0]), int(world), _ffi.ptr(owner))
+    return owner
+
+
+def init_nccl(gen, rank: int, world: int, group=None) -> None:
+    """Create the context's NCCL communicator: rank 0 draws the unique id, the
+    default torch.distributed group (any backend) carries it to every rank."""
+    import torch.distributed as dist
+    lib = gen.dev.lib
+    buf = ct.create_string_buffer(128)
+    if rank == 0:
+        _ffi.check(lib.cbie_nccl_unique_id(buf, 128))
+    obj = [bytes(buf.raw) if rank == 0 else None]
+    dist.broadcast_object_list(obj, src=0, group=group)
+    gen.dev.check(lib.cbie_dist_init(gen.dev.h, obj[0], int(rank), int(world)))
+
+
+def finalize(gen) -> None:
+    gen.dev.lib.cbie_dist_finalize(gen.dev.h)

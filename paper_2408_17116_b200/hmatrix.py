@@ -17,16 +17,26 @@ from . import _ffi
 class HMatrix:
     """H-matrix of the equilibrated system D_r A D_c (solver.py:132-145)."""
 
-    def __init__(self, gen, n_leaf: int, eta: float, aca_tol: float):
+    def __init__(self, gen, n_leaf: int, eta: float, aca_tol: float, shard=None):
+        """shard = (rank, world, exchange): fill only this process's leaves (LPT
+        partition); exchange=True broadcasts the shards over the context's NCCL
+        communicator (dist.init_nccl) so every rank holds the complete H-matrix."""
         self.gen = gen                     # keeps the device context alive
         self.dev = gen.dev
         self.C = gen.C
         self.N = gen.n_dofs
         self.eta = eta
         self.aca_tol = aca_tol
+        self.shard = shard
         h = ct.c_void_p()
-        self.dev.check(self.dev.lib.cbie_hmatrix_build(self.dev.h, int(n_leaf), float(eta),
-                                                       float(aca_tol), ct.byref(h)))
+        if shard is None:
+            self.dev.check(self.dev.lib.cbie_hmatrix_build(self.dev.h, int(n_leaf), float(eta),
+                                                           float(aca_tol), ct.byref(h)))
+        else:
+            rank, world, exchange = shard
+            self.dev.check(self.dev.lib.cbie_hmatrix_build_shard(
+                self.dev.h, int(n_leaf), float(eta), float(aca_tol), int(rank), int(world),
+                int(bool(exchange)), ct.byref(h)))
         self.h = h
         self._stats = _ffi.stats(h, 1)
 
@@ -51,13 +61,16 @@ class HMatrix:
         return self.tree()[0]
 
     def leaf(self, i: int):
-        """('dense', D) or ('lowrank', U, V) in permuted local order."""
+        """('dense', D) or ('lowrank', U, V) in permuted local order; ('remote',) for a
+        leaf another shard filled (partial H-matrix before the exchange)."""
         perm, lv = self.tree()
         m = int(lv[i, 1] - lv[i, 0]) * self.C
         n = int(lv[i, 3] - lv[i, 2]) * self.C
         kind, rank = ct.c_int(), ct.c_int()
         self.dev.check(self.dev.lib.cbie_hmatrix_leaf(self.h, int(i), ct.byref(kind),
                                                       ct.byref(rank), None, None))
+        if kind.value < 0:
+            return ("remote",)
         if kind.value == 0:
             D = np.empty((m, n), complex)
             self.dev.check(self.dev.lib.cbie_hmatrix_leaf(self.h, int(i), ct.byref(kind),

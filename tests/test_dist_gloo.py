@@ -1,5 +1,7 @@
-"""Multi-process (world_size 2, gloo) checks of the N > 1 bench plumbing on CPU:
-max-over-ranks timing and whole-job throughput aggregation."""
+"""Multi-process (world_size 2, gloo) checks of the N > 1 host logic on CPU:
+max-over-ranks timing, whole-job throughput aggregation, and the leaf-sharded
+fill's ownership (cbie_partition_lpt, shard.cu) plus its owner-major exchange plan
+(every owner broadcasts one contiguous range; all ranks end with every leaf)."""
 
 import os
 import socket
@@ -46,3 +48,80 @@ def test_two_rank_max_reduction():
     # whole-job value = ranks * N / max time
     N = 12288
     assert 2 * N / (150.0 / 1e3) == pytest.approx(163840.0)
+
+
+def _leaf_costs(seed=5, n_dense=1272, n_lr=2008):
+    """Config-2-like leaf population: 192^2 dense leaves, 192^2 / 384^2 admissible ones
+    (the cost model of shard.cu: m n for dense, 3 min(budget, 24) (m + n) otherwise)."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    m = rng.choice([192, 384], size=n_lr, p=[0.8, 0.2])
+    cost = np.concatenate([np.full(n_dense, 192.0 * 192.0), 3.0 * np.minimum(m // 2, 24) * (2.0 * m)])
+    return cost[rng.permutation(cost.size)]
+
+
+def _shard_worker(rank, world, port, q):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2408_17116_b200 import dist as cdist
+    cost = _leaf_costs()
+    owner = cdist.partition_lpt(cost, world)          # computed independently per rank
+    allo = [torch.zeros(cost.size, dtype=torch.int32) for _ in range(world)]
+    dist.all_gather(allo, torch.from_numpy(owner.astype(np.int32)))
+    same = all(torch.equal(allo[0], a) for a in allo)
+    # owner-major exchange plan: leaf data (here: its index repeated by size) packed in
+    # owner order, each owner broadcasts its contiguous range
+    size = (cost / cost.min()).round().astype(np.int64)
+    order = np.concatenate([np.flatnonzero(owner == o) for o in range(world)])
+    off = np.zeros(cost.size, np.int64)
+    off[order] = np.concatenate([[0], np.cumsum(size[order])[:-1]])
+    arena = torch.full((int(size.sum()),), -1.0, dtype=torch.float64)
+    for li in np.flatnonzero(owner == rank):
+        arena[off[li]:off[li] + size[li]] = float(li)
+    lo = [int(off[owner == o].min()) for o in range(world)]
+    hi = [int((off + size)[owner == o].max()) for o in range(world)]
+    for o in range(world):
+        seg = arena[lo[o]:hi[o]].clone()
+        dist.broadcast(seg, src=o)
+        arena[lo[o]:hi[o]] = seg
+    expect = np.repeat(np.arange(cost.size)[order], size[order]).astype(np.float64)
+    ok = bool(np.array_equal(arena.numpy(), expect))
+    loads = [float(cost[owner == o].sum()) for o in range(world)]
+    contiguous = all(hi[o] - lo[o] == int(size[owner == o].sum()) for o in range(world))
+    q.put((rank, same, ok, loads, contiguous))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_leaf_sharding_and_exchange_plan():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_shard_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = sorted(q.get(timeout=180) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    cost = _leaf_costs()
+    for rank, same, ok, loads, contiguous in out:
+        assert same and ok and contiguous
+        # LPT bound: max load <= mean + largest item
+        assert max(loads) <= sum(loads) / 2 + cost.max()
+        assert max(loads) / min(loads) < 1.01
+
+
+def test_lpt_partition_covers_every_leaf_once():
+    import numpy as np
+    from paper_2408_17116_b200 import dist as cdist
+    cost = _leaf_costs()
+    for world in (1, 2, 4, 8):
+        owner = cdist.partition_lpt(cost, world)
+        assert owner.min() >= 0 and owner.max() < world
+        loads = np.bincount(owner, weights=cost, minlength=world)
+        assert loads.max() <= cost.sum() / world + cost.max()
+        assert np.array_equal(owner, cdist.partition_lpt(cost, world))   # deterministic
