@@ -16,6 +16,8 @@
 #include <map>
 
 #include "hlu_kernels.cuh"
+#include <array>
+
 #include "hmatrix.h"
 
 std::string stats_to_json(const std::map<std::string, double>& m);
@@ -112,8 +114,15 @@ struct Recorder {
     Access a;
     int level;
     bool w;
+    int kind;   // op kind of the access, -1: collapsed (see floor_)
   };
   std::vector<std::vector<Entry>> ent;
+  // per buffer: latest level per op kind among the accesses folded into its
+  // collapsed entries; a task conflicting with a collapsed entry depends on all of them
+  std::vector<std::array<int, 8>> floor_w, floor_r;   // writes / reads folded
+  // per launch group (level, kind): latest level of every kind it depends on (the
+  // executor runs each kind on its own stream, so one event per kind suffices)
+  std::map<std::pair<int, int>, std::array<int, 8>> gdep;
   std::vector<int> last_w, max_r;   // (kept for the whole-buffer fast path)
   // tapes
   std::vector<GemmD> gemm;
@@ -134,7 +143,24 @@ struct Recorder {
     last_w.push_back(0);
     max_r.push_back(0);
     ent.emplace_back();
+    std::array<int, 8> f;
+    f.fill(-1);
+    floor_w.push_back(f);
+    floor_r.push_back(f);
     return nbuf++;
+  }
+  // fold the per-kind levels of the entries about to be collapsed; as_write: the
+  // collapsed result is a single write (chunk reuse), so reads fold into floor_w too
+  void fold(int buf, bool as_write) {
+    for (auto& e : ent[buf]) {
+      if (e.kind < 0) {
+        if (as_write && !e.w)
+          for (int q = 0; q < 8; ++q) floor_w[buf][q] = std::max(floor_w[buf][q], floor_r[buf][q]);
+        continue;
+      }
+      auto& f = (e.w || as_write) ? floor_w[buf] : floor_r[buf];
+      f[e.kind] = std::max(f[e.kind], e.level);
+    }
   }
   static Access whole(int buf) { return Access{buf, -1, 0, 1 << 30, 0, 1 << 30}; }
   static Access acc(const Mat& m) { return Access{m.buf, m.rid, m.nr0, m.nr1, m.nc0, m.nc1}; }
@@ -147,34 +173,57 @@ struct Recorder {
   void collapse(int buf) {   // forget rectangles: whole-buffer write / read at the max levels
     int mw = 0, mr = 0;
     for (auto& e : ent[buf]) (e.w ? mw : mr) = std::max(e.w ? mw : mr, e.level);
+    fold(buf, false);
     ent[buf].clear();
-    ent[buf].push_back(Entry{whole(buf), mw, true});
-    if (mr > 0) ent[buf].push_back(Entry{whole(buf), mr, false});
+    ent[buf].push_back(Entry{whole(buf), mw, true, -1});
+    if (mr > 0) ent[buf].push_back(Entry{whole(buf), mr, false, -1});
   }
   void collapse_reuse(int buf) {   // chunk handed to a new owner: all history is a write
     int mx = 0;
     for (auto& e : ent[buf]) mx = std::max(mx, e.level);
+    fold(buf, true);
     ent[buf].clear();
-    ent[buf].push_back(Entry{whole(buf), mx, true});
+    ent[buf].push_back(Entry{whole(buf), mx, true, -1});
   }
   void addA(int kind, int idx, const std::vector<Access>& rd, const std::vector<Access>& wr) {
     int lvl = 0;
+    int dk[8];
+    for (int q = 0; q < 8; ++q) dk[q] = -1;
+    auto dep = [&](const Entry& e, int buf) {
+      lvl = std::max(lvl, e.level);
+      if (e.kind >= 0) {
+        dk[e.kind] = std::max(dk[e.kind], e.level);
+      } else {   // collapsed entry: every folded access of its own type
+        const auto& f = e.w ? floor_w[buf] : floor_r[buf];
+        for (int q = 0; q < 8; ++q) dk[q] = std::max(dk[q], f[q]);
+      }
+    };
     for (const Access& r : rd) {
       if (r.buf < 0) continue;
       for (const Entry& e : ent[r.buf])
-        if (e.w && conflict(e.a, r)) lvl = std::max(lvl, e.level);
+        if (e.w && conflict(e.a, r)) dep(e, r.buf);
     }
     for (const Access& w : wr) {
       if (w.buf < 0) continue;
       for (const Entry& e : ent[w.buf])
-        if (conflict(e.a, w)) lvl = std::max(lvl, e.level);
+        if (conflict(e.a, w)) dep(e, w.buf);
     }
     ++lvl;
     if (serial) lvl = (int)tasks.size() + 1;
+    {
+      auto it = gdep.find({lvl, kind});
+      if (it == gdep.end()) {
+        std::array<int, 8> a;
+        for (int q = 0; q < 8; ++q) a[q] = dk[q];
+        gdep.emplace(std::make_pair(lvl, kind), a);
+      } else {
+        for (int q = 0; q < 8; ++q) it->second[q] = std::max(it->second[q], dk[q]);
+      }
+    }
     for (const Access& r : rd)
-      if (r.buf >= 0) ent[r.buf].push_back(Entry{r, lvl, false});
+      if (r.buf >= 0) ent[r.buf].push_back(Entry{r, lvl, false, kind});
     for (const Access& w : wr)
-      if (w.buf >= 0) ent[w.buf].push_back(Entry{w, lvl, true});
+      if (w.buf >= 0) ent[w.buf].push_back(Entry{w, lvl, true, kind});
     for (const Access& w : wr)
       if (w.buf >= 0 && ent[w.buf].size() > 24) collapse(w.buf);
     for (const Access& r : rd)
@@ -999,6 +1048,7 @@ struct Grp {
   int kind, start, count, level, kmax;
   int split = 0;       // OP_TRUNC: descriptors [start, start + split) form the first part
   bool gram = false;   // OP_TRUNC: the first part runs the Gram path
+  std::vector<int> deps;   // groups of OTHER kinds this group waits for (multi-stream executor)
 };
 
 // A recorded tape turned into launch groups with device-resident descriptors.
@@ -1080,6 +1130,30 @@ void make_plan(Plan& P, cudaStream_t s) {
     groups.push_back(gr);
     i = j;
   }
+  // exact cross-kind dependencies (Recorder::gdep): the latest group of every other
+  // kind this group's tasks depend on
+  {
+    std::map<std::pair<int, int>, int> gid;
+    for (size_t i = 0; i < groups.size(); ++i) gid[{groups[i].level, groups[i].kind}] = (int)i;
+    for (auto& gr : groups) {
+      auto it = R.gdep.find({gr.level, gr.kind});
+      if (it == R.gdep.end()) continue;
+      for (int q = 0; q < OP_NKIND; ++q) {
+        const int L = it->second[q];
+        if (q == gr.kind || L < 0) continue;
+        if (L >= gr.level) throw cbie_error(CBIE_EINVALID, "H-LU schedule: dependency not earlier than its task");
+        auto jt = gid.find({L, q});
+        if (jt != gid.end()) gr.deps.push_back(jt->second);
+        else if (getenv("CBIE_DEP_DUMP")) fprintf(stderr, "missing group (%d,%d)\n", L, q);
+      }
+    }
+    if (getenv("CBIE_DEP_DUMP"))
+      for (size_t i = 0; i < groups.size() && i < 60; ++i) {
+        fprintf(stderr, "G%zu L%d K%d n=%d deps:", i, groups[i].level, groups[i].kind, groups[i].count);
+        for (int d : groups[i].deps) fprintf(stderr, " (%d,%d)", groups[d].level, groups[d].kind);
+        fprintf(stderr, "\n");
+      }
+  }
   P.ddl.upload(dl, s);
   P.dg.upload(g, s);
   P.de.upload(e, s);
@@ -1097,8 +1171,9 @@ void make_plan(Plan& P, cudaStream_t s) {
 }
 
 Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag,
-              unsigned long long* ovf, TruncWork* tw, double tol, cudaStream_t s) {
+              unsigned long long* ovf, TruncWork* tw, double tol, cudaStream_t s0) {
   Exec ex;
+  cudaStream_t s = s0;
   // second stream for the large-block half of split recompression groups
   cudaStream_t s2 = nullptr;
   cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
@@ -1144,7 +1219,37 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
     cudaEventCreate(&e1);
   }
   std::vector<cudaEvent_t> tev;   // (start, stop) pairs around every truncation launch
-  for (auto& gr : P.groups) {
+  // multi-stream executor: one stream per op kind (groups of a kind stay in order on
+  // it), cross-kind dependencies through one event per group (Grp::deps) instead of
+  // level barriers; CBIE_PROFILE / CBIE_LEVEL_SYNC keep the single-stream order
+  const bool ms = !prof && getenv("CBIE_LEVEL_SYNC") == nullptr;
+  cudaStream_t ks[OP_NKIND] = {};
+  std::vector<cudaEvent_t> gev;
+  if (ms) {
+    cudaEvent_t st0;
+    CK(cudaEventCreateWithFlags(&st0, cudaEventDisableTiming));
+    CK(cudaEventRecord(st0, s0));
+    // debug: CBIE_MS_MASK = bit mask of the kinds with their own stream (others share one)
+    const int mask = getenv("CBIE_MS_MASK") ? atoi(getenv("CBIE_MS_MASK")) : 0x7f;
+    int shared_q = -1;
+    for (int q = 0; q < OP_NKIND; ++q) {
+      if (!(mask >> q & 1) && shared_q >= 0) {
+        ks[q] = ks[shared_q];
+        continue;
+      }
+      CK(cudaStreamCreateWithFlags(&ks[q], cudaStreamNonBlocking));
+      CK(cudaStreamWaitEvent(ks[q], st0, 0));
+      if (!(mask >> q & 1)) shared_q = q;
+    }
+    cudaEventDestroy(st0);
+    gev.resize(P.groups.size());
+    for (auto& e : gev) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
+  for (size_t gi = 0; gi < P.groups.size(); ++gi) {
+    auto& gr = P.groups[gi];
+    cudaStream_t s = ms ? ks[gr.kind] : s0;
+    if (ms)
+      for (int d : gr.deps) CK(cudaStreamWaitEvent(s, gev[d], 0));
     if (gr.level != lvl) {
       ++ex.levels;
       lvl = gr.level;
@@ -1263,6 +1368,7 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
       }
     }
     CKL();
+    if (ms) CK(cudaEventRecord(gev[gi], s));
     if (prof) {
       cudaEventRecord(e1, s);
       cudaEventSynchronize(e1);
@@ -1293,6 +1399,15 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   }
+  if (ms) {
+    for (int q = 0; q < OP_NKIND; ++q) {
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CK(cudaEventRecord(e, ks[q]));
+      CK(cudaStreamWaitEvent(s0, e, 0));
+      cudaEventDestroy(e);
+    }
+  }
   if (s3) {
     CK(cudaEventRecord(rc_ev, s3));
     CK(cudaStreamWaitEvent(s, rc_ev, 0));
@@ -1305,6 +1420,12 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
   cudaEventDestroy(fork_ev);
   cudaEventDestroy(join_ev);
   cudaStreamDestroy(s2);
+  for (auto& e : gev) cudaEventDestroy(e);
+  for (int q = 0; q < OP_NKIND; ++q) {
+    bool dup = false;
+    for (int p = 0; p < q; ++p) dup |= ks[p] == ks[q];
+    if (ks[q] && !dup) cudaStreamDestroy(ks[q]);
+  }
   for (size_t i = 0; i + 1 < tev.size(); i += 2) {
     float ms = 0;
     cudaEventElapsedTime(&ms, tev[i], tev[i + 1]);
