@@ -92,6 +92,18 @@ struct LR {
 };
 
 enum OpKind { OP_GEMM, OP_EW, OP_CONCAT, OP_TRSM, OP_GETRF, OP_TRUNC, OP_DLR, OP_NKIND };
+// executor streams ("virtual kinds"): one per op kind, the recompressions on
+// TRUNC_LANES streams (lane = level % TRUNC_LANES, each with its own workspaces) so
+// independent recompression groups of different levels overlap
+constexpr int TRUNC_LANES = 3;
+constexpr int NVK = 16;
+static_assert(OP_NKIND + TRUNC_LANES - 1 <= NVK, "virtual kinds");
+inline int vkind(int kind, int level) {
+  if (kind != OP_TRUNC) return kind;
+  const int lane = level % TRUNC_LANES;
+  return lane == 0 ? OP_TRUNC : OP_NKIND + lane - 1;
+}
+inline int trunc_lane(int level) { return level % TRUNC_LANES; }
 
 struct Task {
   int kind, idx, level;
@@ -114,15 +126,15 @@ struct Recorder {
     Access a;
     int level;
     bool w;
-    int kind;   // op kind of the access, -1: collapsed (see floor_)
+    int kind;   // virtual kind (executor stream) of the access, -1: collapsed (see floor_w / floor_r)
   };
   std::vector<std::vector<Entry>> ent;
   // per buffer: latest level per op kind among the accesses folded into its
   // collapsed entries; a task conflicting with a collapsed entry depends on all of them
-  std::vector<std::array<int, 8>> floor_w, floor_r;   // writes / reads folded
+  std::vector<std::array<int, NVK>> floor_w, floor_r;   // writes / reads folded
   // per launch group (level, kind): latest level of every kind it depends on (the
   // executor runs each kind on its own stream, so one event per kind suffices)
-  std::map<std::pair<int, int>, std::array<int, 8>> gdep;
+  std::map<std::pair<int, int>, std::array<int, NVK>> gdep;
   std::vector<int> last_w, max_r;   // (kept for the whole-buffer fast path)
   // tapes
   std::vector<GemmD> gemm;
@@ -143,7 +155,7 @@ struct Recorder {
     last_w.push_back(0);
     max_r.push_back(0);
     ent.emplace_back();
-    std::array<int, 8> f;
+    std::array<int, NVK> f;
     f.fill(-1);
     floor_w.push_back(f);
     floor_r.push_back(f);
@@ -155,7 +167,7 @@ struct Recorder {
     for (auto& e : ent[buf]) {
       if (e.kind < 0) {
         if (as_write && !e.w)
-          for (int q = 0; q < 8; ++q) floor_w[buf][q] = std::max(floor_w[buf][q], floor_r[buf][q]);
+          for (int q = 0; q < NVK; ++q) floor_w[buf][q] = std::max(floor_w[buf][q], floor_r[buf][q]);
         continue;
       }
       auto& f = (e.w || as_write) ? floor_w[buf] : floor_r[buf];
@@ -187,15 +199,15 @@ struct Recorder {
   }
   void addA(int kind, int idx, const std::vector<Access>& rd, const std::vector<Access>& wr) {
     int lvl = 0;
-    int dk[8];
-    for (int q = 0; q < 8; ++q) dk[q] = -1;
+    int dk[NVK];
+    for (int q = 0; q < NVK; ++q) dk[q] = -1;
     auto dep = [&](const Entry& e, int buf) {
       lvl = std::max(lvl, e.level);
       if (e.kind >= 0) {
         dk[e.kind] = std::max(dk[e.kind], e.level);
       } else {   // collapsed entry: every folded access of its own type
         const auto& f = e.w ? floor_w[buf] : floor_r[buf];
-        for (int q = 0; q < 8; ++q) dk[q] = std::max(dk[q], f[q]);
+        for (int q = 0; q < NVK; ++q) dk[q] = std::max(dk[q], f[q]);
       }
     };
     for (const Access& r : rd) {
@@ -210,20 +222,21 @@ struct Recorder {
     }
     ++lvl;
     if (serial) lvl = (int)tasks.size() + 1;
+    const int vk = vkind(kind, lvl);
     {
-      auto it = gdep.find({lvl, kind});
+      auto it = gdep.find({lvl, vk});
       if (it == gdep.end()) {
-        std::array<int, 8> a;
-        for (int q = 0; q < 8; ++q) a[q] = dk[q];
-        gdep.emplace(std::make_pair(lvl, kind), a);
+        std::array<int, NVK> a;
+        for (int q = 0; q < NVK; ++q) a[q] = dk[q];
+        gdep.emplace(std::make_pair(lvl, vk), a);
       } else {
-        for (int q = 0; q < 8; ++q) it->second[q] = std::max(it->second[q], dk[q]);
+        for (int q = 0; q < NVK; ++q) it->second[q] = std::max(it->second[q], dk[q]);
       }
     }
     for (const Access& r : rd)
-      if (r.buf >= 0) ent[r.buf].push_back(Entry{r, lvl, false, kind});
+      if (r.buf >= 0) ent[r.buf].push_back(Entry{r, lvl, false, vk});
     for (const Access& w : wr)
-      if (w.buf >= 0) ent[w.buf].push_back(Entry{w, lvl, true, kind});
+      if (w.buf >= 0) ent[w.buf].push_back(Entry{w, lvl, true, vk});
     for (const Access& w : wr)
       if (w.buf >= 0 && ent[w.buf].size() > 24) collapse(w.buf);
     for (const Access& r : rd)
@@ -1134,13 +1147,14 @@ void make_plan(Plan& P, cudaStream_t s) {
   // kind this group's tasks depend on
   {
     std::map<std::pair<int, int>, int> gid;
-    for (size_t i = 0; i < groups.size(); ++i) gid[{groups[i].level, groups[i].kind}] = (int)i;
+    for (size_t i = 0; i < groups.size(); ++i) gid[{groups[i].level, vkind(groups[i].kind, groups[i].level)}] = (int)i;
     for (auto& gr : groups) {
-      auto it = R.gdep.find({gr.level, gr.kind});
+      const int gvk = vkind(gr.kind, gr.level);
+      auto it = R.gdep.find({gr.level, gvk});
       if (it == R.gdep.end()) continue;
-      for (int q = 0; q < OP_NKIND; ++q) {
+      for (int q = 0; q < NVK; ++q) {
         const int L = it->second[q];
-        if (q == gr.kind || L < 0) continue;
+        if (q == gvk || L < 0) continue;
         if (L >= gr.level) throw cbie_error(CBIE_EINVALID, "H-LU schedule: dependency not earlier than its task");
         auto jt = gid.find({L, q});
         if (jt != gid.end()) gr.deps.push_back(jt->second);
@@ -1174,12 +1188,16 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
               unsigned long long* ovf, TruncWork* tw, double tol, cudaStream_t s0) {
   Exec ex;
   cudaStream_t s = s0;
-  // second stream for the large-block half of split recompression groups
-  cudaStream_t s2 = nullptr;
-  cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
-  CK(cudaStreamCreateWithFlags(&s2, cudaStreamNonBlocking));
-  CK(cudaEventCreateWithFlags(&fork_ev, cudaEventDisableTiming));
-  CK(cudaEventCreateWithFlags(&join_ev, cudaEventDisableTiming));
+  // per recompression lane: second stream (dense-mode / Householder share of a group),
+  // fork / join events, two workspaces (twl[2 lane], twl[2 lane + 1])
+  TruncWork* twl = tw;
+  cudaStream_t s2l[TRUNC_LANES] = {};
+  cudaEvent_t fork_l[TRUNC_LANES] = {}, join_l[TRUNC_LANES] = {};
+  for (int l = 0; l < TRUNC_LANES; ++l) {
+    CK(cudaStreamCreateWithFlags(&s2l[l], cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&fork_l[l], cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&join_l[l], cudaEventDisableTiming));
+  }
   const auto& g = P.g;
   const auto& t = P.t;
   const auto& tr = P.tr;
@@ -1223,16 +1241,16 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
   // it), cross-kind dependencies through one event per group (Grp::deps) instead of
   // level barriers; CBIE_PROFILE / CBIE_LEVEL_SYNC keep the single-stream order
   const bool ms = !prof && getenv("CBIE_LEVEL_SYNC") == nullptr;
-  cudaStream_t ks[OP_NKIND] = {};
+  cudaStream_t ks[NVK] = {};
   std::vector<cudaEvent_t> gev;
   if (ms) {
     cudaEvent_t st0;
     CK(cudaEventCreateWithFlags(&st0, cudaEventDisableTiming));
     CK(cudaEventRecord(st0, s0));
     // debug: CBIE_MS_MASK = bit mask of the kinds with their own stream (others share one)
-    const int mask = getenv("CBIE_MS_MASK") ? atoi(getenv("CBIE_MS_MASK")) : 0x7f;
+    const int mask = getenv("CBIE_MS_MASK") ? atoi(getenv("CBIE_MS_MASK")) : 0xffff;
     int shared_q = -1;
-    for (int q = 0; q < OP_NKIND; ++q) {
+    for (int q = 0; q < NVK; ++q) {
       if (!(mask >> q & 1) && shared_q >= 0) {
         ks[q] = ks[shared_q];
         continue;
@@ -1247,7 +1265,11 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
   }
   for (size_t gi = 0; gi < P.groups.size(); ++gi) {
     auto& gr = P.groups[gi];
-    cudaStream_t s = ms ? ks[gr.kind] : s0;
+    cudaStream_t s = ms ? ks[vkind(gr.kind, gr.level)] : s0;
+    const int lane = ms ? trunc_lane(gr.level) : 0;
+    cudaStream_t s2 = s2l[lane];
+    cudaEvent_t fork_ev = fork_l[lane], join_ev = join_l[lane];
+    TruncWork* tw = twl + 2 * lane;
     if (ms)
       for (int d : gr.deps) CK(cudaStreamWaitEvent(s, gev[d], 0));
     if (gr.level != lvl) {
@@ -1400,7 +1422,8 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
     cudaEventDestroy(e1);
   }
   if (ms) {
-    for (int q = 0; q < OP_NKIND; ++q) {
+    for (int q = 0; q < NVK; ++q) {
+      if (!ks[q]) continue;
       cudaEvent_t e;
       CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       CK(cudaEventRecord(e, ks[q]));
@@ -1417,11 +1440,13 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
     cudaEventDestroy(rc_ev);
     cudaStreamDestroy(s3);
   }
-  cudaEventDestroy(fork_ev);
-  cudaEventDestroy(join_ev);
-  cudaStreamDestroy(s2);
+  for (int l = 0; l < TRUNC_LANES; ++l) {
+    cudaEventDestroy(fork_l[l]);
+    cudaEventDestroy(join_l[l]);
+    cudaStreamDestroy(s2l[l]);
+  }
   for (auto& e : gev) cudaEventDestroy(e);
-  for (int q = 0; q < OP_NKIND; ++q) {
+  for (int q = 0; q < NVK; ++q) {
     bool dup = false;
     for (int p = 0; p < q; ++p) dup |= ks[p] == ks[q];
     if (ks[q] && !dup) cudaStreamDestroy(ks[q]);
@@ -1453,7 +1478,7 @@ struct PlanCache {
   uint64_t key = 0;
   Plan plan;
   DBuf<zc> work;
-  TruncWork tw[2];   // recompression workspaces of the two streams
+  TruncWork tw[2 * TRUNC_LANES];   // recompression workspaces (two per lane)
   int64_t leaf_end = 0;
 };
 std::unique_ptr<PlanCache> g_plan_cache;
@@ -1477,8 +1502,7 @@ void hlu_trim_cache(bool force) {
   // keep the plan (small); release the workspace only when HBM runs short
   if (force || (double)fr < 0.25 * (double)tot) {
     g_plan_cache->work.release();
-    g_plan_cache->tw[0].release();
-    g_plan_cache->tw[1].release();
+    for (auto& w : g_plan_cache->tw) w.release();
   }
 }
 
@@ -1737,7 +1761,7 @@ static void hlu_solve_impl(cbie_hlu* F, const zc* b, zc* x, int nrhs) {
   rc.alloc(1);
   DBuf<unsigned long long> ovf;
   ovf.alloc(1);
-  TruncWork tw[2];
+  TruncWork tw[2 * TRUNC_LANES];
   execute(R, F->arena.p, ranks.p, F->piv.p, rc.p, flag.p, ovf.p, tw, F->tol, s);
   CK(cudaMemcpy(bp.data(), F->arena.p + X.off, sizeof(zc) * bp.size(), cudaMemcpyDeviceToHost));
   for (size_t p = 0; p < T.pperm.size(); ++p)
