@@ -48,6 +48,9 @@ __device__ __forceinline__ double bsum(double v, double* red) {
   for (int i = 0; i < NW; ++i) t += red[i];
   return t;
 }
+__device__ __forceinline__ zc zshfl(zc v, int src) {
+  return zmk(__shfl_sync(FULL, v.x, src), __shfl_sync(FULL, v.y, src));
+}
 __device__ __forceinline__ double warp_max(double v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(FULL, v, o));
@@ -629,50 +632,62 @@ constexpr double CHOL_EPS = 1e-13;  // pivoted-Cholesky stop (squared, relative)
 
 __host__ __device__ inline int64_t gram_scratch_per() { return 4 * (int64_t)GSQ + 64; }
 
-// G (k x k, ld k, shared, zeroed) += X^H X, X (m x k) col-major ld ldx in global memory
+// G (k x k, ld k, shared, zeroed) += X^H X, X (m x k) col-major ld ldx in global memory.
+// Hermitian: only the 4 x 4 tiles on and above the block diagonal are accumulated
+// (conjugate-FMA, 4 DFMA per complex term), the lower part is mirrored; thread groups
+// split the rows; the next 64-row chunk is loaded into registers while the current
+// one is consumed from shared memory.
 __device__ void gram_acc(const zc* __restrict__ X, int m, int k, int ldx, zc* G, zc* Xs) {
-  const int ta = (k + 3) / 4, tb = (k + 1) / 2, ntile = ta * tb;
+  constexpr int PER = GCH * KG / NT;   // staged elements per thread
+  const int tb = (k + 3) / 4, ntile = tb * (tb + 1) / 2;
   const int groups = max(1, NT / ntile);
   const int g = threadIdx.x / ntile, t = threadIdx.x % ntile;
   const bool act = g < groups;
-  const int a0 = 4 * (t % ta), b0 = 2 * (t / ta);
-  zc acc[4][2];
+  int tj = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+  while ((tj + 1) * (tj + 2) / 2 <= t) ++tj;
+  while (tj * (tj + 1) / 2 > t) --tj;
+  const int ti = t - tj * (tj + 1) / 2;
+  const int a0 = 4 * ti, b0 = 4 * tj;
+  double ar[4][4], ai[4][4];
 #pragma unroll
   for (int qa = 0; qa < 4; ++qa)
 #pragma unroll
-    for (int qb = 0; qb < 2; ++qb) acc[qa][qb] = zmk(0.0, 0.0);
+    for (int qb = 0; qb < 4; ++qb) ar[qa][qb] = ai[qa][qb] = 0.0;
+  zc v[PER];
+  auto fetch = [&](int r0) {
+    const int rows = min(GCH, m - r0);
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const int e = threadIdx.x + u * NT;
+      v[u] = (r0 < m && e < rows * k) ? X[(int64_t)(e / rows) * ldx + r0 + e % rows] : zmk(0.0, 0.0);
+    }
+  };
+  fetch(0);
   for (int r0 = 0; r0 < m; r0 += GCH) {
     const int rows = min(GCH, m - r0);
     __syncthreads();
-    {
-      zc v[GCH * KG / NT];
 #pragma unroll
-      for (int u = 0; u < GCH * KG / NT; ++u) {
-        const int e = threadIdx.x + u * NT;
-        v[u] = e < rows * k ? X[(int64_t)(e / rows) * ldx + r0 + e % rows] : zmk(0.0, 0.0);
-      }
-#pragma unroll
-      for (int u = 0; u < GCH * KG / NT; ++u) {
-        const int e = threadIdx.x + u * NT;
-        if (e < rows * k) Xs[(e % rows) * GLD + e / rows] = v[u];
-      }
+    for (int u = 0; u < PER; ++u) {
+      const int e = threadIdx.x + u * NT;
+      if (e < rows * k) Xs[(e % rows) * GLD + e / rows] = v[u];
     }
     __syncthreads();
+    fetch(r0 + GCH);
     if (act) {
       for (int i = g; i < rows; i += groups) {
         const zc* xr = Xs + i * GLD;
-        zc xa[4], xb[2];
+        zc xa[4], xb[4];
 #pragma unroll
-        for (int q = 0; q < 4; ++q) xa[q] = a0 + q < k ? xr[a0 + q] : zmk(0.0, 0.0);
-#pragma unroll
-        for (int q = 0; q < 2; ++q) xb[q] = b0 + q < k ? xr[b0 + q] : zmk(0.0, 0.0);
+        for (int q = 0; q < 4; ++q) {
+          xa[q] = a0 + q < k ? xr[a0 + q] : zmk(0.0, 0.0);
+          xb[q] = b0 + q < k ? xr[b0 + q] : zmk(0.0, 0.0);
+        }
 #pragma unroll
         for (int qa = 0; qa < 4; ++qa)
 #pragma unroll
-          for (int qb = 0; qb < 2; ++qb) {
-            const zc p = zcmul(xa[qa], xb[qb]);
-            acc[qa][qb].x += p.x;
-            acc[qa][qb].y += p.y;
+          for (int qb = 0; qb < 4; ++qb) {   // conj(xa) xb
+            ar[qa][qb] = fma(xa[qa].x, xb[qb].x, fma(xa[qa].y, xb[qb].y, ar[qa][qb]));
+            ai[qa][qb] = fma(xa[qa].x, xb[qb].y, fma(-xa[qa].y, xb[qb].x, ai[qa][qb]));
           }
       }
     }
@@ -681,12 +696,18 @@ __device__ void gram_acc(const zc* __restrict__ X, int m, int k, int ldx, zc* G,
 #pragma unroll
     for (int qa = 0; qa < 4; ++qa)
 #pragma unroll
-      for (int qb = 0; qb < 2; ++qb)
-        if (a0 + qa < k && b0 + qb < k) {
-          double* gp = reinterpret_cast<double*>(G + (b0 + qb) * k + a0 + qa);
-          atomicAdd(gp, acc[qa][qb].x);
-          atomicAdd(gp + 1, acc[qa][qb].y);
+      for (int qb = 0; qb < 4; ++qb) {
+        const int a = a0 + qa, b = b0 + qb;
+        if (a >= k || b >= k || (ti == tj && a > b)) continue;
+        double* gp = reinterpret_cast<double*>(G + b * k + a);
+        atomicAdd(gp, ar[qa][qb]);
+        atomicAdd(gp + 1, ai[qa][qb]);
+        if (a != b) {   // mirror: G[b][a] = conj(G[a][b])
+          double* gq = reinterpret_cast<double*>(G + a * k + b);
+          atomicAdd(gq, ar[qa][qb]);
+          atomicAdd(gq + 1, -ai[qa][qb]);
         }
+      }
   __syncthreads();
 }
 
@@ -752,28 +773,39 @@ __device__ int pchol(zc* G, int k, int* perm, double thr_rel, Smem& S) {
     }
     __syncthreads();
     if (S.flag) break;
-    const int rem = k - j - 1;
-    for (int e = threadIdx.x; e < rem * rem; e += NT) {
-      const int a = j + 1 + e % rem, b = j + 1 + e / rem;
-      G[b * k + a] = zsub(G[b * k + a], zcmul(G[a * k + j], G[b * k + j]));
-    }
+    // trailing update on the lower triangle a >= b > j (Hermitian: mirrored below)
+    for (int b = j + 1 + (threadIdx.x >> 6); b < k; b += NT / 64)
+      for (int a = b + (threadIdx.x & 63); a < k; a += 64) {
+        const zc v = zsub(G[b * k + a], zcmul(G[a * k + j], G[b * k + j]));
+        G[b * k + a] = v;
+        if (a != b) G[a * k + b] = zconj(v);
+      }
     __syncthreads();
   }
   __syncthreads();
   return j;
 }
 
-// Z (kk x r, ld kk, shared) <- R11^{-1} Z with R11 = rows/cols 0..kk-1 of R (ld k), then
-// row j scaled by sc[j]; thread per column
+// Z (kk x r, ld kk, shared) <- R11^{-1} Z with R11 = rows/cols 0..kk-1 of R (ld k, upper),
+// then row j scaled by sc[j]; one warp per column, lanes hold rows lane, lane + 32
 __device__ void tri_solve_cols(const zc* R, int k, int kk, zc* Z, int r, const double* sc) {
-  for (int l = threadIdx.x; l < r; l += NT) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int l = w; l < r; l += NW) {
     zc* z = Z + (int64_t)l * kk;
+    zc x0 = lane < kk ? z[lane] : zmk(0.0, 0.0);
+    zc x1 = lane + 32 < kk ? z[lane + 32] : zmk(0.0, 0.0);
     for (int a = kk - 1; a >= 0; --a) {
-      zc s = z[a];
-      for (int j = a + 1; j < kk; ++j) s = zsub(s, zmul(R[j * k + a], z[j]));
-      z[a] = zscale(s, 1.0 / R[a * k + a].x);
+      const zc own = a >= 32 ? x1 : x0;
+      const zc xa = zscale(zshfl(own, a & 31), 1.0 / R[a * k + a].x);
+      if (lane == (a & 31)) {
+        if (a >= 32) x1 = xa;
+        else x0 = xa;
+      }
+      if (lane < a) x0 = zsub(x0, zmul(R[a * k + lane], xa));
+      if (lane + 32 < a) x1 = zsub(x1, zmul(R[a * k + lane + 32], xa));
     }
-    for (int a = 0; a < kk; ++a) z[a] = zscale(z[a], sc[a]);
+    if (lane < kk) z[lane] = zscale(x0, sc[lane]);
+    if (lane + 32 < kk) z[lane + 32] = zscale(x1, sc[lane + 32]);
   }
   __syncthreads();
 }
@@ -809,26 +841,11 @@ __device__ void apply_sel(const zc* __restrict__ X, int mo, int ldx, const int* 
 // rotation of pair (p, q) is the one of jacobi_nw for the 2 x 2 Gram [h_pp h_pq; . h_qq].
 // Returns the number of sweeps.
 __device__ int herm_jacobi(zc* H, int n, zc* X, Smem& S) {
-  __shared__ double rc[KG / 2];
-  __shared__ zc rs[KG / 2];
-  __shared__ int rp[KG / 2], rq[KG / 2];
+  __shared__ double rc[KG / 2 + 1];
+  __shared__ zc rs[KG / 2 + 1];
+  __shared__ int rp[KG / 2 + 1], rq[KG / 2 + 1];
   if (n < 2) return 0;
   const int ne = n + (n & 1), np = ne / 2;
-  constexpr int NB = 2 * KG * (KG / 2) / NT, NC = KG * (KG / 2) / NT;
-  int bi[NB], bt[NB], ci[NC], ct[NC];   // fixed (row, pair) items of this thread
-#pragma unroll
-  for (int u = 0; u < NB; ++u) {
-    const int e = threadIdx.x + u * NT;
-    const int f = e % (n * np);
-    bi[u] = e < 2 * n * np ? f % n : -1;
-    bt[u] = f / n + (e >= n * np ? KG : 0);   // + KG marks the X update
-  }
-#pragma unroll
-  for (int u = 0; u < NC; ++u) {
-    const int e = threadIdx.x + u * NT;
-    ci[u] = e < n * np ? e % n : -1;
-    ct[u] = e / n;
-  }
   double f2 = 0.0;
   for (int e = threadIdx.x; e < n * n; e += NT) f2 += zabs2(H[e]);
   f2 = bsum(f2, S.red);
@@ -840,6 +857,7 @@ __device__ int herm_jacobi(zc* H, int n, zc* X, Smem& S) {
     off = bsum(off, S.red);
     if (!(off > 1e-26 * f2)) break;
     for (int rd = 0; rd < ne - 1; ++rd) {
+      // rotation of every pair (round-robin ordering); an index >= n pairs with identity
       if (threadIdx.x < np) {
         const int t = threadIdx.x;
         const int pb = ne - 1 - t;
@@ -847,8 +865,7 @@ __device__ int herm_jacobi(zc* H, int n, zc* X, Smem& S) {
         const int q = pb == 0 ? 0 : ((pb - 1 + rd) % (ne - 1)) + 1;
         double cs = 1.0;
         zc se = zmk(0.0, 0.0);
-        const bool ok = p < n && q < n;
-        if (ok) {
+        if (p < n && q < n) {
           const double al = H[p * n + p].x, be = H[q * n + q].x;
           const zc gm = H[q * n + p];   // h_pq
           const double g = sqrt(zabs2(gm));
@@ -860,41 +877,44 @@ __device__ int herm_jacobi(zc* H, int n, zc* X, Smem& S) {
             se = zmk(gm.x * ig * sn, gm.y * ig * sn);
           }
         }
-        rp[t] = ok ? p : -1;
+        rp[t] = p;
         rq[t] = q;
         rc[t] = cs;
         rs[t] = se;
       }
       __syncthreads();
-      // columns: [h_p h_q] <- [h_p h_q] J, J = [cs se; -conj(se) cs]; same for X
-#pragma unroll
-      for (int u = 0; u < NB; ++u) {
-        if (bi[u] < 0) continue;
-        const int t = bt[u] & (KG - 1);
-        const int p = rp[t], q = rq[t];
-        if (p < 0) continue;
-        zc* A = bt[u] >= KG ? X : H;
-        const int i = bi[u];
-        const double cs = rc[t];
-        const zc se = rs[t];
-        const zc xi = A[p * n + i], yi = A[q * n + i];
-        A[p * n + i] = zsub(zscale(xi, cs), zmul(zconj(se), yi));
-        A[q * n + i] = zadd(zmul(se, xi), zscale(yi, cs));
-      }
-      __syncthreads();
-      // rows: H <- J^H H
-#pragma unroll
-      for (int u = 0; u < NC; ++u) {
-        if (ci[u] < 0) continue;
-        const int t = ct[u];
-        const int p = rp[t], q = rq[t];
-        if (p < 0) continue;
-        const int j = ci[u];
-        const double cs = rc[t];
-        const zc se = rs[t];
-        const zc xp = H[j * n + p], xq = H[j * n + q];
-        H[j * n + p] = zsub(zscale(xp, cs), zmul(se, xq));
-        H[j * n + q] = zadd(zmul(zconj(se), xp), zscale(xq, cs));
+      // H <- J^H H J by disjoint 2 x 2 blocks (rows of pair t1, columns of pair t2),
+      // X <- X J by (row, pair) items; no two items touch the same entry.
+      // J = [cs se; -conj(se) cs] acts on the (p, q) columns.
+      for (int e = threadIdx.x; e < np * np + n * np; e += NT) {
+        if (e < np * np) {
+          const int t1 = e % np, t2 = e / np;
+          const int a0 = rp[t1], a1 = rq[t1], b0 = rp[t2], b1 = rq[t2];
+          const bool va0 = a0 < n, va1 = a1 < n, vb0 = b0 < n, vb1 = b1 < n;
+          const double c1 = rc[t1], c2 = rc[t2];
+          const zc s1 = rs[t1], s2 = rs[t2];
+          const zc z0 = zmk(0.0, 0.0);
+          const zc hpp = va0 && vb0 ? H[b0 * n + a0] : z0, hpq = va0 && vb1 ? H[b1 * n + a0] : z0;
+          const zc hqp = va1 && vb0 ? H[b0 * n + a1] : z0, hqq = va1 && vb1 ? H[b1 * n + a1] : z0;
+          const zc cpp = zsub(zscale(hpp, c2), zmul(zconj(s2), hpq));
+          const zc cpq = zadd(zmul(s2, hpp), zscale(hpq, c2));
+          const zc cqp = zsub(zscale(hqp, c2), zmul(zconj(s2), hqq));
+          const zc cqq = zadd(zmul(s2, hqp), zscale(hqq, c2));
+          if (va0 && vb0) H[b0 * n + a0] = zsub(zscale(cpp, c1), zmul(s1, cqp));
+          if (va0 && vb1) H[b1 * n + a0] = zsub(zscale(cpq, c1), zmul(s1, cqq));
+          if (va1 && vb0) H[b0 * n + a1] = zadd(zmul(zconj(s1), cpp), zscale(cqp, c1));
+          if (va1 && vb1) H[b1 * n + a1] = zadd(zmul(zconj(s1), cpq), zscale(cqq, c1));
+        } else {
+          const int f = e - np * np;
+          const int i = f % n, t = f / n;
+          const int p = rp[t], q = rq[t];
+          if (p >= n || q >= n) continue;
+          const double cs = rc[t];
+          const zc se = rs[t];
+          const zc xi = X[p * n + i], yi = X[q * n + i];
+          X[p * n + i] = zsub(zscale(xi, cs), zmul(zconj(se), yi));
+          X[q * n + i] = zadd(zmul(se, xi), zscale(yi, cs));
+        }
       }
       __syncthreads();
     }
