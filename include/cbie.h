@@ -183,6 +183,22 @@ void cbie_dist_finalize(cbie_ctx* ctx);
 int cbie_hmatrix_build_shard(cbie_ctx* ctx, int n_leaf, double eta, double aca_tol, int rank,
                              int world, int exchange, cbie_hmat** out);
 
+/* Block-row-distributed H-LU (replaces the single-core recursion
+ * hlu_factor / _factor, hmatrix.py:827-858): every rank of the cbie_dist_init
+ * communicator records the same tape, runs the tasks of the block rows it owns
+ * (row clusters dealt cyclically at the first tree level with >= 2 world
+ * clusters) and exchanges the factored diagonal blocks / panels its peers read
+ * with ncclSend / ncclRecv between dependency levels; at the end every owner
+ * broadcasts its factored leaves, so every rank holds complete factors
+ * (cbie_hlu_solve / cbie_hlu_leaf as for cbie_hlu_factor).  Collective: every
+ * rank calls it with the same complete H-matrix. */
+int cbie_hlu_factor_dist(cbie_hmat* h, double trunc_tol, cbie_hlu** out);
+
+/* The same distributed plan executed by `world` virtual ranks inside this
+ * process on one GPU (one arena per virtual rank, device copies instead of
+ * NCCL) -- checks the ownership / transfer plan without several GPUs. */
+int cbie_hlu_factor_emulated(cbie_hmat* h, double trunc_tol, int world, cbie_hlu** out);
+
 /* Timings (CUDA events), counts, flops, bytes as one JSON object.
  * which: 0 = context, 1 = hmatrix, 2 = hlu. */
 int cbie_stats_json(const void* handle, int which, char* buf, size_t cap);

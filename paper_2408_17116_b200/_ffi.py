@@ -50,6 +50,8 @@ _SIGS = {
     "cbie_hmatvec": (ct.c_int, [P, P, P, ct.c_int]),
     "cbie_hlu_factor": (ct.c_int, [P, ct.c_double, ct.POINTER(P)]),
     "cbie_hlu_destroy": (None, [P]),
+    "cbie_hlu_factor_dist": (ct.c_int, [P, ct.c_double, ct.POINTER(P)]),
+    "cbie_hlu_factor_emulated": (ct.c_int, [P, ct.c_double, ct.c_int, ct.POINTER(P)]),
     "cbie_hlu_leaf": (ct.c_int, [P, ct.c_int64, ct.POINTER(ct.c_int), ct.POINTER(ct.c_int), P, P, P]),
     "cbie_hlu_solve": (ct.c_int, [P, P, P, ct.c_int]),
     "cbie_lowrank_truncate": (ct.c_int, [P, P, ct.c_int, ct.c_int, P, ct.c_int, ct.c_double,

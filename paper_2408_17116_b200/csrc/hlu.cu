@@ -17,6 +17,8 @@
 
 #include "hlu_kernels.cuh"
 #include <array>
+#include <tuple>
+#include <nccl.h>
 
 #include "hmatrix.h"
 
@@ -150,8 +152,18 @@ struct Recorder {
   double flops = 0.0;
   int64_t trunc_count = 0, gemm_count = 0, trsm_count = 0, getrf_count = 0;
   bool serial = getenv("CBIE_SERIAL") != nullptr;
+  // access log for the block-row-distributed H-LU (hlu_dist.cuh): per task the
+  // buffers it reads / writes, and the tape positions where a pooled chunk was
+  // handed to a new temporary (its previous contents are dead from there on)
+  bool track = false;
+  std::vector<int64_t> acc_start{0};
+  std::vector<int> acc_buf;          // >= 0: read, ~b: write of buffer b
+  std::vector<std::pair<int, int>> reuse_at;   // (task index, buffer)
+  std::vector<int64_t> buf_off, buf_len;       // temporaries: pool chunk of every buffer
 
   int new_buf() {
+    buf_off.push_back(-1);
+    buf_len.push_back(0);
     last_w.push_back(0);
     max_r.push_back(0);
     ent.emplace_back();
@@ -242,6 +254,13 @@ struct Recorder {
     for (const Access& r : rd)
       if (r.buf >= 0 && ent[r.buf].size() > 24) collapse(r.buf);
     tasks.push_back(Task{kind, idx, lvl});
+    if (track) {
+      for (const Access& r : rd)
+        if (r.buf >= 0) acc_buf.push_back(r.buf);
+      for (const Access& w : wr)
+        if (w.buf >= 0) acc_buf.push_back(~w.buf);
+      acc_start.push_back((int64_t)acc_buf.size());
+    }
   }
   void accs_of(const Mat& m, std::vector<Access>& v) const {
     v.push_back(acc(m));
@@ -316,9 +335,12 @@ struct Recorder {
       auto pr = fl.front();   // oldest freed chunk first
       fl.erase(fl.begin());
       collapse_reuse(pr.second);   // new owner: every earlier access conflicts
+      if (track) reuse_at.push_back({(int)tasks.size(), pr.second});
       return Tmp{pr.first, cls, pr.second};
     }
     Tmp t{leaf_end + pool_top, cls, new_buf()};
+    buf_off[t.buf] = t.off;
+    buf_len[t.buf] = sz;
     pool_top += sz;
     return t;
   }
@@ -487,6 +509,7 @@ struct cbie_hlu {
   DBuf<int> piv;
   DBuf<double> rcond;
   int64_t leaf_end = 0;
+  int64_t npiv = 0;
   int nslot_leaf = 0;
   std::map<std::string, double> stat;
 };
@@ -1087,9 +1110,17 @@ struct Plan {
   int maxn_lu = 0;   // largest diagonal leaf (getrf / trsm)
 };
 
-void make_plan(Plan& P, cudaStream_t s) {
-  Recorder& R = P.R;
-  std::vector<Task> ts = R.tasks;
+// owner != nullptr: only the tasks with owner[i] == me (block-row-distributed H-LU)
+void make_plan(Plan& P, cudaStream_t s, const Recorder* Rx = nullptr, const std::vector<int>* owner = nullptr,
+               int me = 0) {
+  const Recorder& R = Rx ? *Rx : P.R;
+  std::vector<Task> ts;
+  if (owner) {
+    for (size_t i = 0; i < R.tasks.size(); ++i)
+      if ((*owner)[i] == me) ts.push_back(R.tasks[i]);
+  } else {
+    ts = R.tasks;
+  }
   std::stable_sort(ts.begin(), ts.end(), [](const Task& a, const Task& b) {
     return a.level != b.level ? a.level < b.level : a.kind < b.kind;
   });
@@ -1184,9 +1215,13 @@ void make_plan(Plan& P, cudaStream_t s) {
   P.maxn_lu = std::max(maxn_trsm, maxn_getrf);
 }
 
+// lvl_lo / lvl_hi: run only the groups of these levels, level-synchronously on s0
+// (the distributed H-LU exchanges data between levels)
 Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag,
-              unsigned long long* ovf, TruncWork* tw, double tol, cudaStream_t s0) {
+              unsigned long long* ovf, TruncWork* tw, double tol, cudaStream_t s0, int lvl_lo = 0,
+              int lvl_hi = 1 << 30) {
   Exec ex;
+  const bool ranged = lvl_lo > 0 || lvl_hi < (1 << 30);
   cudaStream_t s = s0;
   // per recompression lane: second stream (dense-mode / Householder share of a group),
   // fork / join events, two workspaces (twl[2 lane], twl[2 lane + 1])
@@ -1240,7 +1275,7 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
   // multi-stream executor: one stream per op kind (groups of a kind stay in order on
   // it), cross-kind dependencies through one event per group (Grp::deps) instead of
   // level barriers; CBIE_PROFILE / CBIE_LEVEL_SYNC keep the single-stream order
-  const bool ms = !prof && getenv("CBIE_LEVEL_SYNC") == nullptr;
+  const bool ms = !prof && !ranged && getenv("CBIE_LEVEL_SYNC") == nullptr;
   cudaStream_t ks[NVK] = {};
   std::vector<cudaEvent_t> gev;
   if (ms) {
@@ -1265,6 +1300,7 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
   }
   for (size_t gi = 0; gi < P.groups.size(); ++gi) {
     auto& gr = P.groups[gi];
+    if (gr.level < lvl_lo || gr.level > lvl_hi) continue;
     cudaStream_t s = ms ? ks[vkind(gr.kind, gr.level)] : s0;
     const int lane = ms ? trunc_lane(gr.level) : 0;
     cudaStream_t s2 = s2l[lane];
@@ -1509,16 +1545,14 @@ void hlu_trim_cache(bool force) {
 // ---------------------------------------------------------------------------
 // factor / solve drivers
 // ---------------------------------------------------------------------------
-static void hlu_factor_impl(cbie_hlu* F) {
+// factor storage layout (F->tree offsets, F->pivoff) and the copy of the H-matrix leaves
+static int64_t hlu_layout(cbie_hlu* F, std::vector<CopySeg>& segs) {
   cbie_hmat* H = F->H;
-  cbie_ctx* c = H->ctx;
-  cudaStream_t s = c->stream;
   F->tree = H->tree;
   Tree& T = F->tree;
   const int nleaf = (int)T.leaves.size();
   // factor storage: the H-matrix keeps exact ranks; the factors get room to grow
   // (cap = min(budget, 2 r + 48); truncations clipped at cap are counted)
-  std::vector<CopySeg> segs;
   int64_t leaf_end = 0;
   for (int li = 0; li < nleaf; ++li) {
     auto& L = T.leaves[li];
@@ -1548,6 +1582,48 @@ static void hlu_factor_impl(cbie_hlu* F) {
       F->pivoff[li] = npiv;
       npiv += T.leaves[li].m;
     }
+  F->npiv = npiv;
+  return leaf_end;
+}
+
+// temporaries before chunk reuse: most of the free HBM after the factor copy (a
+// reused chunk orders its new owner after every earlier access, which costs
+// parallelism), shared by `share` arenas on this device; CBIE_POOL_GB overrides
+static int64_t hlu_pool_budget(int64_t leaf_end, int share) {
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  double gb = 0.7 * ((double)fr / share - 2.0 * (double)leaf_end * sizeof(zc)) / (double)(1ll << 30) - 4.0;
+  gb = std::max(4.0, std::min(gb, 120.0));
+  if (getenv("CBIE_POOL_GB")) gb = atof(getenv("CBIE_POOL_GB"));
+  return (int64_t)(gb * (double)(1ll << 30)) / (int64_t)sizeof(zc);
+}
+
+// record the H-LU tape of F's block structure into R
+static void hlu_record(cbie_hlu* F, Recorder& R, int64_t leaf_end, int64_t budget, bool track) {
+  const Tree& T = F->tree;
+  const int nleaf = (int)T.leaves.size();
+  R.tol = F->tol;
+  R.leaf_end = leaf_end;
+  R.pool_budget = budget;
+  R.track = track;
+  for (int li = 0; li < nleaf; ++li) {
+    R.new_buf();
+    R.new_slot(0, li);
+  }
+  Builder B(R, *F);
+  B.factor(T.root_node);
+  B.flush_all();
+}
+
+static void hlu_factor_impl(cbie_hlu* F) {
+  cbie_hmat* H = F->H;
+  cbie_ctx* c = H->ctx;
+  cudaStream_t s = c->stream;
+  std::vector<CopySeg> segs;
+  const int64_t leaf_end = hlu_layout(F, segs);
+  const Tree& T = F->tree;
+  const int nleaf = (int)T.leaves.size();
+  const int64_t npiv = F->npiv;
   // structure key: leaf layout + tolerance; a hit skips recording and descriptor upload
   uint64_t key = 1469598103934665603ull;
   key = fnv(key, nleaf);
@@ -1561,27 +1637,7 @@ static void hlu_factor_impl(cbie_hlu* F) {
   if (!(use_cache && g_plan_cache && g_plan_cache->key == key)) {
     g_plan_cache.reset();   // release the previous plan's workspace first
     auto pc = std::make_unique<PlanCache>();
-    Recorder& R = pc->plan.R;
-    R.tol = F->tol;
-    R.leaf_end = leaf_end;
-    // temporaries before chunk reuse: most of the free HBM after the factor copy (a
-    // reused chunk orders its new owner after every earlier access, which costs
-    // parallelism), CBIE_POOL_GB overrides
-    {
-      size_t fr = 0, tot = 0;
-      cudaMemGetInfo(&fr, &tot);
-      double gb = 0.7 * ((double)fr - 2.0 * (double)leaf_end * sizeof(zc)) / (double)(1ll << 30) - 4.0;
-      gb = std::max(4.0, std::min(gb, 120.0));
-      if (getenv("CBIE_POOL_GB")) gb = atof(getenv("CBIE_POOL_GB"));
-      R.pool_budget = (int64_t)(gb * (double)(1ll << 30)) / (int64_t)sizeof(zc);
-    }
-    for (int li = 0; li < nleaf; ++li) {
-      R.new_buf();
-      R.new_slot(0, li);
-    }
-    Builder B(R, *F);
-    B.factor(T.root_node);
-    B.flush_all();
+    hlu_record(F, pc->plan.R, leaf_end, hlu_pool_budget(leaf_end, 1), false);
     make_plan(pc->plan, s);
     pc->key = key;
     pc->leaf_end = leaf_end;
@@ -1709,6 +1765,8 @@ static void hlu_factor_impl(cbie_hlu* F) {
   }
 }
 
+#include "hlu_dist.cuh"
+
 static void hlu_solve_impl(cbie_hlu* F, const zc* b, zc* x, int nrhs) {
   cbie_hmat* H = F->H;
   cudaStream_t s = H->ctx->stream;
@@ -1791,6 +1849,34 @@ int cbie_hlu_factor(cbie_hmat* h, double trunc_tol, cbie_hlu** out) {
     return e.code;
   }
   return CBIE_OK;
+}
+
+static int hlu_factor_dist_entry(cbie_hmat* h, double trunc_tol, int world, bool emulated, cbie_hlu** out) {
+  cbie_hlu* F = nullptr;
+  try {
+    cudaSetDevice(h->ctx->device);
+    if (!(trunc_tol > 0.0 && trunc_tol < 1.0)) throw cbie_error(CBIE_EINVALID, "trunc_tol in (0,1)");
+    if (h->partial) throw cbie_error(CBIE_ESTATE, "partial (sharded) H-matrix: exchange the shards first");
+    F = new cbie_hlu();
+    F->H = h;
+    F->tol = trunc_tol;
+    hlu_factor_dist_impl(F, world, emulated);
+    *out = F;
+  } catch (const cbie_error& e) {
+    h->ctx->err = e.what();
+    delete F;
+    *out = nullptr;
+    return e.code;
+  }
+  return CBIE_OK;
+}
+
+int cbie_hlu_factor_dist(cbie_hmat* h, double trunc_tol, cbie_hlu** out) {
+  return hlu_factor_dist_entry(h, trunc_tol, 0, false, out);
+}
+
+int cbie_hlu_factor_emulated(cbie_hmat* h, double trunc_tol, int world, cbie_hlu** out) {
+  return hlu_factor_dist_entry(h, trunc_tol, world, true, out);
 }
 
 void cbie_hlu_destroy(cbie_hlu* f) { delete f; }

@@ -193,6 +193,15 @@ void shard_exchange(cbie_hmat* H) {
 std::string stats_to_json(const std::map<std::string, double>& m);
 void hmatrix_build_entry(cbie_hmat* H, int n_leaf);
 
+bool dist_comm_of(const cbie_ctx* c, ncclComm_t* comm, int* rank, int* world) {
+  auto it = comms().find(c);
+  if (it == comms().end() || !it->second.comm) return false;
+  *comm = it->second.comm;
+  *rank = it->second.rank;
+  *world = it->second.world;
+  return true;
+}
+
 extern "C" {
 
 void cbie_partition_lpt(const double* cost, int64_t n, int world, int* owner) {

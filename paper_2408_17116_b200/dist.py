@@ -1,6 +1,7 @@
-"""Multi-GPU plumbing of the H-matrix fill: one process per GPU,
-torch.distributed only to hand the NCCL unique id to every rank; the shard
-exchange itself is ncclBroadcast inside libcbie (csrc/shard.cu).
+"""Multi-GPU plumbing of the H-matrix fill and H-LU: one process
+per GPU, torch.distributed only to hand the NCCL unique id to every rank; the
+shard exchange (csrc/shard.cu) and the block-row-distributed H-LU exchanges
+(csrc/hlu_dist.cuh) are NCCL calls inside libcbie.
 
 The reference parallelises the fill with a ThreadPoolExecutor over leaves
 (hmatrix.py:217-219); here the leaves are partitioned over processes by the
@@ -40,3 +41,10 @@ def init_nccl(gen, rank: int, world: int, group=None) -> None:
 
 def finalize(gen) -> None:
     gen.dev.lib.cbie_dist_finalize(gen.dev.h)
+
+
+def hlu_factor_distributed(H, tol: float):
+    """Block-row-distributed H-LU (cbie_hlu_factor_dist): every rank passes the
+    same complete H-matrix and gets the complete factors back."""
+    from .hmatrix import HLUFactors
+    return HLUFactors(H, tol, distributed=True)

@@ -136,11 +136,21 @@ class HMatrix:
 class HLUFactors:
     """H-LU factors on the device (HLUFactors, hmatrix.py:798-824)."""
 
-    def __init__(self, H: HMatrix, tol: float):
+    def __init__(self, H: HMatrix, tol: float, *, distributed: bool = False, emulate_world: int = 0):
+        """distributed: block-row-distributed H-LU over the context's NCCL
+        communicator (dist.init_nccl first; collective over the ranks);
+        emulate_world > 0: the same distributed plan run by that many virtual
+        ranks on this GPU (plan check without several GPUs)."""
         self.H = H
         self.dev = H.dev
         h = ct.c_void_p()
-        self.dev.check(self.dev.lib.cbie_hlu_factor(H.h, float(tol), ct.byref(h)))
+        lib = self.dev.lib
+        if emulate_world:
+            self.dev.check(lib.cbie_hlu_factor_emulated(H.h, float(tol), int(emulate_world), ct.byref(h)))
+        elif distributed:
+            self.dev.check(lib.cbie_hlu_factor_dist(H.h, float(tol), ct.byref(h)))
+        else:
+            self.dev.check(lib.cbie_hlu_factor(H.h, float(tol), ct.byref(h)))
         self.h = h
         self._stats = _ffi.stats(h, 2)
 
@@ -184,5 +194,5 @@ class HLUFactors:
         return ("lowrank", U, V)
 
 
-def hlu_factor(H: HMatrix, tol: float) -> HLUFactors:
-    return HLUFactors(H, tol)
+def hlu_factor(H: HMatrix, tol: float, **kw) -> HLUFactors:
+    return HLUFactors(H, tol, **kw)

@@ -97,3 +97,44 @@ def test_cfg1_rcs_within_005_db():
     # the host far-field restatement itself reproduces the reference on the reference's x
     sig_r, db_r = post.rcs_cut(prob, gen, g["x_direct"], 0.0, theta)
     assert np.abs(db_r - ref_db)[mask].max() <= 1e-9
+
+
+@pytest.mark.parametrize("world", [2, 3, 4])
+def test_distributed_hlu_plan_emulated(world):
+    """Block-row-distributed H-LU (cbie_hlu_factor_dist): the same
+    ownership + transfer plan run by `world` virtual ranks on one GPU (one arena
+    each, copies instead of NCCL).  A missing transfer leaves a stale block on the
+    reading rank, so the factors must match the single-GPU factorisation and the
+    solve must match the reference's surface current (10 x aca_tol)."""
+    from paper_2408_17116_b200 import hmatrix as hm
+    g = golden("cfg1_solve.npz")
+    from paper_2408_17116_b200 import geometry as geo, kernels as ker
+    from paper_2408_17116_b200.solver import Problem
+    vac = ker.Medium.from_relative(1.0, 1.0, 1.0)
+    # config 1 with leaf size 64: a deeper tree, more block rows, more exchanges
+    prob = Problem(geo.unit_sphere_patches(0.5, 1, (6, 6)), ker.FormulationSpec(ker.MFIE_PEC, vac),
+                   ker.PlaneWave([0, 0, 1], [1, 0, 0], 1.0), aca_tol=1e-6, eta=1.0, n_leaf=64)
+    gen = prob.generator()
+    H = hm.HMatrix(gen, prob.n_leaf, prob.eta, prob.aca_tol)
+    F1 = hm.hlu_factor(H, prob.effective_trunc_tol)
+    Fd = hm.hlu_factor(H, prob.effective_trunc_tol, emulate_world=world)
+    st = Fd.stats()
+    assert st["dist_world"] == world
+    assert st["dist_xfer_bytes"] > 0 and st["dist_msgs"] > 0
+    assert st["dist_tasks_min"] > 0                       # every rank factors something
+    b = gen.rhs(prob.excitation)
+    x1 = F1.solve(b)
+    xd = Fd.solve(b)
+    assert _rel(xd, x1) <= 1e-8
+    assert _rel(xd, g["x_direct"]) <= 10 * prob.aca_tol
+    perm, lv = H.tree()
+    for i in range(0, lv.shape[0], max(1, lv.shape[0] // 40)):
+        a, c = F1.leaf(i), Fd.leaf(i)
+        assert a[0] == c[0]
+        if a[0] == "lowrank":
+            A1, A2 = a[1] @ a[2], c[1] @ c[2]
+        else:
+            A1, A2 = a[1], c[1]
+            if a[0] == "lu":
+                assert np.array_equal(a[2], c[2])
+        assert np.linalg.norm(A2 - A1) <= 1e-8 * max(np.linalg.norm(A1), 1e-300)
