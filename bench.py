@@ -9,7 +9,8 @@ the H-LU factorisation (K7-K10).  metric = unknowns/s = N / (fill + H-LU time).
 For N > 1 (torchrun) every rank factors its own replica of the problem
 (weak scaling, no data-path collective); value = N * ranks / max step time.
 Beside it, "fill_sharded" times the fill of ONE problem with its leaves sharded
-over the ranks plus the NCCL exchange of the shards (strong scaling of the fill).
+over the ranks plus the NCCL exchange of the shards (strong scaling of the fill),
+and "hlu_distributed" the block-row-distributed H-LU of that H-matrix.
 
 --impl reference times the CPU oracle (numpy restatement of the reference,
 oracle/) on a bounded sample of the same workload (see oracle/baseline.py).
@@ -236,7 +237,7 @@ def run_gpu(args):
     # N > 1: the fill of ONE problem sharded over the ranks (LPT leaf partition, no
     # collective during the fill) + the NCCL exchange of the shards (csrc/shard.cu);
     # max-over-ranks device time, reported beside the replica throughput
-    fill_shard = None
+    fill_shard = hlu_dist = None
     if world > 1:
         from paper_2408_17116_b200 import dist as cdist
         cdist.init_nccl(gen, rank, world)
@@ -254,7 +255,29 @@ def run_gpu(args):
             torch.cuda.synchronize()
             t_f.append(a.elapsed_time(b))
             t_x.append(HS.stats().get("exchange_ms", 0.0))
-            del HS
+        # block-row-distributed H-LU of that H-matrix (csrc/hlu_dist.cuh): ncclSend/Recv
+        # of the blocks peers read between dependency levels, final broadcast of the factors
+        FD = cdist.hlu_factor_distributed(HS, prob.effective_trunc_tol)   # warm-up
+        del FD
+        t_h = []
+        for _ in range(max(1, args.steps)):
+            _barrier(world)
+            torch.cuda.synchronize()
+            a = torch.cuda.Event(enable_timing=True)
+            b = torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            FD = cdist.hlu_factor_distributed(HS, prob.effective_trunc_tol)
+            b.record(stream)
+            torch.cuda.synchronize()
+            t_h.append(a.elapsed_time(b))
+            dst = FD.stats()
+            del FD
+        h_ms = _reduce_max(statistics.median(t_h), world)
+        hlu_dist = {"ms": h_ms, "single_gpu_hlu_ms": statistics.mean(f["factor_device_ms"] for f in fstats),
+                    "xfer_bytes": dst.get("dist_xfer_bytes"), "final_bytes": dst.get("dist_final_bytes"),
+                    "messages": dst.get("dist_msgs"), "row_level": dst.get("dist_row_level"),
+                    "scheme": "block rows dealt cyclically, level-synchronous ncclSend/Recv of peer-read blocks"}
+        del HS
         f_ms = _reduce_max(statistics.median(t_f), world)
         x_ms = _reduce_max(statistics.median(t_x), world)
         single = statistics.mean(h["fill_ms"] for h in hstats)
@@ -311,6 +334,8 @@ def run_gpu(args):
         line["e2e"] = e2e
     if fill_shard:
         line["fill_sharded"] = fill_shard
+    if hlu_dist:
+        line["hlu_distributed"] = hlu_dist
     if rank == 0 and world == 1 and not args.no_cpu:
         v, sec, desc, det = cpu_baseline_line(args.config, 1, 0, args.ref_level)
         line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "port", "sample": desc,

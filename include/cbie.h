@@ -150,6 +150,13 @@ int cbie_hlu_leaf(cbie_hlu* f, int64_t leaf, int* kind, int* rank, cbie_c128* D_
  * HLUFactors.solve (hmatrix.py:807-816). */
 int cbie_hlu_solve(cbie_hlu* f, const cbie_c128* b, cbie_c128* x, int nrhs);
 
+/* Far-field radiation sums (postprocess.far_field, postprocess.py:193-212):
+ * out[a][t] = sum_n exp(j k rhat_a . pos_n) tab[n][t] over the context's
+ * quadrature nodes (cbie_node_frames order); tab [npts][ntab] row-major
+ * (ntab <= 8: the w J, w div J [, w M, w div M] tables), rhat [nang][3]. */
+int cbie_far_field_sums(cbie_ctx* ctx, const cbie_c128* tab, int ntab, const double* rhat, int nang,
+                        double k, cbie_c128* out);
+
 /* Low-rank recompression of host data (truncate_lowrank, hmatrix.py:412-426):
  * U [m][k] row-major, V [k][n] row-major -> Uo [m][*r], Vo [*r][n] (capacity
  * min(m, n, k) rows/cols).  V == NULL: truncated SVD of the dense U [m][n]

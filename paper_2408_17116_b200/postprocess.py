@@ -1,13 +1,14 @@
-"""Far field and bistatic RCS from a solution vector (host numpy; used for the
-RCS parity check of BASELINE.json, not part of the accelerated path).
+"""Far field and bistatic RCS from a solution vector.
 Restates postprocess.py:30-233 (density_grids, _patch_tables native branch,
-far_field, rcs_cut)."""
+far_field, rcs_cut): the O(N) quadrature tables are formed on the host, the
+O(angles x N) phase-weighted radiation sums run on the device
+(cbie_far_field_sums, csrc/farfield.cu)."""
 
 from __future__ import annotations
 
 import numpy as np
 
-from . import geometry as geo
+from . import _ffi, geometry as geo
 
 
 def _fejer_weights(n):
@@ -48,14 +49,22 @@ def radiation_tables(gen, solution):
 def far_field(problem, gen, solution, theta, phi):
     med = problem.spec.outer
     k, omega = med.k, med.omega
+    if abs(np.imag(k)) > 0.0:
+        raise ValueError("far field: lossy exterior medium (complex k) is not supported")
     pos, tabs = radiation_tables(gen, solution)
-    rhat = np.stack([np.sin(theta) * np.cos(phi), np.sin(theta) * np.sin(phi), np.cos(theta)], 1)
-    phase = np.exp(1j * k * (rhat @ pos.T))
-    wJ, wdJ = tabs[0]
-    F = -(1.0 / (4 * np.pi)) * (1j * omega * med.mu * (phase @ wJ)
-                                + (k / (omega * med.eps)) * rhat * (phase @ wdJ)[:, None])
+    rhat = np.ascontiguousarray(
+        np.stack([np.sin(theta) * np.cos(phi), np.sin(theta) * np.sin(phi), np.cos(theta)], 1))
+    cols = [tabs[0][0], tabs[0][1][:, None]]
     if len(tabs) > 1:
-        F = F + (1.0 / (4 * np.pi)) * 1j * k * np.cross(rhat, phase @ tabs[1][0])
+        cols.append(tabs[1][0])
+    tab = np.ascontiguousarray(np.concatenate(cols, axis=1).astype(complex))
+    sums = np.empty((rhat.shape[0], tab.shape[1]), complex)
+    gen.dev.check(gen.dev.lib.cbie_far_field_sums(gen.dev.h, _ffi.ptr(tab), int(tab.shape[1]), _ffi.ptr(rhat),
+                                                  int(rhat.shape[0]), float(np.real(k)), _ffi.ptr(sums)))
+    Jhat, Jdiv = sums[:, 0:3], sums[:, 3]
+    F = -(1.0 / (4 * np.pi)) * (1j * omega * med.mu * Jhat + (k / (omega * med.eps)) * rhat * Jdiv[:, None])
+    if len(tabs) > 1:
+        F = F + (1.0 / (4 * np.pi)) * 1j * k * np.cross(rhat, sums[:, 4:7])
     return F - rhat * np.sum(F * rhat, axis=1)[:, None], rhat
 
 

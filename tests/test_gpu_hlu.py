@@ -138,3 +138,26 @@ def test_distributed_hlu_plan_emulated(world):
             if a[0] == "lu":
                 assert np.array_equal(a[2], c[2])
         assert np.linalg.norm(A2 - A1) <= 1e-8 * max(np.linalg.norm(A1), 1e-300)
+
+
+def test_distributed_hlu_nccl_world1():
+    """cbie_hlu_factor_dist through a real NCCL communicator of one rank: the
+    NCCL code path (budget all-reduce, final broadcast, flag/overflow reductions)
+    runs and gives the single-GPU factors."""
+    import ctypes as ct
+    from paper_2408_17116_b200 import _ffi, dist as cdist, hmatrix as hm
+    prob = _problem("cfg1")
+    gen = prob.generator()
+    lib = gen.dev.lib
+    buf = ct.create_string_buffer(128)
+    _ffi.check(lib.cbie_nccl_unique_id(buf, 128))
+    gen.dev.check(lib.cbie_dist_init(gen.dev.h, bytes(buf.raw), 0, 1))
+    try:
+        H = hm.HMatrix(gen, prob.n_leaf, prob.eta, prob.aca_tol)
+        b = gen.rhs(prob.excitation)
+        x1 = hm.hlu_factor(H, prob.effective_trunc_tol).solve(b)
+        Fd = cdist.hlu_factor_distributed(H, prob.effective_trunc_tol)
+        assert Fd.stats()["dist_world"] == 1
+        assert _rel(Fd.solve(b), x1) <= 1e-8
+    finally:
+        cdist.finalize(gen)
