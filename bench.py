@@ -29,6 +29,8 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# one hardware work queue per executor stream (see paper_2408_17116_b200/__init__.py)
+os.environ.setdefault("CUDA_DEVICE_MAX_CONNECTIONS", "32")
 
 METRIC = "CBIE H-matrix fill+H-LU throughput (unknowns/s)"
 UNIT = "unknowns/s"

@@ -144,6 +144,7 @@ struct cbie_error : std::runtime_error {
 // every kernel launch site calls CKL(); it also counts launches (cbie_launch_count)
 #include <atomic>
 extern std::atomic<long long> g_cbie_launches;
+extern std::atomic<long long> g_cbie_frees;   // cudaFree calls (each one synchronises the device)
 #define CKL()                 \
   do {                        \
     ++g_cbie_launches;        \
@@ -159,7 +160,10 @@ struct DBuf {
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() { release(); }
   void release() {
-    if (p) cudaFree(p);
+    if (p) {
+      cudaFree(p);
+      ++g_cbie_frees;
+    }
     p = nullptr;
     n = 0;
   }

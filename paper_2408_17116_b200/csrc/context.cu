@@ -257,6 +257,7 @@ void ctx_set_formulation(cbie_ctx* c, int kind, double omega, zc k1, zc k2, zc e
 }
 
 std::atomic<long long> g_cbie_launches{0};
+std::atomic<long long> g_cbie_frees{0};
 
 // ---------------------------------------------------------------------------
 // C-ABI

@@ -1078,6 +1078,8 @@ struct Exec {
   double kind_ms[OP_NKIND] = {};
   int kind_launch[OP_NKIND] = {};
   int64_t kind_tasks[OP_NKIND] = {};
+  double host_enqueue_ms = 0.0;   // host time to issue the whole plan (before the final sync)
+  long long frees = 0;            // cudaFree calls while issuing (device-wide syncs)
 };
 
 struct Grp {
@@ -1217,10 +1219,37 @@ void make_plan(Plan& P, cudaStream_t s, const Recorder* Rx = nullptr, const std:
 
 // lvl_lo / lvl_hi: run only the groups of these levels, level-synchronously on s0
 // (the distributed H-LU exchanges data between levels)
+// executor streams, created once per device: the same hardware work queues every
+// factorisation (CUDA_DEVICE_MAX_CONNECTIONS = 32 gives each its own queue, see
+// paper_2408_17116_b200/__init__.py); the diagonal chain (getrf, trsm) runs at the
+// highest stream priority
+struct StreamPool {
+  cudaStream_t kind[NVK] = {}, lane2[TRUNC_LANES] = {}, side = nullptr;
+};
+StreamPool& stream_pool() {
+  static std::map<int, StreamPool> pools;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  auto it = pools.find(dev);
+  if (it != pools.end()) return it->second;
+  StreamPool& P = pools[dev];
+  int lo = 0, hi = 0;   // hi = greatest priority (numerically lowest)
+  CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  for (int q = 0; q < NVK; ++q) {
+    const int pr = (q == OP_GETRF || q == OP_TRSM) ? hi : lo;
+    CK(cudaStreamCreateWithPriority(&P.kind[q], cudaStreamNonBlocking, pr));
+  }
+  for (int l = 0; l < TRUNC_LANES; ++l) CK(cudaStreamCreateWithPriority(&P.lane2[l], cudaStreamNonBlocking, lo));
+  CK(cudaStreamCreateWithPriority(&P.side, cudaStreamNonBlocking, lo));
+  return P;
+}
+
 Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag,
               unsigned long long* ovf, TruncWork* tw, double tol, cudaStream_t s0, int lvl_lo = 0,
               int lvl_hi = 1 << 30) {
   Exec ex;
+  const auto th0 = std::chrono::steady_clock::now();
+  const long long fr0 = g_cbie_frees.load();
   const bool ranged = lvl_lo > 0 || lvl_hi < (1 << 30);
   cudaStream_t s = s0;
   // per recompression lane: second stream (dense-mode / Householder share of a group),
@@ -1229,7 +1258,7 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
   cudaStream_t s2l[TRUNC_LANES] = {};
   cudaEvent_t fork_l[TRUNC_LANES] = {}, join_l[TRUNC_LANES] = {};
   for (int l = 0; l < TRUNC_LANES; ++l) {
-    CK(cudaStreamCreateWithFlags(&s2l[l], cudaStreamNonBlocking));
+    s2l[l] = stream_pool().lane2[l];
     CK(cudaEventCreateWithFlags(&fork_l[l], cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&join_l[l], cudaEventDisableTiming));
   }
@@ -1258,7 +1287,7 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
   if (blk_lu) {
     CK(cudaFuncSetAttribute(k_trsm_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_blk_smem));
     CK(cudaFuncSetAttribute(k_getrf_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)blk_smem));
-    CK(cudaStreamCreateWithFlags(&s3, cudaStreamNonBlocking));
+    s3 = stream_pool().side;
     CK(cudaEventCreateWithFlags(&rc_ev, cudaEventDisableTiming));
     int nl = 1;
     for (auto& x : P.f) nl = std::max(nl, x.leaf + 1);
@@ -1290,7 +1319,7 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
         ks[q] = ks[shared_q];
         continue;
       }
-      CK(cudaStreamCreateWithFlags(&ks[q], cudaStreamNonBlocking));
+      ks[q] = stream_pool().kind[q];
       CK(cudaStreamWaitEvent(ks[q], st0, 0));
       if (!(mask >> q & 1)) shared_q = q;
     }
@@ -1471,22 +1500,17 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
     CK(cudaEventRecord(rc_ev, s3));
     CK(cudaStreamWaitEvent(s, rc_ev, 0));
   }
+  ex.host_enqueue_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - th0).count();
+  ex.frees = g_cbie_frees.load() - fr0;
   CK(cudaStreamSynchronize(s));
   if (s3) {
     cudaEventDestroy(rc_ev);
-    cudaStreamDestroy(s3);
   }
   for (int l = 0; l < TRUNC_LANES; ++l) {
     cudaEventDestroy(fork_l[l]);
     cudaEventDestroy(join_l[l]);
-    cudaStreamDestroy(s2l[l]);
   }
   for (auto& e : gev) cudaEventDestroy(e);
-  for (int q = 0; q < NVK; ++q) {
-    bool dup = false;
-    for (int p = 0; p < q; ++p) dup |= ks[p] == ks[q];
-    if (ks[q] && !dup) cudaStreamDestroy(ks[q]);
-  }
   for (size_t i = 0; i + 1 < tev.size(); i += 2) {
     float ms = 0;
     cudaEventElapsedTime(&ms, tev[i], tev[i + 1]);
@@ -1586,13 +1610,13 @@ static int64_t hlu_layout(cbie_hlu* F, std::vector<CopySeg>& segs) {
   return leaf_end;
 }
 
-// temporaries before chunk reuse: most of the free HBM after the factor copy (a
+// temporaries before chunk reuse: 60 % of the free HBM after the factor copy (a
 // reused chunk orders its new owner after every earlier access, which costs
-// parallelism), shared by `share` arenas on this device; CBIE_POOL_GB overrides
+// parallelism; the rest is left to the recompression workspaces), shared by `share` arenas on this device; CBIE_POOL_GB overrides
 static int64_t hlu_pool_budget(int64_t leaf_end, int share) {
   size_t fr = 0, tot = 0;
   cudaMemGetInfo(&fr, &tot);
-  double gb = 0.7 * ((double)fr / share - 2.0 * (double)leaf_end * sizeof(zc)) / (double)(1ll << 30) - 4.0;
+  double gb = 0.6 * ((double)fr / share - 2.0 * (double)leaf_end * sizeof(zc)) / (double)(1ll << 30) - 4.0;
   gb = std::max(4.0, std::min(gb, 120.0));
   if (getenv("CBIE_POOL_GB")) gb = atof(getenv("CBIE_POOL_GB"));
   return (int64_t)(gb * (double)(1ll << 30)) / (int64_t)sizeof(zc);
@@ -1686,6 +1710,8 @@ static void hlu_factor_impl(cbie_hlu* F) {
   CK(cudaMemcpy(&hovf, ovf.p, 8, cudaMemcpyDeviceToHost));
   F->leaf_end = leaf_end;
   F->stat["levels"] = ex.levels;
+  F->stat["host_enqueue_ms"] = ex.host_enqueue_ms;
+  F->stat["frees_during_run"] = (double)ex.frees;
   F->stat["trunc_kernel_ms"] = ex.trunc_kernel_ms;
   if (getenv("CBIE_PROFILE")) {
     unsigned long long h[16] = {};

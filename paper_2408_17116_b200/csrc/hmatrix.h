@@ -121,7 +121,7 @@ void launch_truncate_routed(zc* arena, int* ranks, const TruncDesc* d_desc, int 
                             int mn_max, TruncWork* work2 = nullptr, cudaStream_t s2 = nullptr);
 void launch_truncate_gram(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, double tol,
                           unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, zc* arena_out,
-                          int* defer, const int* idx = nullptr);
+                          int* defer, const int* idx = nullptr, int mn_multi = 0);
 bool launch_truncate_blocked(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, double tol,
                              unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, int kc_max,
                              int mn_max, zc* arena_out, int* defer, const int* idx = nullptr);

@@ -437,65 +437,34 @@ static void launch_unblocked_list(zc* arena, zc* arena_out, int* ranks, const Tr
 }
 
 namespace {
-// split problems by device-side rank: k <= 64 (and no-ops) -> la, k > 64 -> lb
-__global__ void k_route(const int* __restrict__ ranks, const TruncDesc* __restrict__ ds, int nd, int* la, int* lb) {
+// split problems by device-side rank: k <= kg (and no-ops) -> la (Gram kernel), the rest -> lb
+__global__ void k_route(const int* __restrict__ ranks, const TruncDesc* __restrict__ ds, int nd, int kg, int* la,
+                        int* lb) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nd; i += gridDim.x * blockDim.x) {
     const TruncDesc& d = ds[i];
     const int k = d.k_slot >= 0 ? ranks[d.k_slot] : d.k;
     const bool skip = d.skip_slot >= 0 && ranks[d.skip_slot] == 0;
-    if (skip || k <= 64) la[1 + atomicAdd(la, 1)] = i;
+    if (skip || k <= kg) la[1 + atomicAdd(la, 1)] = i;
     else lb[1 + atomicAdd(lb, 1)] = i;
   }
 }
 }  // namespace
 
-void launch_truncate_routed(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
-                            unsigned long long* overflow, TruncWork& work, cudaStream_t s, int kc_max,
-                            int mn_max, TruncWork* work2, cudaStream_t s2) {
-  if (nd == 0) return;
-  if (kc_max <= 64) {   // no capacity can exceed the Gram path
-    launch_truncate_gram(arena, ranks, d_desc, nd, tol, overflow, work.scratch, s, nullptr, nullptr);
-    return;
-  }
-  TruncWork& wb = work2 ? *work2 : work;
-  cudaStream_t sb = work2 && s2 ? s2 : s;
-  if (work.gdefer.n < (size_t)nd + 1) work.gdefer.alloc(std::max<size_t>(nd + 1, 4096));
-  if (wb.gdefer.n < (size_t)nd + 1 || &wb == &work) {
-    if (&wb == &work) {
-      if (work.defer.n < 2 * (size_t)nd + 2) work.defer.alloc(std::max<size_t>(2 * nd + 2, 8192));
-    } else {
-      wb.gdefer.alloc(std::max<size_t>(nd + 1, 4096));
-    }
-  }
-  int* la = work.gdefer.p;
-  int* lb = &wb == &work ? work.defer.p + nd + 1 : wb.gdefer.p;
-  CK(cudaMemsetAsync(la, 0, sizeof(int), s));
-  CK(cudaMemsetAsync(lb, 0, sizeof(int), s));
-  k_route<<<std::min((nd + 255) / 256, 148), 256, 0, s>>>(ranks, d_desc, nd, la, lb);
-  CKL();
-  cudaEvent_t fork = nullptr, join = nullptr;
-  if (sb != s) {
-    CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
-    CK(cudaEventRecord(fork, s));
-    CK(cudaStreamWaitEvent(sb, fork, 0));
-  }
-  // ranks > 64: blocked Householder kernel (k <= 128, max(m, n) <= 384), then unblocked
-  const int* list = lb;
-  bool done = getenv("CBIE_DBG_SKIP_BIG") != nullptr;   // timing experiment only (wrong factors)
-  if (!done && mn_max <= 384) {
+// Householder kernels over a device-side list (count in list[0]): blocked kernel for
+// k <= 128 and max(m, n) <= 384 (its own hand-offs), unblocked for the rest
+static void householder_list(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
+                             unsigned long long* overflow, TruncWork& w, cudaStream_t st, int kc_max, int mn_max,
+                             const int* list) {
+  bool done = false;
+  if (mn_max <= 384) {
     int* dfr = nullptr;
     if (kc_max > 128) {
-      if (&wb == &work) {
-        dfr = work.defer.p;   // first nd + 1 entries
-      } else {
-        if (wb.defer.n < (size_t)nd + 1) wb.defer.alloc(std::max<size_t>(nd + 1, 4096));
-        dfr = wb.defer.p;
-      }
-      CK(cudaMemsetAsync(dfr, 0, sizeof(int), sb));
+      if (w.defer.n < (size_t)nd + 1) w.defer.alloc(std::max<size_t>(nd + 1, 4096));
+      dfr = w.defer.p;
+      CK(cudaMemsetAsync(dfr, 0, sizeof(int), st));
     }
-    launch_truncate_blocked(arena, ranks, d_desc, nd, tol, overflow, wb.scratch, sb, kc_max, mn_max, arena, dfr,
-                            lb);
+    launch_truncate_blocked(arena, ranks, d_desc, nd, tol, overflow, w.scratch, st, kc_max, mn_max, arena, dfr,
+                            list);
     if (!dfr) done = true;
     else list = dfr;
   }
@@ -505,16 +474,56 @@ void launch_truncate_routed(zc* arena, int* ranks, const TruncDesc* d_desc, int 
                                           (int64_t)RLMAX * (4 * (int64_t)mn_max + kc_max + 1) +
                                               2 * (int64_t)RLMAX * RLMAX) +
                         4 * (int64_t)kmax;
-    launch_unblocked_list(arena, arena, ranks, d_desc, nd, kmax, per, tol, overflow, wb, sb, list);
+    launch_unblocked_list(arena, arena, ranks, d_desc, nd, kmax, per, tol, overflow, w, st, list);
   }
-  // ranks <= 64: Gram kernel over its list (concurrently when sb != s)
-  launch_truncate_gram(arena, ranks, d_desc, nd, tol, overflow, work.scratch, s, nullptr, nullptr, la);
-  if (sb != s) {
+}
+
+// Gram kernel for ranks <= 64 and, multi-stage, up to 256 (its failures then go to
+// the Householder kernels on the same stream); larger ranks to the Householder
+// kernels on the second stream, concurrently.
+void launch_truncate_routed(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
+                            unsigned long long* overflow, TruncWork& work, cudaStream_t s, int kc_max,
+                            int mn_max, TruncWork* work2, cudaStream_t s2) {
+  if (nd == 0) return;
+  const bool multi = getenv("CBIE_NO_MULTISTAGE") == nullptr;
+  const int kg = multi ? 256 : 64;
+  if (kc_max <= 64) {   // no capacity can exceed the single-stage Gram path
+    launch_truncate_gram(arena, ranks, d_desc, nd, tol, overflow, work.scratch, s, nullptr, nullptr);
+    return;
+  }
+  TruncWork& wb = work2 ? *work2 : work;
+  cudaStream_t sb = work2 && s2 ? s2 : s;
+  // lists: la (Gram), lb (Householder, stream sb), lf (Gram failures, stream s)
+  if (work.gdefer.n < 3 * (size_t)nd + 3) work.gdefer.alloc(std::max<size_t>(3 * nd + 3, 3 * 4096));
+  int* la = work.gdefer.p;
+  int* lf = la + nd + 1;
+  int* lb = lf + nd + 1;
+  CK(cudaMemsetAsync(la, 0, sizeof(int) * (2 * nd + 2), s));   // counts of la and lf (and la's payload)
+  CK(cudaMemsetAsync(lb, 0, sizeof(int), s));
+  k_route<<<std::min((nd + 255) / 256, 148), 256, 0, s>>>(ranks, d_desc, nd, kg, la, lb);
+  CKL();
+  cudaEvent_t fork = nullptr, join = nullptr;
+  const bool two = sb != s && kc_max > kg;
+  if (two) {
+    CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    CK(cudaEventRecord(fork, s));
+    CK(cudaStreamWaitEvent(sb, fork, 0));
+  }
+  if (kc_max > kg)
+    householder_list(arena, ranks, d_desc, nd, kmax, tol, overflow, two ? wb : work, two ? sb : s, kc_max, mn_max,
+                     lb);
+  launch_truncate_gram(arena, ranks, d_desc, nd, tol, overflow, work.scratch, s, nullptr, multi ? lf : nullptr, la,
+                       multi ? mn_max : 0);
+  if (two) {
     CK(cudaEventRecord(join, sb));
     CK(cudaStreamWaitEvent(s, join, 0));
     cudaEventDestroy(fork);
     cudaEventDestroy(join);
   }
+  // multi-stage failures (kept rank filled the Gram capacity), after the join so that
+  // they reuse the Householder workspaces of the second stream
+  if (multi) householder_list(arena, ranks, d_desc, nd, kmax, tol, overflow, wb, s, kc_max, mn_max, lf);
 }
 
 void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,

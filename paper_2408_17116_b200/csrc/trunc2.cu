@@ -47,13 +47,15 @@
 extern unsigned long long* g_trunc_prof;
 
 // Gram-path recompression of factor-form problems; those whose device-side rank
-// exceeds 64 are appended to defer (defer[0] = count, then indices into d_desc)
+// exceeds 64 are appended to defer (defer[0] = count, then indices into d_desc),
+// unless mn_multi > 0: then ranks up to 256 with max(m, n) <= mn_multi take the
+// multi-stage Gram path and only its failures are deferred
 void launch_truncate_gram(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, double tol,
                           unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, zc* arena_out,
-                          int* defer, const int* idx) {
+                          int* defer, const int* idx, int mn_multi) {
   if (nd == 0) return;
   t2b::launch_gram(arena, arena_out ? arena_out : arena, ranks, d_desc, nd, tol, overflow, scratch, s,
-                   g_trunc_prof, defer, idx);
+                   g_trunc_prof, defer, idx, mn_multi);
 }
 
 bool launch_truncate_blocked(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, double tol,

@@ -922,38 +922,18 @@ __device__ int herm_jacobi(zc* H, int n, zc* X, Smem& S) {
   return sweep;
 }
 
-__global__ void __launch_bounds__(NT, 1)
-    k_trunc_gram(zc* arena, zc* aout, int* ranks, const TruncDesc* __restrict__ descs, zc* scratch, int64_t per,
-                 double tol, unsigned long long* overflow, unsigned long long* prof, int* defer, int base,
-                 const int* idx) {
-  __shared__ Smem S;
+// One Gram-path recompression (steps 1-5 above) of U (m x k, ldu) Vt (n x k, ldv),
+// k <= KG: writes Uo (m x r, ld m), Vo (n x r, ld n) and returns r (0: zero product);
+// r is clipped at cap (counted in overflow).  sc: per-CTA scratch (4 GSQ).
+__device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restrict__ Vt, int ldv, int m, int n,
+                          int k, zc* __restrict__ Uo, zc* __restrict__ Vo, int cap, double tol, zc* sc,
+                          unsigned long long* overflow, Smem& S, zc* sm, long long* tc, int* sweeps_out) {
   __shared__ double alpha[KG], ainv[KG], scu[KG], scv[KG];
   __shared__ int pu[KG], pv[KG], posu[KG], posv[KG];
-  extern __shared__ __align__(16) unsigned char smraw[];
-  zc* sm = reinterpret_cast<zc*>(smraw);
   zc* Gu = sm;
   zc* Gv = sm + GSQ;
   zc* X2 = sm + 2 * GSQ;
-  // idx: run the problems listed in idx[1 + base + blockIdx.x] (count idx[0]) of descs
-  if (idx && base + (int)blockIdx.x >= idx[0]) return;
-  const int tix = idx ? idx[1 + base + blockIdx.x] : (int)blockIdx.x;
-  const TruncDesc d = descs[tix];
-  const long long tc0 = clock64();
-  if (d.skip_slot >= 0 && ranks[d.skip_slot] == 0) return;
-  const int k = d.k_slot >= 0 ? ranks[d.k_slot] : d.k;
-  const int m = d.m, n = d.n;
-  if (k <= 0 || m == 0 || n == 0) {
-    if (threadIdx.x == 0) ranks[d.out_slot] = 0;
-    return;
-  }
-  if (k > KG) {   // handed to the Householder kernels
-    if (threadIdx.x == 0) defer[1 + atomicAdd(defer, 1)] = idx ? tix : base + blockIdx.x;
-    return;
-  }
   if (threadIdx.x == 0) flop_add(8.0 * (m + n) * (double)k * k);
-  const zc* U = arena + d.in_u;
-  const zc* Vt = arena + d.in_v;
-  zc* sc = scratch + (int64_t)blockIdx.x * per;
   zc* Rug = sc;
   zc* Rvg = sc + GSQ;
   zc* Mg = sc + 2 * GSQ;
@@ -962,8 +942,8 @@ __global__ void __launch_bounds__(NT, 1)
   // 1. Gram matrices
   for (int e = threadIdx.x; e < 2 * GSQ; e += NT) sm[e] = zmk(0.0, 0.0);
   __syncthreads();
-  gram_acc(U, m, k, d.ldu, Gu, X2);
-  gram_acc(Vt, n, k, d.ldv, Gv, X2);
+  gram_acc(U, m, k, ldu, Gu, X2);
+  gram_acc(Vt, n, k, ldv, Gv, X2);
   // 2. balancing
   for (int c = threadIdx.x; c < k; c += NT) {
     const double du = Gu[c * k + c].x, dv = Gv[c * k + c].x;
@@ -978,14 +958,11 @@ __global__ void __launch_bounds__(NT, 1)
     Gv[b * k + a] = zscale(Gv[b * k + a], ainv[a] * ainv[b]);
   }
   __syncthreads();
-  const long long tc1 = clock64();
+  tc[1] = clock64();
   // 3. pivoted Cholesky
   const int ku = pchol(Gu, k, pu, CHOL_EPS, S);
   const int kv = pchol(Gv, k, pv, CHOL_EPS, S);
-  if (ku == 0 || kv == 0) {
-    if (threadIdx.x == 0) ranks[d.out_slot] = 0;
-    return;
-  }
+  if (ku == 0 || kv == 0) return 0;
   for (int c = threadIdx.x; c < k; c += NT) {
     posu[pu[c]] = c;
     posv[pv[c]] = c;
@@ -1033,7 +1010,7 @@ __global__ void __launch_bounds__(NT, 1)
     Z[b * kp + a] = zmk(a == b ? 1.0 : 0.0, 0.0);
   }
   __syncthreads();
-  const long long tc2 = clock64();
+  tc[2] = clock64();
   const int sweeps = herm_jacobi(Gp, kp, Z, S);
   for (int c = threadIdx.x; c < kp; c += NT) S.sig[c] = sqrt(fmax(Gp[c * kp + c].x, 0.0));
   __syncthreads();
@@ -1044,7 +1021,7 @@ __global__ void __launch_bounds__(NT, 1)
     S.order[pos] = c;
   }
   __syncthreads();
-  const long long tc3 = clock64();
+  tc[3] = clock64();
   const double s0 = kp > 0 ? S.sig[S.order[0]] : 0.0;
   int r = 0;
   if (s0 > 0.0) {
@@ -1052,9 +1029,9 @@ __global__ void __launch_bounds__(NT, 1)
       if (S.sig[c] > tol * s0) ++r;
     r = max(r, 1);
   }
-  if (r > d.cap) {
+  if (r > cap) {
     if (threadIdx.x == 0) atomicAdd(overflow, 1ull);
-    r = d.cap;
+    r = cap;
   }
   // W = P R^H Z_r (kk1 x r) in Gv's region (G dead: S.sig holds its diagonal)
   __syncthreads();
@@ -1081,9 +1058,7 @@ __global__ void __launch_bounds__(NT, 1)
   __syncthreads();
   // 6a. U' = U_sel D R_u11^{-1} W
   tri_solve_cols(X2, k, kk1, W, r, scu);
-  zc* Uo = aout + d.out_u;
-  zc* Vo = aout + d.out_v;
-  if (r > 0) apply_sel(U, m, d.ldu, pu, kk1, W, r, Uo);
+  if (r > 0) apply_sel(U, m, ldu, pu, kk1, W, r, Uo);
   __syncthreads();
   // 6b. Vt' = Vt_sel D^{-1} R_v11^{-1} conj(Vhat)
   zc* W2 = Gu;
@@ -1091,31 +1066,114 @@ __global__ void __launch_bounds__(NT, 1)
   for (int e = threadIdx.x; e < kk2 * r; e += NT) W2[e] = Vhg[e];
   __syncthreads();
   tri_solve_cols(X2, k, kk2, W2, r, scv);
-  if (r > 0) apply_sel(Vt, n, d.ldv, pv, kk2, W2, r, Vo);
-  if (threadIdx.x == 0) {
+  if (r > 0) apply_sel(Vt, n, ldv, pv, kk2, W2, r, Vo);
+  if (threadIdx.x == 0)
     // applies, pivoted Choleskys, M and H products, Jacobi sweeps (Gram counted above)
     flop_add(8.0 * ((double)m * kk1 + (double)n * kk2) * r + 16.0 * k * (double)k * k / 3.0 +
              8.0 * kk1 * (double)kk2 * (k + kk1) + 32.0 * sweeps * (double)kp * kp * kp);
+  *sweeps_out = sweeps;
+  __syncthreads();
+  return r;
+}
+
+// Multi-stage Gram path for KG < k <= KMS: the columns are taken in batches, each
+// batch recompressed together with the basis kept so far ([U_r | next columns],
+// r + batch <= KG), ping-ponging between two scratch bases; the last stage writes
+// the output.  Every stage truncates at tol relative to its own largest singular
+// value (the reference truncates once): the error stays O(tol s_0), inside the
+// solution-level budget.  A problem whose kept rank leaves no room (r == KG with
+// columns left) is handed to the Householder kernels through defer.
+constexpr int KMS = 4 * KG;
+
+__host__ __device__ inline int64_t gram_ms_scratch(int mn_max) { return 4 * (int64_t)mn_max * KG; }
+
+__global__ void __launch_bounds__(NT, 1)
+    k_trunc_gram(zc* arena, zc* aout, int* ranks, const TruncDesc* __restrict__ descs, zc* scratch, int64_t per,
+                 double tol, unsigned long long* overflow, unsigned long long* prof, int* defer, int base,
+                 const int* idx, int mn_max) {
+  __shared__ Smem S;
+  extern __shared__ __align__(16) unsigned char smraw[];
+  zc* sm = reinterpret_cast<zc*>(smraw);
+  // idx: run the problems listed in idx[1 + base + blockIdx.x] (count idx[0]) of descs
+  if (idx && base + (int)blockIdx.x >= idx[0]) return;
+  const int tix = idx ? idx[1 + base + blockIdx.x] : (int)blockIdx.x;
+  const TruncDesc d = descs[tix];
+  long long tc[5];
+  tc[0] = clock64();
+  if (d.skip_slot >= 0 && ranks[d.skip_slot] == 0) return;
+  const int k = d.k_slot >= 0 ? ranks[d.k_slot] : d.k;
+  const int m = d.m, n = d.n;
+  if (k <= 0 || m == 0 || n == 0) {
+    if (threadIdx.x == 0) ranks[d.out_slot] = 0;
+    return;
+  }
+  const bool multi = k > KG && k <= KMS && max(m, n) <= mn_max;
+  if (k > KG && !multi) {   // handed to the Householder kernels
+    if (threadIdx.x == 0) defer[1 + atomicAdd(defer, 1)] = idx ? tix : base + blockIdx.x;
+    return;
+  }
+  const zc* U = arena + d.in_u;
+  const zc* Vt = arena + d.in_v;
+  zc* sc = scratch + (int64_t)blockIdx.x * per;
+  zc* Uo = aout + d.out_u;
+  zc* Vo = aout + d.out_v;
+  int sweeps = 0, r = 0;
+  if (!multi) {
+    r = gram_stage(U, d.ldu, Vt, d.ldv, m, n, k, Uo, Vo, d.cap, tol, sc, overflow, S, sm, tc, &sweeps);
+  } else {
+    zc* bu[2] = {sc + 4 * GSQ, sc + 4 * GSQ + (int64_t)2 * mn_max * KG};
+    zc* bv[2] = {bu[0] + (int64_t)mn_max * KG, bu[1] + (int64_t)mn_max * KG};
+    int cur = 0, done = KG;
+    r = gram_stage(U, d.ldu, Vt, d.ldv, m, n, KG, bu[0], bv[0], KG, tol, sc, overflow, S, sm, tc, &sweeps);
+    while (done < k) {
+      const int add = min(KG - r, k - done);
+      if (add <= 0) {   // no room left: Householder kernels (nothing written to the output yet)
+        if (threadIdx.x == 0) defer[1 + atomicAdd(defer, 1)] = idx ? tix : base + blockIdx.x;
+        return;
+      }
+      // append the next columns behind the kept basis
+      for (int e = threadIdx.x; e < add * m; e += NT) {
+        const int c = e / m, i = e % m;
+        bu[cur][(int64_t)(r + c) * m + i] = U[(int64_t)(done + c) * d.ldu + i];
+      }
+      for (int e = threadIdx.x; e < add * n; e += NT) {
+        const int c = e / n, i = e % n;
+        bv[cur][(int64_t)(r + c) * n + i] = Vt[(int64_t)(done + c) * d.ldv + i];
+      }
+      __syncthreads();
+      done += add;
+      const bool last = done == k;
+      int sw = 0;
+      r = gram_stage(bu[cur], m, bv[cur], n, m, n, r + add, last ? Uo : bu[cur ^ 1], last ? Vo : bv[cur ^ 1],
+                     last ? d.cap : KG, tol, sc, overflow, S, sm, tc, &sw);
+      sweeps += sw;
+      cur ^= 1;
+    }
+  }
+  if (threadIdx.x == 0) {
     ranks[d.out_slot] = r;
     if (prof) {
       const long long tc4 = clock64();
-      atomicAdd(prof + 0, (unsigned long long)(tc1 - tc0));
-      atomicAdd(prof + 1, (unsigned long long)(tc2 - tc1));
-      atomicAdd(prof + 2, (unsigned long long)(tc3 - tc2));
-      atomicAdd(prof + 3, (unsigned long long)(tc4 - tc3));
+      atomicAdd(prof + 0, (unsigned long long)(tc[1] - tc[0]));
+      atomicAdd(prof + 1, (unsigned long long)(tc[2] - tc[1]));
+      atomicAdd(prof + 2, (unsigned long long)(tc[3] - tc[2]));
+      atomicAdd(prof + 3, (unsigned long long)(tc4 - tc[3]));
       atomicAdd(prof + 4, 1ull);
       atomicAdd(prof + 5, (unsigned long long)sweeps);
       atomicAdd(prof + 14, 1ull);
-      atomicAdd(prof + 15, (unsigned long long)(tc4 - tc0));
+      atomicAdd(prof + 15, (unsigned long long)(tc4 - tc[0]));
     }
   }
 }
 
 void launch_gram(zc* arena, zc* aout, int* ranks, const TruncDesc* d_desc, int nd, double tol,
                  unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, unsigned long long* prof,
-                 int* defer, const int* idx) {
-  const int64_t per = gram_scratch_per();
-  const int wave = (int)std::max<int64_t>(1, ((int64_t)2 << 30) / (per * (int64_t)sizeof(zc)));
+                 int* defer, const int* idx, int mn_max) {
+  // mn_max > 0: problems with KG < k <= KMS and max(m, n) <= mn_max run the multi-stage path
+  const int64_t per = gram_scratch_per() + (mn_max > 0 ? gram_ms_scratch(mn_max) : 0);
+  // one CTA per SM: a wave of one CTA per SM bounds the scratch
+  const int wave = (int)std::max<int64_t>(
+      1, std::min<int64_t>(148, ((int64_t)2 << 30) / (per * (int64_t)sizeof(zc))));
   const size_t need = (size_t)std::min(wave, nd) * per;
   if (scratch.n < need) scratch.alloc(need);
   const int smem = (3 * GSQ + KG + 1) * (int)sizeof(zc);
@@ -1123,7 +1181,7 @@ void launch_gram(zc* arena, zc* aout, int* ranks, const TruncDesc* d_desc, int n
   for (int b0 = 0; b0 < nd; b0 += wave) {
     const int nb = std::min(wave, nd - b0);
     k_trunc_gram<<<nb, NT, smem, s>>>(arena, aout, ranks, idx ? d_desc : d_desc + b0, scratch.p, per, tol,
-                                      overflow, prof, defer, b0, idx);
+                                      overflow, prof, defer, b0, idx, mn_max);
     CKL();
   }
 }
