@@ -206,6 +206,16 @@ int cbie_hlu_factor_dist(cbie_hmat* h, double trunc_tol, cbie_hlu** out);
  * NCCL) -- checks the ownership / transfer plan without several GPUs. */
 int cbie_hlu_factor_emulated(cbie_hmat* h, double trunc_tol, int world, cbie_hlu** out);
 
+/* Host only (no GPU): the distributed H-LU plan of the block structure of the
+ * points pts [npts][3] (leaf size n_leaf dofs, admissibility eta), low-rank
+ * capacities from an assumed rank min(m, n) / 8.  stats[11] = tasks, messages,
+ * transferred buffers, transferred complex elements, write conflicts (always 0:
+ * a conflict is an error), dependency levels, block-row tree level, fewest /
+ * most tasks of a rank, complex elements of the final factor broadcast,
+ * leaves; leaf_owner[nleaf] (may be NULL) = owning rank of every leaf. */
+int cbie_hlu_dist_plan_host(const double* pts, int64_t npts, int C, int n_leaf, double eta, int world,
+                            int64_t* stats, int32_t* leaf_owner);
+
 /* Timings (CUDA events), counts, flops, bytes as one JSON object.
  * which: 0 = context, 1 = hmatrix, 2 = hlu. */
 int cbie_stats_json(const void* handle, int which, char* buf, size_t cap);

@@ -514,8 +514,14 @@ static void hmatrix_build(cbie_hmat* H, int n_leaf) {
     if ((int64_t)staging.n < stoff) staging.alloc(std::max<int64_t>(stoff, 1));
     DBuf<TruncDesc> dtd;
     dtd.upload(td, s);
-    launch_truncate(scratch.p, H->rank.p, dtd.p, (int)td.size(), kmax_t, H->tol, ovf.p, tscratch, s,
-                    kcm, mnm, staging.p, TRUNC_NO_DENSE);
+    // factor-form recompression: Gram path (multi-stage up to rank 256) at tol >= 1e-5,
+    // like the H-LU (lowrank.cu launch_truncate_routed); Householder kernels otherwise
+    if (H->tol >= 1e-5 && getenv("CBIE_NO_GRAM") == nullptr)
+      launch_truncate_routed(scratch.p, H->rank.p, dtd.p, (int)td.size(), kmax_t, H->tol, ovf.p, tscratch, s, kcm,
+                             mnm, nullptr, nullptr, staging.p);
+    else
+      launch_truncate(scratch.p, H->rank.p, dtd.p, (int)td.size(), kmax_t, H->tol, ovf.p, tscratch, s,
+                      kcm, mnm, staging.p, TRUNC_NO_DENSE);
     std::vector<int> rk(nleaf);
     CK(cudaStreamSynchronize(s));   // ranks come from the (non-blocking) library stream
     CK(cudaMemcpy(rk.data(), H->rank.p, sizeof(int) * nleaf, cudaMemcpyDeviceToHost));

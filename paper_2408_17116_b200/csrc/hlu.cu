@@ -1905,6 +1905,61 @@ int cbie_hlu_factor_emulated(cbie_hmat* h, double trunc_tol, int world, cbie_hlu
   return hlu_factor_dist_entry(h, trunc_tol, world, true, out);
 }
 
+// host-only: the distributed plan of the block structure of pts (no GPU needed);
+// low-rank leaves get the factor capacity of an assumed rank min(m, n) / 8
+int cbie_hlu_dist_plan_host(const double* pts, int64_t npts, int C, int n_leaf, double eta, int world,
+                            int64_t* stats, int32_t* leaf_owner) {
+  try {
+    if (world < 1 || world > 64) throw cbie_error(CBIE_EINVALID, "world in [1, 64]");
+    cbie_hlu F;
+    Tree& T = F.tree;
+    T.build_clusters(pts, (int)npts, C, n_leaf);
+    T.build_blocks(eta);
+    const int nleaf = (int)T.leaves.size();
+    int64_t leaf_end = 0;
+    F.pivoff.assign(nleaf, -1);
+    for (int li = 0; li < nleaf; ++li) {
+      auto& L = T.leaves[li];
+      if (L.kind == BLK_DENSE) {
+        L.off_d = leaf_end;
+        leaf_end += (int64_t)L.m * L.n;
+        if (L.r == L.c) {
+          F.pivoff[li] = F.npiv;
+          F.npiv += L.m;
+        }
+      } else {
+        const int r = std::max(1, std::min(L.m, L.n) / 8);
+        L.cap = std::max(1, std::min(std::max(1, std::min(L.m, L.n) / 2), 2 * r + 48));
+        L.off_u = leaf_end;
+        leaf_end += (int64_t)L.m * L.cap;
+        L.off_v = leaf_end;
+        leaf_end += (int64_t)L.n * L.cap;
+      }
+    }
+    Recorder R;
+    hlu_record(&F, R, leaf_end, (int64_t)1 << 40, true);
+    DistPlan D;
+    dist_plan(R, F, world, D, nullptr, false);
+    int64_t fe = 0;
+    for (auto& m : D.final) fe += m.elems;
+    int64_t tmin = INT64_MAX, tmax = 0;
+    for (auto t : D.tasks_of) {
+      tmin = std::min(tmin, t);
+      tmax = std::max(tmax, t);
+    }
+    const int64_t st[11] = {(int64_t)R.tasks.size(), D.n_msgs, D.n_xfer, D.xfer_elems, D.conflicts,
+                            D.max_level, D.Ld, tmin, tmax, fe, nleaf};
+    if (stats) std::copy(st, st + 11, stats);
+    if (leaf_owner)
+      for (int li = 0; li < nleaf; ++li) leaf_owner[li] = D.leaf_owner[li];
+  } catch (const cbie_error& e) {
+    return e.code;
+  } catch (const std::exception&) {
+    return CBIE_EINVALID;
+  }
+  return CBIE_OK;
+}
+
 void cbie_hlu_destroy(cbie_hlu* f) { delete f; }
 
 int cbie_hlu_leaf(cbie_hlu* f, int64_t leaf, int* kind, int* rank, cbie_c128* D_or_U,

@@ -134,7 +134,7 @@ void add_buf_segs(const Recorder& R, const cbie_hlu& F, const std::vector<std::v
   for (int sl : slots_of[b]) push(1, sl, 1);
 }
 
-void dist_plan(const Recorder& R, const cbie_hlu& F, int W, DistPlan& D, cudaStream_t s) {
+void dist_plan(const Recorder& R, const cbie_hlu& F, int W, DistPlan& D, cudaStream_t s, bool upload = true) {
   const Tree& T = F.tree;
   const int nleaf = (int)T.leaves.size();
   const int nt = (int)R.tasks.size();
@@ -222,7 +222,7 @@ void dist_plan(const Recorder& R, const cbie_hlu& F, int W, DistPlan& D, cudaStr
     D.xfer_elems += m.elems;
     D.n_xfer += (int64_t)bs.size();
     ++D.n_msgs;
-    m.dsegs->upload(m.segs, s);
+    if (upload) m.dsegs->upload(m.segs, s);
     D.after[std::get<0>(kv.first)].push_back(std::move(m));
   }
   // 3. final: every owner broadcasts the leaves it wrote
@@ -230,7 +230,8 @@ void dist_plan(const Recorder& R, const cbie_hlu& F, int W, DistPlan& D, cudaStr
   for (int p = 0; p < W; ++p) D.final[p].src = p;
   for (int b = 0; b < nleaf; ++b)
     if (home[b] >= 0) add_buf_segs(R, F, slots_of, b, true, D.final[home[b]]);
-  for (auto& m : D.final) m.dsegs->upload(m.segs, s);
+  if (upload)
+    for (auto& m : D.final) m.dsegs->upload(m.segs, s);
 }
 
 void xfer_pack(const Msg& m, zc* arena, int* ranks, int* piv, double* rcond, zc* stage, bool unpack,

@@ -118,7 +118,8 @@ void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int
 // Gram kernel: a routing kernel splits the problems by their device-side rank first.
 void launch_truncate_routed(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
                             unsigned long long* overflow, TruncWork& work, cudaStream_t s, int kc_max,
-                            int mn_max, TruncWork* work2 = nullptr, cudaStream_t s2 = nullptr);
+                            int mn_max, TruncWork* work2 = nullptr, cudaStream_t s2 = nullptr,
+                            zc* arena_out = nullptr);
 void launch_truncate_gram(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, double tol,
                           unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, zc* arena_out,
                           int* defer, const int* idx = nullptr, int mn_multi = 0);

@@ -454,7 +454,7 @@ __global__ void k_route(const int* __restrict__ ranks, const TruncDesc* __restri
 // k <= 128 and max(m, n) <= 384 (its own hand-offs), unblocked for the rest
 static void householder_list(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
                              unsigned long long* overflow, TruncWork& w, cudaStream_t st, int kc_max, int mn_max,
-                             const int* list) {
+                             const int* list, zc* aout) {
   bool done = false;
   if (mn_max <= 384) {
     int* dfr = nullptr;
@@ -463,7 +463,7 @@ static void householder_list(zc* arena, int* ranks, const TruncDesc* d_desc, int
       dfr = w.defer.p;
       CK(cudaMemsetAsync(dfr, 0, sizeof(int), st));
     }
-    launch_truncate_blocked(arena, ranks, d_desc, nd, tol, overflow, w.scratch, st, kc_max, mn_max, arena, dfr,
+    launch_truncate_blocked(arena, ranks, d_desc, nd, tol, overflow, w.scratch, st, kc_max, mn_max, aout, dfr,
                             list);
     if (!dfr) done = true;
     else list = dfr;
@@ -474,7 +474,7 @@ static void householder_list(zc* arena, int* ranks, const TruncDesc* d_desc, int
                                           (int64_t)RLMAX * (4 * (int64_t)mn_max + kc_max + 1) +
                                               2 * (int64_t)RLMAX * RLMAX) +
                         4 * (int64_t)kmax;
-    launch_unblocked_list(arena, arena, ranks, d_desc, nd, kmax, per, tol, overflow, w, st, list);
+    launch_unblocked_list(arena, aout, ranks, d_desc, nd, kmax, per, tol, overflow, w, st, list);
   }
 }
 
@@ -483,12 +483,13 @@ static void householder_list(zc* arena, int* ranks, const TruncDesc* d_desc, int
 // kernels on the second stream, concurrently.
 void launch_truncate_routed(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
                             unsigned long long* overflow, TruncWork& work, cudaStream_t s, int kc_max,
-                            int mn_max, TruncWork* work2, cudaStream_t s2) {
+                            int mn_max, TruncWork* work2, cudaStream_t s2, zc* arena_out) {
   if (nd == 0) return;
+  zc* aout = arena_out ? arena_out : arena;
   const bool multi = getenv("CBIE_NO_MULTISTAGE") == nullptr;
   const int kg = multi ? 256 : 64;
   if (kc_max <= 64) {   // no capacity can exceed the single-stage Gram path
-    launch_truncate_gram(arena, ranks, d_desc, nd, tol, overflow, work.scratch, s, nullptr, nullptr);
+    launch_truncate_gram(arena, ranks, d_desc, nd, tol, overflow, work.scratch, s, aout, nullptr);
     return;
   }
   TruncWork& wb = work2 ? *work2 : work;
@@ -512,8 +513,8 @@ void launch_truncate_routed(zc* arena, int* ranks, const TruncDesc* d_desc, int 
   }
   if (kc_max > kg)
     householder_list(arena, ranks, d_desc, nd, kmax, tol, overflow, two ? wb : work, two ? sb : s, kc_max, mn_max,
-                     lb);
-  launch_truncate_gram(arena, ranks, d_desc, nd, tol, overflow, work.scratch, s, nullptr, multi ? lf : nullptr, la,
+                     lb, aout);
+  launch_truncate_gram(arena, ranks, d_desc, nd, tol, overflow, work.scratch, s, aout, multi ? lf : nullptr, la,
                        multi ? mn_max : 0);
   if (two) {
     CK(cudaEventRecord(join, sb));
@@ -523,7 +524,7 @@ void launch_truncate_routed(zc* arena, int* ranks, const TruncDesc* d_desc, int 
   }
   // multi-stage failures (kept rank filled the Gram capacity), after the join so that
   // they reuse the Householder workspaces of the second stream
-  if (multi) householder_list(arena, ranks, d_desc, nd, kmax, tol, overflow, wb, s, kc_max, mn_max, lf);
+  if (multi) householder_list(arena, ranks, d_desc, nd, kmax, tol, overflow, wb, s, kc_max, mn_max, lf, aout);
 }
 
 void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,

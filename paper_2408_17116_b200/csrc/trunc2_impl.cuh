@@ -640,7 +640,7 @@ __host__ __device__ inline int64_t gram_scratch_per() { return 4 * (int64_t)GSQ 
 __device__ void gram_acc(const zc* __restrict__ X, int m, int k, int ldx, zc* G, zc* Xs) {
   constexpr int PER = GCH * KG / NT;   // staged elements per thread
   const int tb = (k + 3) / 4, ntile = tb * (tb + 1) / 2;
-  const int groups = max(1, NT / ntile);
+  const int groups = max(1, min(8, NT / ntile));   // row groups, summed in a fixed order below
   const int g = threadIdx.x / ntile, t = threadIdx.x % ntile;
   const bool act = g < groups;
   int tj = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
@@ -692,23 +692,22 @@ __device__ void gram_acc(const zc* __restrict__ X, int m, int k, int ldx, zc* G,
       }
     }
   }
-  if (act)
+  // group partials added in group order (deterministic: bit-identical results for a
+  // problem whatever batch or launch it runs in)
+  for (int gg = 0; gg < groups; ++gg) {
+    if (act && g == gg)
 #pragma unroll
-    for (int qa = 0; qa < 4; ++qa)
+      for (int qa = 0; qa < 4; ++qa)
 #pragma unroll
-      for (int qb = 0; qb < 4; ++qb) {
-        const int a = a0 + qa, b = b0 + qb;
-        if (a >= k || b >= k || (ti == tj && a > b)) continue;
-        double* gp = reinterpret_cast<double*>(G + b * k + a);
-        atomicAdd(gp, ar[qa][qb]);
-        atomicAdd(gp + 1, ai[qa][qb]);
-        if (a != b) {   // mirror: G[b][a] = conj(G[a][b])
-          double* gq = reinterpret_cast<double*>(G + a * k + b);
-          atomicAdd(gq, ar[qa][qb]);
-          atomicAdd(gq + 1, -ai[qa][qb]);
+        for (int qb = 0; qb < 4; ++qb) {
+          const int a = a0 + qa, b = b0 + qb;
+          if (a >= k || b >= k || (ti == tj && a > b)) continue;
+          zc& gp = G[b * k + a];
+          gp = zmk(gp.x + ar[qa][qb], gp.y + ai[qa][qb]);
+          if (a != b) G[a * k + b] = zconj(gp);   // mirror: G[b][a] = conj(G[a][b])
         }
-      }
-  __syncthreads();
+    __syncthreads();
+  }
 }
 
 // pivoted Cholesky of the Hermitian G (k x k, ld k, shared) in place: row j < kk of G
@@ -1173,7 +1172,7 @@ void launch_gram(zc* arena, zc* aout, int* ranks, const TruncDesc* d_desc, int n
   const int64_t per = gram_scratch_per() + (mn_max > 0 ? gram_ms_scratch(mn_max) : 0);
   // one CTA per SM: a wave of one CTA per SM bounds the scratch
   const int wave = (int)std::max<int64_t>(
-      1, std::min<int64_t>(148, ((int64_t)2 << 30) / (per * (int64_t)sizeof(zc))));
+      1, std::min<int64_t>(148, ((int64_t)8 << 30) / (per * (int64_t)sizeof(zc))));
   const size_t need = (size_t)std::min(wave, nd) * per;
   if (scratch.n < need) scratch.alloc(need);
   const int smem = (3 * GSQ + KG + 1) * (int)sizeof(zc);

@@ -48,3 +48,18 @@ def hlu_factor_distributed(H, tol: float):
     same complete H-matrix and gets the complete factors back."""
     from .hmatrix import HLUFactors
     return HLUFactors(H, tol, distributed=True)
+
+
+def hlu_dist_plan(points, C: int, n_leaf: int, eta: float, world: int):
+    """Host-only distributed H-LU plan of the block structure of `points` (no GPU):
+    (stats dict, leaf owner array) -- cbie_hlu_dist_plan_host."""
+    lib = _ffi.load()
+    pts = np.ascontiguousarray(np.asarray(points, dtype=np.float64))
+    st = np.zeros(11, np.int64)
+    args = (_ffi.ptr(pts), int(pts.shape[0]), int(C), int(n_leaf), float(eta), int(world), _ffi.ptr(st))
+    _ffi.check(lib.cbie_hlu_dist_plan_host(*args, None))
+    owner = np.full(int(st[10]), -1, np.int32)
+    _ffi.check(lib.cbie_hlu_dist_plan_host(*args, _ffi.ptr(owner)))
+    keys = ("tasks", "messages", "xfer_buffers", "xfer_elems", "conflicts", "levels", "row_level",
+            "tasks_min", "tasks_max", "final_elems", "leaves")
+    return dict(zip(keys, (int(v) for v in st))), owner

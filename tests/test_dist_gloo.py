@@ -125,3 +125,63 @@ def test_lpt_partition_covers_every_leaf_once():
         loads = np.bincount(owner, weights=cost, minlength=world)
         assert loads.max() <= cost.sum() / world + cost.max()
         assert np.array_equal(owner, cdist.partition_lpt(cost, world))   # deterministic
+
+
+def _sphere_points(n=864, seed=3):
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    p = rng.standard_normal((n, 3))
+    return p / np.linalg.norm(p, axis=1)[:, None]
+
+
+def _hlu_plan_worker(rank, world, port, q):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2408_17116_b200 import dist as cdist
+    st, owner = cdist.hlu_dist_plan(_sphere_points(), 2, 64, 1.0, world)
+    # every rank derives the same plan from the same structure (no negotiation needed)
+    t = torch.tensor(owner.astype(np.int64))
+    ts = [torch.zeros_like(t) for _ in range(world)]
+    dist.all_gather(ts, t)
+    same = all(torch.equal(ts[0], x) for x in ts)
+    q.put((rank, st, owner.tolist(), same))
+    dist.barrier()
+    dist.destroy_process_group()
+
+
+def test_two_rank_distributed_hlu_plan():
+    """Block-row-distributed H-LU plan (hlu_dist.cuh) on 2 gloo ranks, host only: both
+    ranks derive the identical leaf ownership, every rank owns leaves and tasks,
+    no buffer has two writer ranks, and factored blocks cross ranks between levels."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    ps = [ctx.Process(target=_hlu_plan_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in ps:
+        p.start()
+    out = sorted(q.get(timeout=300) for _ in ps)
+    for p in ps:
+        p.join(timeout=60)
+    (_, st0, own0, same0), (_, st1, own1, same1) = out
+    assert same0 and same1 and own0 == own1 and st0 == st1
+    assert st0["conflicts"] == 0
+    assert set(own0) == {0, 1}
+    assert st0["tasks_min"] > 0 and st0["messages"] > 0 and st0["xfer_elems"] > 0
+    assert st0["final_elems"] > 0
+
+
+def test_distributed_hlu_plan_world_sizes():
+    """World 1 needs no transfers; more ranks spread the tasks (max share shrinks)."""
+    from paper_2408_17116_b200 import dist as cdist
+    pts = _sphere_points()
+    s1, o1 = cdist.hlu_dist_plan(pts, 2, 64, 1.0, 1)
+    assert s1["messages"] == 0 and s1["xfer_elems"] == 0 and set(o1.tolist()) == {0}
+    s4, o4 = cdist.hlu_dist_plan(pts, 2, 64, 1.0, 4)
+    assert set(o4.tolist()) == {0, 1, 2, 3}
+    assert s4["tasks"] == s1["tasks"]                     # same tape, split over ranks
+    assert s4["tasks_max"] < s1["tasks_max"]
+    assert s4["conflicts"] == 0

@@ -22,4 +22,4 @@ for it in range(int(sys.argv[2]) if len(sys.argv) > 2 else 6):
     t4 = time.perf_counter()
     print(f"step {it}: classify {1e3*(tc-t0):.1f} del {1e3*(t4-t3):.1f} fill_wall {1e3*(t1-t0):.1f} hlu_wall {1e3*(t2-t1):.1f} device {st['factor_device_ms']:.1f} "
           f"enqueue {st.get('host_enqueue_ms', 0):.1f} frees {st.get('frees_during_run', 0):.0f} "
-          f"cached {st.get('plan_cached')}", flush=True)
+          f"cached {st.get('plan_cached')} trunc_ms {st.get('trunc_kernel_ms', 0):.1f}", flush=True)
