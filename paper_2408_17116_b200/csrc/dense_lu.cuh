@@ -124,6 +124,7 @@ __device__ __forceinline__ double lu_block_sum(double v, double* red) {
   return t;
 }
 // CTA argmax (first index among equal values); returns the index, all threads
+template <int NWARP = LU_NW>
 __device__ __forceinline__ int lu_block_argmax(double bv, int bi, double* sv, int* si) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -143,7 +144,7 @@ __device__ __forceinline__ int lu_block_argmax(double bv, int bi, double* sv, in
   double B = sv[0];
   int I = si[0];
 #pragma unroll
-  for (int w = 1; w < LU_NW; ++w)
+  for (int w = 1; w < NWARP; ++w)
     if (sv[w] > B || (sv[w] == B && si[w] < I)) {
       B = sv[w];
       I = si[w];
@@ -155,7 +156,14 @@ __device__ __forceinline__ int lu_block_argmax(double bv, int bi, double* sv, in
 // GETRF + rcond, one 512-thread CTA per diagonal leaf, n <= LU_NMAX
 // dynamic shared memory: n * LU_NB complex (panel, later the estimator vector)
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(LU_NT) k_getrf_blk(zc* __restrict__ ar, int* __restrict__ pivs,
+constexpr int GF_NT = 512;   // getrf threads (more loads in flight in the global-memory phases)
+constexpr int GF_NW = GF_NT / 32;
+
+__device__ __forceinline__ zc zshfl32(zc v, int src) {
+  return zmk(__shfl_sync(0xffffffffu, v.x, src), __shfl_sync(0xffffffffu, v.y, src));
+}
+
+__global__ void __launch_bounds__(GF_NT) k_getrf_blk(zc* __restrict__ ar, int* __restrict__ pivs,
                                                      const GetrfD* __restrict__ ds, double* anorm_out) {
   const GetrfD d = ds[blockIdx.x];
   const int n = d.n;
@@ -164,8 +172,8 @@ __global__ void __launch_bounds__(LU_NT) k_getrf_blk(zc* __restrict__ ar, int* _
   if (threadIdx.x == 0) flop_add(8.0 * n * (double)n * n / 3.0);
   extern __shared__ __align__(16) unsigned char smem_raw[];
   zc* P = reinterpret_cast<zc*>(smem_raw);   // panel, column c at P[c * n + i] (absolute rows)
-  __shared__ double sv[LU_NW], red[LU_NW];
-  __shared__ int si[LU_NW];
+  __shared__ double sv[GF_NW], red[GF_NW];
+  __shared__ int si[GF_NW];
   __shared__ int spiv[LU_NB];
   __shared__ int trow[2 * LU_NB], tsrc[2 * LU_NB];
   __shared__ int ntouch;
@@ -175,7 +183,7 @@ __global__ void __launch_bounds__(LU_NT) k_getrf_blk(zc* __restrict__ ar, int* _
   {
     const int lane = tid & 31, w = tid >> 5;
     double loc = 0.0;
-    for (int j = w; j < n; j += LU_NW) {   // warp per column, coalesced
+    for (int j = w; j < n; j += GF_NW) {   // warp per column, coalesced
       double s = 0.0;
       for (int i = lane; i < n; i += 32) {
         const zc a = A[(int64_t)j * n + i];
@@ -185,7 +193,7 @@ __global__ void __launch_bounds__(LU_NT) k_getrf_blk(zc* __restrict__ ar, int* _
     }
     if (lane == 0) red[w] = loc;
     __syncthreads();
-    for (int q = 0; q < LU_NW; ++q) anorm = fmax(anorm, red[q]);
+    for (int q = 0; q < GF_NW; ++q) anorm = fmax(anorm, red[q]);
     __syncthreads();
   }
 
@@ -194,7 +202,7 @@ __global__ void __launch_bounds__(LU_NT) k_getrf_blk(zc* __restrict__ ar, int* _
   (void)zero_pivot;
   for (int j0 = 0; j0 < n; j0 += LU_NB) {
     const int jb = min(LU_NB, n - j0);
-    for (int e = tid; e < jb * (n - j0); e += LU_NT) {
+    for (int e = tid; e < jb * (n - j0); e += GF_NT) {
       const int c = e / (n - j0), i = j0 + e % (n - j0);
       P[c * n + i] = A[(int64_t)(j0 + c) * n + i];
     }
@@ -204,7 +212,7 @@ __global__ void __launch_bounds__(LU_NT) k_getrf_blk(zc* __restrict__ ar, int* _
       const int col = j0 + c;
       double bv = -1.0;
       int bi = 0x7fffffff;
-      for (int i = col + tid; i < n; i += LU_NT) {
+      for (int i = col + tid; i < n; i += GF_NT) {
         const zc a = P[c * n + i];
         const double v = fabs(a.x) + fabs(a.y);
         if (v > bv) {
@@ -212,7 +220,7 @@ __global__ void __launch_bounds__(LU_NT) k_getrf_blk(zc* __restrict__ ar, int* _
           bi = i;
         }
       }
-      const int pr = lu_block_argmax(bv, bi, sv, si);
+      const int pr = lu_block_argmax<GF_NW>(bv, bi, sv, si);
       if (tid == 0) {
         spiv[c] = pr;
         piv[col] = pr;
@@ -230,7 +238,7 @@ __global__ void __launch_bounds__(LU_NT) k_getrf_blk(zc* __restrict__ ar, int* _
         continue;
       }
       const zc rinv = zdiv(zmk(1.0, 0.0), ajj);
-      for (int i = col + 1 + tid; i < n; i += LU_NT) {
+      for (int i = col + 1 + tid; i < n; i += GF_NT) {
         const zc l = zmul(P[c * n + i], rinv);
         P[c * n + i] = l;
         for (int cc = c + 1; cc < jb; ++cc) P[cc * n + i] = zsub(P[cc * n + i], zmul(l, P[cc * n + col]));
@@ -238,7 +246,7 @@ __global__ void __launch_bounds__(LU_NT) k_getrf_blk(zc* __restrict__ ar, int* _
       __syncthreads();
     }
     // --- write the panel back ---
-    for (int e = tid; e < jb * (n - j0); e += LU_NT) {
+    for (int e = tid; e < jb * (n - j0); e += GF_NT) {
       const int c = e / (n - j0), i = j0 + e % (n - j0);
       A[(int64_t)(j0 + c) * n + i] = P[c * n + i];
     }
@@ -275,7 +283,7 @@ __global__ void __launch_bounds__(LU_NT) k_getrf_blk(zc* __restrict__ ar, int* _
       // column land in registers before its writes)
       const int nt = ntouch, lane = tid & 31, w = tid >> 5;
       const int nq = n - jb;
-      for (int q0 = 4 * w; q0 < nq; q0 += 4 * LU_NW) {
+      for (int q0 = 4 * w; q0 < nq; q0 += 4 * GF_NW) {
         zc v[4][2];
 #pragma unroll
         for (int a = 0; a < 4; ++a) {
@@ -303,37 +311,42 @@ __global__ void __launch_bounds__(LU_NT) k_getrf_blk(zc* __restrict__ ar, int* _
     __syncthreads();
     const int j1 = j0 + jb;
     if (j1 >= n) break;
-    // --- U12 = L11^{-1} A12 (thread per column, unit lower L11 from the panel) ---
-    for (int q = j1 + tid; q < n; q += LU_NT) {
-      zc* colp = A + (int64_t)q * n + j0;
-      zc u[LU_NB];
-#pragma unroll
-      for (int r = 0; r < LU_NB; ++r) u[r] = r < jb ? colp[r] : zmk(0.0, 0.0);
-#pragma unroll
-      for (int c = 0; c < LU_NB; ++c)
-#pragma unroll
-        for (int r = c + 1; r < LU_NB; ++r)
-          if (r < jb) u[r] = zsub(u[r], zmul(P[c * n + j0 + r], u[c]));
-#pragma unroll
-      for (int r = 0; r < LU_NB; ++r)
-        if (r < jb) colp[r] = u[r];
-    }
-    __syncthreads();
-    // --- A22 -= L21 U12: L21 from the panel, U12 staged in column chunks of
-    //     LU_QC columns; 2 x 2 register tiles ---
+    // --- per chunk of LU_QC columns: U12 = L11^{-1} A12 (a warp per 4 columns, lanes =
+    //     rows of the unit lower L11 from the panel, shuffle substitution), written to A
+    //     and to shared memory; then A22 -= L21 U12 with 2 x 2 register tiles ---
     {
       zc* Us = P + (size_t)n * LU_NB;   // [LU_QC][LU_NB]
       const int m2 = n - j1;
       const int tr = (m2 + 1) / 2;
+      const int lane = tid & 31, w = tid >> 5;
       for (int q0 = j1; q0 < n; q0 += LU_QC) {
         const int qc = min(LU_QC, n - q0);
-        for (int e = tid; e < qc * jb; e += LU_NT) {
-          const int q = e / jb, c = e % jb;
-          Us[q * LU_NB + c] = A[(int64_t)(q0 + q) * n + j0 + c];
+        for (int c4 = 4 * w; c4 < qc; c4 += 4 * GF_NW) {
+          zc x[4];
+#pragma unroll
+          for (int h = 0; h < 4; ++h)
+            x[h] = (c4 + h < qc && lane < jb) ? A[(int64_t)(q0 + c4 + h) * n + j0 + lane] : zmk(0.0, 0.0);
+#pragma unroll 4
+          for (int c = 0; c < LU_NB; ++c) {
+            if (c < jb) {
+              const zc l = lane > c && lane < jb ? P[c * n + j0 + lane] : zmk(0.0, 0.0);
+#pragma unroll
+              for (int h = 0; h < 4; ++h) {
+                const zc xc = zshfl32(x[h], c);
+                x[h] = zsub(x[h], zmul(l, xc));
+              }
+            }
+          }
+#pragma unroll
+          for (int h = 0; h < 4; ++h)
+            if (c4 + h < qc && lane < jb) {
+              A[(int64_t)(q0 + c4 + h) * n + j0 + lane] = x[h];
+              Us[(c4 + h) * LU_NB + lane] = x[h];
+            }
         }
         __syncthreads();
         const int tq = (qc + 1) / 2, ntile = tr * tq;
-        for (int tix = tid; tix < ntile; tix += LU_NT) {
+        for (int tix = tid; tix < ntile; tix += GF_NT) {
           const int i = j1 + 2 * (tix % tr), ql = 2 * (tix / tr);
           const bool i1 = i + 1 < n, q1 = ql + 1 < qc;
           zc a00 = zmk(0, 0), a01 = zmk(0, 0), a10 = zmk(0, 0), a11 = zmk(0, 0);

@@ -1110,6 +1110,10 @@ struct Plan {
   DBuf<DenseLRDesc> ddl;
   size_t trsm_smem = 0, getrf_smem = 0;
   int maxn_lu = 0;   // largest diagonal leaf (getrf / trsm)
+  // executor scratch kept with the plan: no cudaMalloc / cudaFree (device-wide sync)
+  // while a cached plan runs
+  DBuf<zc> dlr_scratch;
+  DBuf<double> anorm;
 };
 
 // owner != nullptr: only the tasks with owner[i] == me (block-row-distributed H-LU)
@@ -1273,7 +1277,7 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
   auto& df = P.df;
   auto& dtr = P.dtr;
   auto& ddl = P.ddl;
-  DBuf<zc> dlr_scratch;
+  DBuf<zc>& dlr_scratch = P.dlr_scratch;
   const size_t trsm_smem = P.trsm_smem, getrf_smem = P.getrf_smem;
   CK(cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem));
   // blocked diagonal-leaf kernels (dense_lu.cuh) unless a leaf exceeds LU_NMAX
@@ -1283,7 +1287,7 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
   // rcond estimates run on a side stream (nothing downstream consumes them)
   cudaStream_t s3 = nullptr;
   cudaEvent_t rc_ev = nullptr;
-  DBuf<double> anorm;
+  DBuf<double>& anorm = P.anorm;
   if (blk_lu) {
     CK(cudaFuncSetAttribute(k_trsm_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_blk_smem));
     CK(cudaFuncSetAttribute(k_getrf_blk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)blk_smem));
@@ -1291,7 +1295,7 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
     CK(cudaEventCreateWithFlags(&rc_ev, cudaEventDisableTiming));
     int nl = 1;
     for (auto& x : P.f) nl = std::max(nl, x.leaf + 1);
-    anorm.alloc(nl);
+    if ((int)anorm.n < nl) anorm.alloc(nl);
   }
   int lvl = -1;
   const bool prof = getenv("CBIE_PROFILE") != nullptr;
@@ -1387,7 +1391,7 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
       }
       case OP_GETRF:
         if (blk_lu) {
-          k_getrf_blk<<<gr.count, LU_NT, blk_smem, s>>>(arena, piv, df.p + gr.start, anorm.p);
+          k_getrf_blk<<<gr.count, GF_NT, blk_smem, s>>>(arena, piv, df.p + gr.start, anorm.p);
           CK(cudaEventRecord(rc_ev, s));
           CK(cudaStreamWaitEvent(s3, rc_ev, 0));
           k_rcond_blk<<<gr.count, LU_NT, (size_t)P.maxn_lu * sizeof(zc), s3>>>(arena, piv, df.p + gr.start,
