@@ -1126,7 +1126,9 @@ __global__ void __launch_bounds__(NT, 1)
     r = gram_stage(U, d.ldu, Vt, d.ldv, m, n, KG, bu[0], bv[0], KG, tol, sc, overflow, S, sm, tc, &sweeps);
     while (done < k) {
       const int add = min(KG - r, k - done);
-      if (add <= 0) {   // no room left: Householder kernels (nothing written to the output yet)
+      // too little room left for the remaining columns (each stage costs a full Gram
+      // recompression): Householder kernels -- nothing was written to the output yet
+      if (add < min(16, k - done)) {
         if (threadIdx.x == 0) defer[1 + atomicAdd(defer, 1)] = idx ? tix : base + blockIdx.x;
         return;
       }
