@@ -313,6 +313,7 @@ def run_gpu(args):
             del H2, gen2, F2
         e_ms = _reduce_max(statistics.median(t_e2e), world)
         e2e = {"value": world * N / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
+               "iter_ms": [round(t, 2) for t in t_e2e],
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "api": "solver.build_hmatrix + hmatrix.hlu_factor + HLUFactors.solve (host arrays)"}
 

@@ -80,6 +80,13 @@ def load(path: str | None = None):
         if not os.path.exists(p):
             raise errors.NativeUnavailable(
                 f"{p} not built; run paper_2408_17116_b200.build.build() (no CPU fallback)")
+        # torch (plumbing for streams / torch.distributed) bundles a newer NCCL under
+        # the same soname; load it first so libcbie binds to that one and a later
+        # `import torch` does not resolve its NCCL symbols against an older library
+        try:
+            import torch  # noqa: F401
+        except ImportError:
+            pass
         lib = ct.CDLL(p)
         for name, (res, args) in _SIGS.items():
             f = getattr(lib, name)

@@ -352,7 +352,7 @@ static void hmatrix_build(cbie_hmat* H, int n_leaf) {
     if (L.kind == BLK_LR) lr_bound += (int64_t)(L.m + L.n) * std::min(aca_budget(L.m, L.n), 128);
   {
     size_t fr = 0, tot = 0;
-    cudaMemGetInfo(&fr, &tot);
+    fr = mem_free_bytes(&tot);
     const int64_t avail = (int64_t)(0.5 * ((double)fr - (double)used * sizeof(zc))) / (int64_t)sizeof(zc);
     const int64_t lr_alloc = std::max<int64_t>(std::min(lr_bound, avail), 1 << 20);
     H->arena.alloc(std::max<int64_t>(used + lr_alloc, 1));

@@ -151,6 +151,17 @@ extern std::atomic<long long> g_cbie_frees;   // cudaFree calls (each one synchr
     CK(cudaGetLastError());   \
   } while (0)
 
+// Device allocations come from the device's default stream-ordered memory pool with
+// an unbounded release threshold: freed blocks stay mapped and are handed out again,
+// so repeated fills / factorisations never unmap memory (cudaFree of large blocks
+// stalled concurrently running kernels by up to 2x).  Allocation is ordered on a
+// private stream and completed before use; release keeps cudaFree's semantics
+// (device-wide synchronisation first).  mem_free_bytes() counts pool-held blocks.
+cudaStream_t cbie_alloc_stream();
+size_t mem_free_bytes(size_t* total = nullptr);
+cudaError_t cbie_malloc(void** p, size_t bytes);
+void cbie_free(void* p);
+
 template <class T>
 struct DBuf {
   T* p = nullptr;
@@ -161,7 +172,7 @@ struct DBuf {
   ~DBuf() { release(); }
   void release() {
     if (p) {
-      cudaFree(p);
+      cbie_free(p);
       ++g_cbie_frees;
     }
     p = nullptr;
@@ -171,12 +182,11 @@ struct DBuf {
     if (count == n && p) return;
     release();
     if (count == 0) return;
-    cudaError_t e = cudaMalloc(&p, count * sizeof(T));
+    cudaError_t e = cbie_malloc(reinterpret_cast<void**>(&p), count * sizeof(T));
     if (e != cudaSuccess) {
       p = nullptr;
       cudaGetLastError();
-      size_t fr = 0, tot = 0;
-      cudaMemGetInfo(&fr, &tot);
+      const size_t fr = mem_free_bytes();
       throw cbie_error(e == cudaErrorMemoryAllocation ? CBIE_EOOM : CBIE_ECUDA,
                        std::string("cudaMalloc of ") + std::to_string(count * sizeof(T) >> 20) +
                            " MiB failed (" + cudaGetErrorString(e) + "; free " +

@@ -4,6 +4,8 @@
 // chebyshev.py:32-108 (Fejer-1 rule, transform tables).
 #include <cmath>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <sstream>
 
 #include "context.h"
@@ -258,6 +260,60 @@ void ctx_set_formulation(cbie_ctx* c, int kind, double omega, zc k1, zc k2, zc e
 
 std::atomic<long long> g_cbie_launches{0};
 std::atomic<long long> g_cbie_frees{0};
+
+namespace {
+struct PoolState {
+  cudaStream_t st = nullptr;
+  cudaMemPool_t pool = nullptr;
+};
+PoolState& pool_state() {
+  // never destroyed: buffers held by static objects are released during exit
+  static std::mutex* mu = new std::mutex;
+  static std::map<int, PoolState>* m = new std::map<int, PoolState>;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(*mu);
+  PoolState& P = (*m)[dev];
+  if (!P.st) {
+    cudaStreamCreateWithFlags(&P.st, cudaStreamNonBlocking);
+    cudaDeviceGetDefaultMemPool(&P.pool, dev);
+    uint64_t thr = UINT64_MAX;
+    cudaMemPoolSetAttribute(P.pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  return P;
+}
+}  // namespace
+
+cudaStream_t cbie_alloc_stream() { return pool_state().st; }
+
+size_t mem_free_bytes(size_t* total) {
+  size_t fr = 0, tot = 0;
+  cudaMemGetInfo(&fr, &tot);
+  PoolState& P = pool_state();
+  uint64_t res = 0, used = 0;
+  cudaMemPoolGetAttribute(P.pool, cudaMemPoolAttrReservedMemCurrent, &res);
+  cudaMemPoolGetAttribute(P.pool, cudaMemPoolAttrUsedMemCurrent, &used);
+  if (total) *total = tot;
+  return fr + (res > used ? (size_t)(res - used) : 0);
+}
+
+cudaError_t cbie_malloc(void** p, size_t bytes) {
+  PoolState& P = pool_state();
+  cudaError_t e = cudaMallocAsync(p, bytes, P.st);
+  if (e == cudaErrorMemoryAllocation) {   // blocks held by the pool of other sizes: give them back, retry
+    cudaGetLastError();
+    cudaDeviceSynchronize();
+    cudaMemPoolTrimTo(P.pool, 0);
+    e = cudaMallocAsync(p, bytes, P.st);
+  }
+  if (e != cudaSuccess) return e;
+  return cudaStreamSynchronize(P.st);
+}
+
+void cbie_free(void* p) {
+  cudaDeviceSynchronize();   // cudaFree semantics: no kernel may still use the block
+  cudaFreeAsync(p, pool_state().st);
+}
 
 // ---------------------------------------------------------------------------
 // C-ABI

@@ -1562,7 +1562,7 @@ uint64_t fnv(uint64_t h, int64_t v) {
 void hlu_trim_cache(bool force) {
   if (!g_plan_cache) return;
   size_t fr = 0, tot = 0;
-  cudaMemGetInfo(&fr, &tot);
+  fr = mem_free_bytes(&tot);
   // keep the plan (small); release the workspace only when HBM runs short
   if (force || (double)fr < 0.25 * (double)tot) {
     g_plan_cache->work.release();
@@ -1619,7 +1619,7 @@ static int64_t hlu_layout(cbie_hlu* F, std::vector<CopySeg>& segs) {
 // parallelism; the rest is left to the recompression workspaces), shared by `share` arenas on this device; CBIE_POOL_GB overrides
 static int64_t hlu_pool_budget(int64_t leaf_end, int share) {
   size_t fr = 0, tot = 0;
-  cudaMemGetInfo(&fr, &tot);
+  fr = mem_free_bytes(&tot);
   double gb = 0.6 * ((double)fr / share - 2.0 * (double)leaf_end * sizeof(zc)) / (double)(1ll << 30) - 4.0;
   gb = std::max(4.0, std::min(gb, 120.0));
   if (getenv("CBIE_POOL_GB")) gb = atof(getenv("CBIE_POOL_GB"));
@@ -1797,12 +1797,26 @@ static void hlu_factor_impl(cbie_hlu* F) {
 
 #include "hlu_dist.cuh"
 
+// the triangular-solve tape of one factor layout + nrhs, recorded once and reused
+// (every solve of the same mesh: bench steps, multiple right-hand sides)
+struct SolveCache {
+  uint64_t key = 0;
+  Plan plan;
+  int64_t pool_top = 0, xoff = 0;
+  DBuf<int> ranks, flag;
+  DBuf<double> rc;
+  DBuf<unsigned long long> ovf;
+  TruncWork tw[2 * TRUNC_LANES];
+};
+std::unique_ptr<SolveCache> g_solve_cache;
+
 static void hlu_solve_impl(cbie_hlu* F, const zc* b, zc* x, int nrhs) {
   cbie_hmat* H = F->H;
   cudaStream_t s = H->ctx->stream;
   const Tree& T = F->tree;
   const int64_t N = H->N;
   const int C = T.C;
+  const int nleaf = (int)T.leaves.size();
   // permuted right-hand sides, column-major N x nrhs
   std::vector<zc> bp((size_t)N * nrhs);
   for (size_t p = 0; p < T.pperm.size(); ++p)
@@ -1810,22 +1824,44 @@ static void hlu_solve_impl(cbie_hlu* F, const zc* b, zc* x, int nrhs) {
       const int64_t ni = (int64_t)p * C + c, oi = (int64_t)T.pperm[p] * C + c;
       for (int r = 0; r < nrhs; ++r) bp[(size_t)r * N + ni] = b[(size_t)oi * nrhs + r];
     }
-  Recorder R;
-  R.leaf_end = F->leaf_end;
-  R.pool_budget = (int64_t)1 << 40;
-  const int nleaf = (int)T.leaves.size();
+  uint64_t key = 1469598103934665603ull;
+  key = fnv(key, nleaf);
+  key = fnv(key, nrhs);
+  key = fnv(key, F->leaf_end);
   for (int li = 0; li < nleaf; ++li) {
-    R.new_buf();
-    R.new_slot(0, li);
+    const auto& L = T.leaves[li];
+    key = fnv(key, L.kind * 1000003ll + L.m * 1009ll + L.n);
+    key = fnv(key, L.cap * 7919ll + (L.kind == BLK_DENSE ? L.off_d : L.off_u));
+    key = fnv(key, F->pivoff[li]);
   }
-  // the rank slots of the factors live in F->ranks (same leaf slot numbering)
-  std::vector<Recorder::Tmp> own;
-  Mat X = R.tmp_mat((int)N, nrhs, -1, -1, own);
-  Builder Bd(R, *F);
-  Bd.lsolve(T.root_node, X);
-  Bd.usolve(T.root_node, X);
+  if (!(g_solve_cache && g_solve_cache->key == key)) {
+    g_solve_cache.reset();
+    auto sc = std::make_unique<SolveCache>();
+    Recorder& R = sc->plan.R;
+    R.leaf_end = F->leaf_end;
+    R.pool_budget = (int64_t)1 << 40;
+    for (int li = 0; li < nleaf; ++li) {
+      R.new_buf();
+      R.new_slot(0, li);
+    }
+    // the rank slots of the factors live in F->ranks (same leaf slot numbering)
+    std::vector<Recorder::Tmp> own;
+    Mat X = R.tmp_mat((int)N, nrhs, -1, -1, own);
+    Builder Bd(R, *F);
+    Bd.lsolve(T.root_node, X);
+    Bd.usolve(T.root_node, X);
+    make_plan(sc->plan, s);
+    sc->pool_top = R.pool_top;
+    sc->xoff = X.off;
+    sc->flag.alloc(1);
+    sc->rc.alloc(1);
+    sc->ovf.alloc(1);
+    sc->key = key;
+    g_solve_cache = std::move(sc);
+  }
+  SolveCache& SC = *g_solve_cache;
   // arena for the solve: factors (shared) + temps: allocate temps after the factor arena
-  const int64_t need = F->leaf_end + R.pool_top + 1;
+  const int64_t need = F->leaf_end + SC.pool_top + 1;
   if ((int64_t)F->arena.n < need) {
     DBuf<zc> bigger;
     bigger.alloc(need);
@@ -1833,25 +1869,16 @@ static void hlu_solve_impl(cbie_hlu* F, const zc* b, zc* x, int nrhs) {
     std::swap(bigger.p, F->arena.p);
     std::swap(bigger.n, F->arena.n);
   }
-  CK(cudaMemcpyAsync(F->arena.p + X.off, bp.data(), sizeof(zc) * bp.size(), cudaMemcpyHostToDevice, s));
-  // slots: leaves keep their factor ranks; extra slots (none expected) appended
-  DBuf<int> ranks;
-  std::vector<int> r0 = R.init_ranks;
-  {
-    std::vector<int> fr(nleaf);
-    CK(cudaMemcpy(fr.data(), F->ranks.p, sizeof(int) * nleaf, cudaMemcpyDeviceToHost));
-    for (int li = 0; li < nleaf; ++li) r0[li] = fr[li];
-  }
-  ranks.upload(r0, s);
-  DBuf<int> flag;
-  flag.alloc(1);
-  DBuf<double> rc;
-  rc.alloc(1);
-  DBuf<unsigned long long> ovf;
-  ovf.alloc(1);
-  TruncWork tw[2 * TRUNC_LANES];
-  execute(R, F->arena.p, ranks.p, F->piv.p, rc.p, flag.p, ovf.p, tw, F->tol, s);
-  CK(cudaMemcpy(bp.data(), F->arena.p + X.off, sizeof(zc) * bp.size(), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpyAsync(F->arena.p + SC.xoff, bp.data(), sizeof(zc) * bp.size(), cudaMemcpyHostToDevice, s));
+  // slots: leaves keep their factor ranks (device to device), the solve's own after them
+  std::vector<int> r0 = SC.plan.R.init_ranks;
+  if ((int64_t)SC.ranks.n != (int64_t)r0.size()) SC.ranks.alloc(r0.size());
+  if (r0.size() > (size_t)nleaf)
+    CK(cudaMemcpyAsync(SC.ranks.p + nleaf, r0.data() + nleaf, sizeof(int) * (r0.size() - nleaf),
+                       cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(SC.ranks.p, F->ranks.p, sizeof(int) * nleaf, cudaMemcpyDeviceToDevice, s));
+  run_plan(SC.plan, F->arena.p, SC.ranks.p, F->piv.p, SC.rc.p, SC.flag.p, SC.ovf.p, SC.tw, F->tol, s);
+  CK(cudaMemcpy(bp.data(), F->arena.p + SC.xoff, sizeof(zc) * bp.size(), cudaMemcpyDeviceToHost));
   for (size_t p = 0; p < T.pperm.size(); ++p)
     for (int c = 0; c < C; ++c) {
       const int64_t ni = (int64_t)p * C + c, oi = (int64_t)T.pperm[p] * C + c;

@@ -20,6 +20,7 @@ def declared():
 def lib():
     from paper_2408_17116_b200 import build
     build.build()
+    import torch  # noqa: F401  (torch's NCCL first, as _ffi.load does)
     return ctypes.CDLL(LIB)
 
 
