@@ -294,7 +294,7 @@ def run_gpu(args):
         import dataclasses
         t_e2e = []
         h2d = d2h = 0
-        for it in range(max(1, min(args.steps, 2)) + 1):
+        for it in range(max(3, min(args.steps, 5)) + 1):   # first iteration: one-off setup, not timed
             torch.cuda.synchronize()
             a = torch.cuda.Event(enable_timing=True)
             b = torch.cuda.Event(enable_timing=True)

@@ -136,6 +136,13 @@ int cbie_hmatrix_leaf(cbie_hmat* h, int64_t leaf, int* kind, int* rank, cbie_c12
  * HMatrix.matvec (hmatrix.py:267-274). */
 int cbie_hmatvec(cbie_hmat* h, const cbie_c128* x, cbie_c128* y, int nrhs);
 
+/* Restarted GMRES on the device H-matvec (gmres / solve_gmres, solver.py:206-307):
+ * zero initial guess, restart length `restart`, one re-orthogonalisation pass,
+ * complex Givens rotations; b, x [N] in original dof order.  *iterations = inner
+ * iterations, *rel_residual = |b - H x| / |b|, *converged = 0 / 1. */
+int cbie_gmres(cbie_hmat* h, const cbie_c128* b, double tol, int restart, int max_iters, cbie_c128* x,
+               int* iterations, double* rel_residual, int* converged);
+
 /* H-LU of the H-matrix (copy; h unchanged).  hlu_factor (hmatrix.py:827-858). */
 int cbie_hlu_factor(cbie_hmat* h, double trunc_tol, cbie_hlu** out);
 void cbie_hlu_destroy(cbie_hlu* f);

@@ -51,6 +51,8 @@ _SIGS = {
     "cbie_hlu_factor": (ct.c_int, [P, ct.c_double, ct.POINTER(P)]),
     "cbie_hlu_destroy": (None, [P]),
     "cbie_far_field_sums": (ct.c_int, [P, P, ct.c_int, P, ct.c_int, ct.c_double, P]),
+    "cbie_gmres": (ct.c_int, [P, P, ct.c_double, ct.c_int, ct.c_int, P, ct.POINTER(ct.c_int),
+                              ct.POINTER(ct.c_double), ct.POINTER(ct.c_int)]),
     "cbie_hlu_dist_plan_host": (ct.c_int, [P, ct.c_int64, ct.c_int, ct.c_int, ct.c_double, ct.c_int, P, P]),
     "cbie_hlu_factor_dist": (ct.c_int, [P, ct.c_double, ct.POINTER(P)]),
     "cbie_hlu_factor_emulated": (ct.c_int, [P, ct.c_double, ct.c_int, ct.POINTER(P)]),

@@ -612,56 +612,70 @@ void hmatrix_build_entry(cbie_hmat* H, int n_leaf) { hmatrix_build(H, n_leaf); }
 // ---------------------------------------------------------------------------
 void hmat_apply(cbie_hmat* H, const zc* d_xp, zc* d_yp, int nrhs, cudaStream_t s);
 
+// gather plan of the H-matvec for one nrhs: leaf partial products, then every row
+// sums its contributions in leaf order (deterministic); built once per H-matrix
+struct MatvecPlan {
+  int nrhs = 0, nleaf = 0, maxr = 1;
+  DBuf<LeafInfo> dl;
+  DBuf<int64_t> dpo, drs, dst;
+  DBuf<int32_t> dco, dro, drp;
+  DBuf<zc> part, tmp;
+};
+
 void hmat_apply(cbie_hmat* H, const zc* d_xp, zc* d_yp, int nrhs, cudaStream_t s) {
   Tree& T = H->tree;
   const int nleaf = (int)T.leaves.size();
-  const int C = T.C;
-  std::vector<int64_t> poff(nleaf);
-  std::vector<int32_t> coloff(nleaf), rowoff(nleaf);
-  int64_t tot = 0;
-  int maxr = 1;
-  for (int li = 0; li < nleaf; ++li) {
-    poff[li] = tot;
-    tot += (int64_t)T.leaves[li].m * nrhs;
-    coloff[li] = T.cl[T.leaves[li].c].lo * C;
-    rowoff[li] = T.cl[T.leaves[li].r].lo * C;
-    maxr = std::max(maxr, T.leaves[li].cap);
-  }
-  // row -> contributing (leaf, local row) in leaf order
   const int64_t N = H->N;
-  std::vector<std::vector<std::pair<int64_t, int64_t>>> rows(N);
-  std::vector<int32_t> rptr(N + 1, 0);
-  std::vector<int64_t> rsrc, rstride;
-  for (int li = 0; li < nleaf; ++li) {
-    const auto& L = T.leaves[li];
-    for (int i = 0; i < L.m; ++i) rows[rowoff[li] + i].push_back({poff[li] + i, L.m});
-  }
-  for (int64_t i = 0; i < N; ++i) {
-    rptr[i + 1] = rptr[i] + (int32_t)rows[i].size();
-    for (auto& pr : rows[i]) {
-      rsrc.push_back(pr.first);
-      rstride.push_back(pr.second);
+  auto* MP = static_cast<MatvecPlan*>(H->mv_plan.get());
+  if (!MP || MP->nrhs != nrhs) {
+    auto mp = std::make_shared<MatvecPlan>();
+    const int C = T.C;
+    std::vector<int64_t> poff(nleaf);
+    std::vector<int32_t> coloff(nleaf), rowoff(nleaf);
+    int64_t tot = 0;
+    int maxr = 1;
+    for (int li = 0; li < nleaf; ++li) {
+      poff[li] = tot;
+      tot += (int64_t)T.leaves[li].m * nrhs;
+      coloff[li] = T.cl[T.leaves[li].c].lo * C;
+      rowoff[li] = T.cl[T.leaves[li].r].lo * C;
+      maxr = std::max(maxr, T.leaves[li].cap);
     }
+    // row -> contributing (leaf, local row) in leaf order
+    std::vector<std::vector<std::pair<int64_t, int64_t>>> rows(N);
+    std::vector<int32_t> rptr(N + 1, 0);
+    std::vector<int64_t> rsrc, rstride;
+    for (int li = 0; li < nleaf; ++li) {
+      const auto& L = T.leaves[li];
+      for (int i = 0; i < L.m; ++i) rows[rowoff[li] + i].push_back({poff[li] + i, L.m});
+    }
+    for (int64_t i = 0; i < N; ++i) {
+      rptr[i + 1] = rptr[i] + (int32_t)rows[i].size();
+      for (auto& pr : rows[i]) {
+        rsrc.push_back(pr.first);
+        rstride.push_back(pr.second);
+      }
+    }
+    mp->nrhs = nrhs;
+    mp->nleaf = nleaf;
+    mp->maxr = maxr;
+    mp->dl.upload(T.leaves, s);
+    mp->dpo.upload(poff, s);
+    mp->drs.upload(rsrc, s);
+    mp->dst.upload(rstride, s);
+    mp->dco.upload(coloff, s);
+    mp->dro.upload(rowoff, s);
+    mp->drp.upload(rptr, s);
+    mp->part.alloc(std::max<int64_t>(tot, 1));
+    mp->tmp.alloc((size_t)nleaf * maxr);
+    H->mv_plan = mp;
+    MP = mp.get();
   }
-  DBuf<LeafInfo> dl;
-  dl.upload(T.leaves, s);
-  DBuf<int64_t> dpo, drs, dst;
-  dpo.upload(poff, s);
-  drs.upload(rsrc, s);
-  dst.upload(rstride, s);
-  DBuf<int32_t> dco, dro, drp;
-  dco.upload(coloff, s);
-  dro.upload(rowoff, s);
-  drp.upload(rptr, s);
-  DBuf<zc> part, tmp;
-  part.alloc(std::max<int64_t>(tot, 1));
-  tmp.alloc((size_t)nleaf * maxr);
-  k_leaf_apply<<<nleaf, 128, 0, s>>>(dl.p, dpo.p, H->rank.p, H->arena.p, d_xp, nrhs, N, dro.p,
-                                     dco.p, part.p, tmp.p, maxr);
+  k_leaf_apply<<<nleaf, 128, 0, s>>>(MP->dl.p, MP->dpo.p, H->rank.p, H->arena.p, d_xp, nrhs, N, MP->dro.p,
+                                     MP->dco.p, MP->part.p, MP->tmp.p, MP->maxr);
   CKL();
-  k_gather_rows<<<ceil_div(N, 128), 128, 0, s>>>(drp.p, drs.p, part.p, N, nrhs, dst.p, d_yp);
+  k_gather_rows<<<ceil_div(N, 128), 128, 0, s>>>(MP->drp.p, MP->drs.p, MP->part.p, N, nrhs, MP->dst.p, d_yp);
   CKL();
-  CK(cudaStreamSynchronize(s));
 }
 
 // ---------------------------------------------------------------------------
@@ -779,6 +793,7 @@ int cbie_hmatvec(cbie_hmat* h, const cbie_c128* x, cbie_c128* y, int nrhs) {
     dx.upload(xp, s);
     dy.alloc((size_t)N * nrhs);
     hmat_apply(h, dx.p, dy.p, nrhs, s);
+    CK(cudaStreamSynchronize(s));
     CK(cudaMemcpy(yp.data(), dy.p, sizeof(zc) * yp.size(), cudaMemcpyDeviceToHost));
     zc* yy = reinterpret_cast<zc*>(y);
     for (size_t p = 0; p < h->tree.pperm.size(); ++p)

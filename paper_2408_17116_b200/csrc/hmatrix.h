@@ -4,6 +4,7 @@
 // Restates hmatrix.py:31-89 (ClusterTree, admissible), 96-204 (block kinds,
 // block tree) with flat arrays so the device kernels can address leaves by index.
 #pragma once
+#include <memory>
 #include <vector>
 
 #include "context.h"
@@ -67,6 +68,7 @@ struct cbie_hmat {
   std::vector<uint8_t> adm;    // [nleaf] admissible in the block tree (before demotion)
   bool partial = false;        // true until the shards were exchanged
   bool owns(int li) const { return owner.empty() || owner[li] == shard_rank; }
+  std::shared_ptr<void> mv_plan;   // cached H-matvec gather plan (aca.cu hmat_apply)
 };
 
 // shard.cu: LPT partition of the leaves over `world` processes by estimated fill cost

@@ -24,6 +24,8 @@ class Problem:
     aca_tol: float = 1e-4
     trunc_tol: Optional[float] = None
     gmres_tol: float = 1e-4
+    gmres_restart: int = 200
+    gmres_max_iters: int = 2000
     eta: float = 2.0
     n_leaf: int = 64
     tau: float = 1.0
@@ -111,6 +113,31 @@ def solve_direct(problem: Problem) -> SolveResult:
         "device": {"generator": gen.stats(), "hmatrix": H.stats(), "hlu": F.stats()},
     }
     return SolveResult(x, residual, metrics)
+
+
+def solve_gmres(problem: Problem, restart: Optional[int] = None,
+                max_iters: Optional[int] = None) -> SolveResult:
+    """Unpreconditioned restarted GMRES on the compressed operator (solver.py:206-307):
+    the Krylov basis, the H-matvec and every vector operation stay on the device
+    (cbie_gmres, csrc/gmres.cu)."""
+    import ctypes as ct
+    from . import _ffi
+    restart = restart if restart is not None else problem.gmres_restart
+    max_iters = max_iters if max_iters is not None else problem.gmres_max_iters
+    H, gen, scaled, times = build_hmatrix(problem)
+    b = np.ascontiguousarray(gen.rhs(problem.excitation) * scaled.row_scale)
+    y = np.empty_like(b)
+    it, rel, ok = ct.c_int(), ct.c_double(), ct.c_int()
+    t0 = time.perf_counter()
+    H.dev.check(H.dev.lib.cbie_gmres(H.h, _ffi.ptr(b), float(problem.gmres_tol), int(restart), int(max_iters),
+                                     _ffi.ptr(y), ct.byref(it), ct.byref(rel), ct.byref(ok)))
+    t_solve = time.perf_counter() - t0
+    x = y * scaled.col_scale
+    metrics = {**times, "operator": "hmatrix", "solve_s": t_solve, "n_dofs": problem.n_dofs,
+               "hmatrix_bytes": H.memory_bytes(), "compression_rate": H.compression_rate(),
+               "peak_rss_bytes": _peak_rss_bytes(),
+               "memory_method": "ru_maxrss sampling + logical leaf accounting"}
+    return SolveResult(x, float(rel.value), metrics, iterations=int(it.value), converged=bool(ok.value))
 
 
 def solve_dense(problem: Problem) -> SolveResult:
