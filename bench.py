@@ -59,6 +59,24 @@ def _fp64_peak():
         (37.0, "fallback (B200 FP64 nominal)")
 
 
+def _ncu_traffic(kernel="k_trunc_gram"):
+    """DRAM bytes (read + write) per launch of the dominant kernel from the committed
+    ncu --set full capture (profiles/r01d_k_trunc_gram_ncu_raw.csv), or None."""
+    import csv
+    path = os.path.join(ROOT, "profiles", "r01d_k_trunc_gram_ncu_raw.csv")
+    try:
+        rows = list(csv.reader(open(path)))
+        h, units, v = rows[0], rows[1], rows[2]
+        scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+        tot = 0.0
+        for name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = h.index(name)
+            tot += float(v[i].replace(",", "")) * scale.get(units[i], 1.0)
+        return tot
+    except (OSError, ValueError, IndexError):
+        return None
+
+
 def _peaks():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -229,7 +247,8 @@ def run_gpu(args):
     roof = {"bound": "tensor", "kernel": "H-LU recompression (k_trunc_gram + k_trunc2, FP64; "
             "B200 DMMA and DFMA share the FP64 peak)",
             "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
-            "peak_source": fp64_src, "traffic": None,
+            "peak_source": fp64_src, "traffic": _ncu_traffic(),
+            "traffic_source": "ncu --set full, one k_trunc_gram launch (profiles/r01d_k_trunc_gram_ncu_raw.csv)",
             "flops_per_launch": tf / max(tl, 1), "avg_launch_ms": tms / max(tl, 1),
             "share_of_step": tms / args.steps / ms,
             "hbm_alg_bytes_per_launch": tb / max(tl, 1),
