@@ -667,9 +667,70 @@ __device__ __forceinline__ double hash_unit(uint32_t a, uint32_t b, uint32_t c) 
   return (double)h * (2.0 / 4294967296.0) - 1.0;
 }
 
+// The three range-finder products of the first attempt for ALL tasks of a launch,
+// 32 x 32 output tiles over the whole GPU (the per-task kernel below then starts from
+// Y; a task has ~1 CTA otherwise, ~20 tasks per launch on 148 SMs):
+//   mode 0: Y = P Omega,  mode 1: Z = P^H Y,  mode 2: Y = P Z
+// (Omega from the same hash as the per-task kernel; tasks on the exact path skip.)
+__global__ void __launch_bounds__(256) k_dlr_range(const zc* __restrict__ arena, const DenseLRDesc* __restrict__ ds,
+                                                   zc* scratch, int64_t scratch_per, int mode) {
+  const DenseLRDesc d = ds[blockIdx.z];
+  const int m = d.m, n = d.n, ld = d.ld;
+  const int full = min(m, n);
+  int l = min(d.l0, full);
+  const bool exact = 2 * l > full;
+  if (exact) l = full;
+  if (exact && l == n) return;
+  const zc* P = arena + d.p;
+  zc* Y = scratch + (int64_t)blockIdx.z * scratch_per;
+  zc* Z = Y + (int64_t)m * d.cap;
+  const int rows = mode == 1 ? n : m, inner = mode == 1 ? m : n;
+  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  if (i0 >= rows || j0 >= l) return;
+  __shared__ zc sA[16][33];
+  __shared__ zc sB[16][33];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  zc acc[2][2] = {{zmk(0, 0), zmk(0, 0)}, {zmk(0, 0), zmk(0, 0)}};
+  for (int k0 = 0; k0 < inner; k0 += 16) {
+    for (int e = threadIdx.x; e < 16 * 32; e += 256) {
+      const int kk = e / 32, ii = e % 32;
+      const int gi = i0 + ii, gk = k0 + kk, gj = j0 + ii;
+      zc a = zmk(0, 0), b = zmk(0, 0);
+      if (gi < rows && gk < inner) a = mode == 1 ? zconj(P[(int64_t)gi * ld + gk]) : P[(int64_t)gk * ld + gi];
+      if (gj < l && gk < inner) {
+        if (mode == 0) b = zmk(hash_unit((uint32_t)gk, (uint32_t)gj, 0), hash_unit((uint32_t)gk, (uint32_t)gj, 1));
+        else if (mode == 1) b = Y[(int64_t)gj * m + gk];
+        else b = Z[(int64_t)gj * n + gk];
+      }
+      sA[kk][ii] = a;
+      sB[kk][ii] = b;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      const zc a0 = sA[kk][ty], a1 = sA[kk][ty + 16];
+      const zc b0 = sB[kk][tx], b1 = sB[kk][tx + 16];
+      zfma(acc[0][0], a0, b0);
+      zfma(acc[0][1], a0, b1);
+      zfma(acc[1][0], a1, b0);
+      zfma(acc[1][1], a1, b1);
+    }
+    __syncthreads();
+  }
+  zc* C = mode == 1 ? Z : Y;
+  const int ldc = mode == 1 ? n : m;
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+      const int gi = i0 + ty + 16 * a, gj = j0 + tx + 16 * b;
+      if (gi < rows && gj < l) C[(int64_t)gj * ldc + gi] = acc[a][b];
+    }
+}
+
 __global__ void __launch_bounds__(LR_NT) k_dense_lr(zc* arena, int* ranks,
                                                     const DenseLRDesc* __restrict__ ds,
-                                                    zc* scratch, int64_t scratch_per) {
+                                                    zc* scratch, int64_t scratch_per, int pre) {
   const DenseLRDesc d = ds[blockIdx.x];
   const int m = d.m, n = d.n, ld = d.ld;
   const zc* P = arena + d.p;
@@ -698,6 +759,8 @@ __global__ void __launch_bounds__(LR_NT) k_dense_lr(zc* arena, int* ranks,
     if (exact && l == n) {
       for (int64_t e = threadIdx.x; e < (int64_t)m * l; e += LR_NT)
         Y[e] = P[(e / m) * ld + e % m];
+    } else if (pre && attempt == 0) {
+      // Y = P (P^H (P Omega)) already in scratch (k_dlr_range)
     } else {
       zc* Om = Z;   // Omega (n x l) staged in the Z region, then Z reused below
       for (int64_t e = threadIdx.x; e < (int64_t)n * l; e += LR_NT)
@@ -765,9 +828,15 @@ void launch_dense_lr(zc* arena, int* ranks, const DenseLRDesc* d_desc, int nd, i
   const size_t smem = (size_t)max_cap * (sizeof(zc) + sizeof(double)) + 32 +
                       (size_t)TG_K * (TG_R + 1 + 65) * sizeof(zc);
   CK(cudaFuncSetAttribute(k_dense_lr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  const int rmax = std::max(max_m, max_n), lmax = std::min(max_m, max_n);
   for (int b0 = 0; b0 < nd; b0 += wave) {
     int nb = std::min(wave, nd - b0);
-    k_dense_lr<<<nb, LR_NT, smem, s>>>(arena, ranks, d_desc + b0, scratch.p, per);
+    for (int mode = 0; mode < 3; ++mode) {
+      k_dlr_range<<<dim3(ceil_div(rmax, 32), ceil_div(lmax, 32), nb), 256, 0, s>>>(arena, d_desc + b0, scratch.p,
+                                                                                    per, mode);
+      CKL();
+    }
+    k_dense_lr<<<nb, LR_NT, smem, s>>>(arena, ranks, d_desc + b0, scratch.p, per, 1);
     CKL();
   }
 }
