@@ -119,23 +119,43 @@ struct ConcatD {
   Piece p[MAX_PIECES];
 };
 __global__ void k_concat(zc* __restrict__ ar, int* __restrict__ ranks, const ConcatD* __restrict__ ds) {
-  const ConcatD d = ds[blockIdx.y];
-  int c0[MAX_PIECES + 1];
-  c0[0] = 0;
-  for (int q = 0; q < d.np; ++q) c0[q + 1] = c0[q] + dimv(d.p[q].cols, ranks);
-  const int tot = c0[d.np];
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < (int64_t)d.rows * tot;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int i = (int)(e % d.rows), j = (int)(e / d.rows);
-    int q = 0;
-    while (j >= c0[q + 1]) ++q;
-    const Piece& P = d.p[q];
-    zc v = zmk(0, 0);
-    if (i >= P.roff && i < P.roff + P.prow) v = zmul(P.scale, ar[vidx(P.src, i - P.roff, j - c0[q])]);
-    ar[d.dst + e] = v;
+  // descriptor and column offsets staged once per CTA in shared memory (a per-thread
+  // copy of the 800-byte descriptor, indexed by piece, went to local memory)
+  __shared__ Piece sp[MAX_PIECES];
+  __shared__ int c0[MAX_PIECES + 1];
+  __shared__ int64_t sdst;
+  __shared__ int srows, snp, sslot;
+  const ConcatD* dp = ds + blockIdx.y;
+  if (threadIdx.x == 0) {
+    snp = dp->np;
+    srows = dp->rows;
+    sdst = dp->dst;
+    sslot = dp->out_slot;
   }
   __syncthreads();
-  if (blockIdx.x == 0 && threadIdx.x == 0) ranks[d.out_slot] = tot;
+  const int np = snp, rows = srows;
+  for (int q = threadIdx.x; q < np; q += blockDim.x) sp[q] = dp->p[q];
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    c0[0] = 0;
+    for (int q = 0; q < np; ++q) c0[q + 1] = c0[q] + dimv(sp[q].cols, ranks);
+  }
+  __syncthreads();
+  const int tot = c0[np];
+  // one column per (CTA, warp-group) pass: rows contiguous in the destination
+  for (int j = blockIdx.x; j < tot; j += gridDim.x) {
+    int q = 0;
+    while (j >= c0[q + 1]) ++q;
+    const Piece& P = sp[q];
+    const int jj = j - c0[q];
+    zc* dst = ar + sdst + (int64_t)j * rows;
+    for (int i = threadIdx.x; i < rows; i += blockDim.x) {
+      zc v = zmk(0, 0);
+      if (i >= P.roff && i < P.roff + P.prow) v = zmul(P.scale, ar[vidx(P.src, i - P.roff, jj)]);
+      dst[i] = v;
+    }
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) ranks[sslot] = tot;
 }
 
 // ---------------------------------------------------------------------------
