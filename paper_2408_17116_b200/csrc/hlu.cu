@@ -1168,6 +1168,14 @@ void make_plan(Plan& P, cudaStream_t s, const Recorder* Rx = nullptr, const std:
       }
     }
     gr.count = (int)(j - i);
+    if (kind == OP_GEMM) {
+      // dense x dense products (every dimension static and >= 128) first: 64 x 64 tiles
+      auto big = [](const GemmD& x) {
+        return x.m.slot < 0 && x.n.slot < 0 && x.k.slot < 0 && x.m.v >= 128 && x.n.v >= 128 && x.k.v >= 128;
+      };
+      std::stable_partition(g.begin() + gr.start, g.end(), big);
+      gr.split = (int)std::count_if(g.begin() + gr.start, g.end(), big);
+    }
     if (kind == OP_TRUNC) {
       // factor-form problems (Gram path + hand-offs) first, dense-mode ones after; the
       // two parts run on two streams.  Without the Gram path: small blocks / large blocks.
@@ -1351,15 +1359,27 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
     if (prof) cudaEventRecord(e0, s);
     switch (gr.kind) {
       case OP_GEMM: {
-        int mt = 1, nt = 1;
-        for (int i = 0; i < gr.count; ++i) {
-          mt = std::max(mt, ceil_div(g[gr.start + i].m.v, GT));
-          nt = std::max(nt, ceil_div(g[gr.start + i].n.v, GT));
-        }
-        for (int b0 = 0; b0 < gr.count; b0 += 65535) {
-          int nb = std::min(65535, gr.count - b0);
-          k_gemm<<<dim3(mt, nt, nb), 256, 0, s>>>(arena, ranks, dg.p + gr.start + b0);
-        }
+        // [start, start + split): dense x dense (64 x 64 tiles); the rest: 32 x 32 tiles
+        const bool g64 = getenv("CBIE_GEMM32") == nullptr;
+        const int split = g64 ? gr.split : 0;
+        auto launch = [&](int b, int e, bool wide) {
+          if (e <= b) return;
+          int mt = 1, nt = 1;
+          for (int i = b; i < e; ++i) {
+            mt = std::max(mt, g[gr.start + i].m.v);
+            nt = std::max(nt, g[gr.start + i].n.v);
+          }
+          for (int b0 = b; b0 < e; b0 += 65535) {
+            const int nb = std::min(65535, e - b0);
+            if (wide)
+              k_gemm64<<<dim3(ceil_div(mt, GT64), ceil_div(nt, GT64), nb), 256, 0, s>>>(arena, ranks,
+                                                                                       dg.p + gr.start + b0);
+            else
+              k_gemm<<<dim3(ceil_div(mt, GT), ceil_div(nt, GT), nb), 256, 0, s>>>(arena, ranks, dg.p + gr.start + b0);
+          }
+        };
+        launch(0, split, true);
+        launch(split, gr.count, false);
         break;
       }
       case OP_EW: {
@@ -1466,6 +1486,19 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
       float ms = 0;
       cudaEventElapsedTime(&ms, e0, e1);
       ex.kind_ms[gr.kind] += ms;
+      if (gr.kind == OP_GEMM && getenv("CBIE_GEMM_DUMP") && ms > 0.3) {
+        std::map<std::string, int> shapes;
+        for (int i = 0; i < gr.count; ++i) {
+          const GemmD& x = g[gr.start + i];
+          char b[96];
+          snprintf(b, sizeof b, "%d%s x %d%s x %d%s", x.m.v, x.m.slot >= 0 ? "*" : "", x.n.v,
+                   x.n.slot >= 0 ? "*" : "", x.k.v, x.k.slot >= 0 ? "*" : "");
+          shapes[b]++;
+        }
+        fprintf(stderr, "GEMM level=%d n=%d ms=%.3f:", gr.level, gr.count, ms);
+        for (auto& kv : shapes) fprintf(stderr, " [%s]x%d", kv.first.c_str(), kv.second);
+        fprintf(stderr, "\n");
+      }
       if (gr.kind == OP_TRUNC && getenv("CBIE_TRUNC_DUMP")) {
         // debug: per-launch size profile (k of every task after its inputs are final)
         int kmx = 0, n64 = 0, n96 = 0, rmx = 0;
