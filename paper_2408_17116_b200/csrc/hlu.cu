@@ -1910,7 +1910,18 @@ static void hlu_solve_impl(cbie_hlu* F, const zc* b, zc* x, int nrhs) {
     CK(cudaMemcpyAsync(SC.ranks.p + nleaf, r0.data() + nleaf, sizeof(int) * (r0.size() - nleaf),
                        cudaMemcpyHostToDevice, s));
   CK(cudaMemcpyAsync(SC.ranks.p, F->ranks.p, sizeof(int) * nleaf, cudaMemcpyDeviceToDevice, s));
-  run_plan(SC.plan, F->arena.p, SC.ranks.p, F->piv.p, SC.rc.p, SC.flag.p, SC.ovf.p, SC.tw, F->tol, s);
+  EvTimer tm;
+  tm.start(s);
+  Exec ex = run_plan(SC.plan, F->arena.p, SC.ranks.p, F->piv.p, SC.rc.p, SC.flag.p, SC.ovf.p, SC.tw, F->tol, s);
+  F->stat["solve_device_ms"] = tm.stop_ms(s);
+  F->stat["solve_levels"] = ex.levels;
+  F->stat["solve_launches"] = ex.launches;
+  F->stat["solve_host_enqueue_ms"] = ex.host_enqueue_ms;
+  {
+    const char* nm[OP_NKIND] = {"gemm", "ew", "concat", "trsm", "getrf", "trunc", "dense_lr"};
+    for (int k = 0; k < OP_NKIND; ++k)
+      if (ex.kind_launch[k]) F->stat[std::string("solve_launch_") + nm[k]] = ex.kind_launch[k];
+  }
   CK(cudaMemcpy(bp.data(), F->arena.p + SC.xoff, sizeof(zc) * bp.size(), cudaMemcpyDeviceToHost));
   for (size_t p = 0; p < T.pperm.size(); ++p)
     for (int c = 0; c < C; ++c) {

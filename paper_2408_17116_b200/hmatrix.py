@@ -171,6 +171,10 @@ class HLUFactors:
     def stats(self) -> dict:
         return dict(self._stats)
 
+    def solve_stats(self) -> dict:
+        """Device statistics of the last solve (levels, launches, device ms)."""
+        return {k: v for k, v in _ffi.stats(self.h, 2).items() if k.startswith("solve_")}
+
     def leaf(self, i: int):
         """('dense', D) | ('lu', LU, piv) | ('lowrank', U, V) for leaf i (permuted order)."""
         perm, lv = self.H.tree()
