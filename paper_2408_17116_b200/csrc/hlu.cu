@@ -1079,6 +1079,9 @@ struct Exec {
   int kind_launch[OP_NKIND] = {};
   int64_t kind_tasks[OP_NKIND] = {};
   double host_enqueue_ms = 0.0;   // host time to issue the whole plan (before the final sync)
+  std::vector<double> gms;        // CBIE_PROFILE: per-group device ms (level-synchronous)
+  double crit_ms = 0.0;           // CBIE_PROFILE: critical path of the multi-stream schedule
+  double crit_kind_ms[OP_NKIND] = {};
   long long frees = 0;            // cudaFree calls while issuing (device-wide syncs)
 };
 
@@ -1486,6 +1489,8 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
       float ms = 0;
       cudaEventElapsedTime(&ms, e0, e1);
       ex.kind_ms[gr.kind] += ms;
+      if (ex.gms.size() < P.groups.size()) ex.gms.resize(P.groups.size(), 0.0);
+      ex.gms[gi] = ms;
       if (gr.kind == OP_GEMM && getenv("CBIE_GEMM_DUMP") && ms > 0.3) {
         std::map<std::string, int> shapes;
         for (int i = 0; i < gr.count; ++i) {
@@ -1522,6 +1527,37 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
   if (prof) {
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
+    // critical path of the multi-stream schedule with these (level-synchronous) group
+    // durations: a group starts after its cross-kind dependencies and after the previous
+    // group of its own stream
+    if (!ex.gms.empty()) {
+      std::vector<double> fin(P.groups.size(), 0.0);
+      std::vector<int> from(P.groups.size(), -1);
+      int lastq[NVK];
+      for (int q = 0; q < NVK; ++q) lastq[q] = -1;
+      int best = -1;
+      for (size_t gi = 0; gi < P.groups.size(); ++gi) {
+        const auto& gr = P.groups[gi];
+        const int q = vkind(gr.kind, gr.level);
+        double st = 0.0;
+        int src = -1;
+        if (lastq[q] >= 0 && fin[lastq[q]] > st) {
+          st = fin[lastq[q]];
+          src = lastq[q];
+        }
+        for (int d : gr.deps)
+          if (fin[d] > st) {
+            st = fin[d];
+            src = d;
+          }
+        fin[gi] = st + ex.gms[gi];
+        from[gi] = src;
+        lastq[q] = (int)gi;
+        if (best < 0 || fin[gi] > fin[best]) best = (int)gi;
+      }
+      ex.crit_ms = best >= 0 ? fin[best] : 0.0;
+      for (int g = best; g >= 0; g = from[g]) ex.crit_kind_ms[P.groups[g].kind] += ex.gms[g];
+    }
   }
   if (ms) {
     for (int q = 0; q < NVK; ++q) {
@@ -1801,10 +1837,14 @@ static void hlu_factor_impl(cbie_hlu* F) {
     for (int k = 0; k < OP_NKIND; ++k) {
       F->stat[std::string("launch_") + nm[k]] = ex.kind_launch[k];
       F->stat[std::string("tasks_") + nm[k]] = (double)ex.kind_tasks[k];
-      if (getenv("CBIE_PROFILE")) F->stat[std::string("ms_") + nm[k]] = ex.kind_ms[k];
+      if (getenv("CBIE_PROFILE")) {
+        F->stat[std::string("ms_") + nm[k]] = ex.kind_ms[k];
+        F->stat[std::string("crit_ms_") + nm[k]] = ex.crit_kind_ms[k];
+      }
     }
   }
   F->stat["launches"] = ex.launches;
+  if (getenv("CBIE_PROFILE")) F->stat["crit_ms"] = ex.crit_ms;
   F->stat["tasks"] = (double)R.tasks.size();
   // executed FP64 work, counted by the kernels with the device-side ranks
   F->stat["flops_dense"] = hlu_flops_read();        // gemm, trsm, getrf
