@@ -534,6 +534,9 @@ struct Builder {
   };
   std::map<int, Pend> pend;   // leaf index -> queued updates
   bool lazy = getenv("CBIE_LAZY") != nullptr;   // off by default (round 1: slower, see DESIGN)
+  // CBIE_LAZY=<n>: flush a leaf's queue after n updates (default MAX_PIECES - 1)
+  int lazy_max = getenv("CBIE_LAZY") && atoi(getenv("CBIE_LAZY")) > 0
+                     ? std::min(atoi(getenv("CBIE_LAZY")), MAX_PIECES - 1) : MAX_PIECES - 1;
   int flushes = 0;
 
   void queue_update(int li, const Mat& U, const Mat& Vt, zc sign) {
@@ -544,7 +547,7 @@ struct Builder {
     p.Vt.push_back(Vt);
     p.sign.push_back(sign);
     p.capsum += U.cols;
-    if ((int)p.U.size() >= MAX_PIECES - 1) flush(li);
+    if ((int)p.U.size() >= lazy_max) flush(li);
   }
   void flush(int li) {
     auto it = pend.find(li);
