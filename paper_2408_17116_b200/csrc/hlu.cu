@@ -1384,6 +1384,20 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
               k_gemm<<<dim3(ceil_div(mt, GT), ceil_div(nt, GT), nb), 256, 0, s>>>(arena, ranks, dg.p + gr.start + b0);
           }
         };
+        bool vec = getenv("CBIE_GEMM32") == nullptr;   // every product a matrix x vector (one rhs)
+        int mv = 1;
+        for (int i = 0; i < gr.count && vec; ++i) {
+          const GemmD& x = g[gr.start + i];
+          vec = x.n.slot < 0 && x.n.v == 1;
+          mv = std::max(mv, x.m.v);
+        }
+        if (vec) {
+          for (int b0 = 0; b0 < gr.count; b0 += 65535) {
+            const int nb = std::min(65535, gr.count - b0);
+            k_gemv<<<dim3(ceil_div(mv, GV_ROWS), nb), GV_NT, 0, s>>>(arena, ranks, dg.p + gr.start + b0);
+          }
+          break;
+        }
         launch(0, split, true);
         launch(split, gr.count, false);
         break;
@@ -1955,15 +1969,21 @@ static void hlu_solve_impl(cbie_hlu* F, const zc* b, zc* x, int nrhs) {
   CK(cudaMemcpyAsync(SC.ranks.p, F->ranks.p, sizeof(int) * nleaf, cudaMemcpyDeviceToDevice, s));
   EvTimer tm;
   tm.start(s);
-  Exec ex = run_plan(SC.plan, F->arena.p, SC.ranks.p, F->piv.p, SC.rc.p, SC.flag.p, SC.ovf.p, SC.tw, F->tol, s);
+  // one stream, level by level: the solve is a ~1,800-level chain of small products whose
+  // cross-stream event hand-offs cost more than the overlap gains
+  const bool solve_ms = getenv("CBIE_SOLVE_MS") != nullptr;
+  Exec ex = run_plan(SC.plan, F->arena.p, SC.ranks.p, F->piv.p, SC.rc.p, SC.flag.p, SC.ovf.p, SC.tw, F->tol, s,
+                     solve_ms ? 0 : 1, 1 << 30);
   F->stat["solve_device_ms"] = tm.stop_ms(s);
   F->stat["solve_levels"] = ex.levels;
   F->stat["solve_launches"] = ex.launches;
   F->stat["solve_host_enqueue_ms"] = ex.host_enqueue_ms;
   {
     const char* nm[OP_NKIND] = {"gemm", "ew", "concat", "trsm", "getrf", "trunc", "dense_lr"};
-    for (int k = 0; k < OP_NKIND; ++k)
+    for (int k = 0; k < OP_NKIND; ++k) {
       if (ex.kind_launch[k]) F->stat[std::string("solve_launch_") + nm[k]] = ex.kind_launch[k];
+      if (ex.kind_ms[k] > 0.0) F->stat[std::string("solve_ms_") + nm[k]] = ex.kind_ms[k];
+    }
   }
   CK(cudaMemcpy(bp.data(), F->arena.p + SC.xoff, sizeof(zc) * bp.size(), cudaMemcpyDeviceToHost));
   for (size_t p = 0; p < T.pperm.size(); ++p)

@@ -135,6 +135,35 @@ __global__ void __launch_bounds__(256) k_gemm64(zc* __restrict__ ar, const int* 
     }
 }
 
+// matrix x vector (n == 1, the triangular solves with one right-hand side): a CTA takes 32
+// rows, its 8 warps split the inner dimension (lanes = rows: coalesced over a column-major
+// A), partial sums reduced through shared memory in a fixed order
+constexpr int GV_NT = 256, GV_ROWS = 32;
+__global__ void __launch_bounds__(GV_NT) k_gemv(zc* __restrict__ ar, const int* __restrict__ ranks,
+                                                const GemmD* __restrict__ ds) {
+  const GemmD d = ds[blockIdx.y];
+  const int m = dimv(d.m, ranks), n = dimv(d.n, ranks), k = dimv(d.k, ranks);
+  if (blockIdx.x == 0 && threadIdx.x == 0) flop_add(8.0 * m * n * k);
+  const int r0 = blockIdx.x * GV_ROWS;
+  if (r0 >= m || n < 1) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int i = r0 + lane;
+  __shared__ zc part[GV_NT / 32][GV_ROWS];
+  zc acc = zmk(0, 0);
+  if (i < m)
+    for (int kk = w; kk < k; kk += GV_NT / 32) zfma(acc, ar[vidx(d.A, i, kk)], ar[vidx(d.B, kk, 0)]);
+  part[w][lane] = acc;
+  __syncthreads();
+  if (w == 0 && i < m) {
+    zc sum = part[0][lane];
+    for (int q = 1; q < GV_NT / 32; ++q) sum = zadd(sum, part[q][lane]);
+    const int64_t o = vidx(d.C, i, 0);
+    zc v = zmul(d.alpha, sum);
+    if (d.beta.x != 0.0 || d.beta.y != 0.0) v = zadd(v, zmul(d.beta, ar[o]));
+    ar[o] = v;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // EW: Y = a X + b Y  (X optional)
 // ---------------------------------------------------------------------------
