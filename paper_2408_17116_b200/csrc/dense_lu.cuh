@@ -501,8 +501,9 @@ __global__ void __launch_bounds__(LU_NT, 2) k_trsm_blk(zc* __restrict__ ar, cons
   for (int bb = 0; bb < nbk; ++bb) {
     const int b = lower ? bb : nbk - 1 - bb;
     const int j0 = b * LU_NB, bs = min(LU_NB, n - j0);
-    // diagonal block: warp w solves columns w, w + 16 (lane = row)
-    {
+    // diagonal block: warp w solves columns w, w + 16 (lane = row); warps without a
+    // column skip the block load (one right-hand side: 1 of 16 warps works here)
+    if (w < nc) {
       zc t[LU_NB];
 #pragma unroll
       for (int s = 0; s < LU_NB; ++s) t[s] = (s < bs && lane < bs) ? el(j0 + lane, j0 + s) : zmk(0.0, 0.0);
