@@ -1239,8 +1239,8 @@ void make_plan(Plan& P, cudaStream_t s, const Recorder* Rx = nullptr, const std:
 // (the distributed H-LU exchanges data between levels)
 // executor streams, created once per device: the same hardware work queues every
 // factorisation (CUDA_DEVICE_MAX_CONNECTIONS = 32 gives each its own queue, see
-// paper_2408_17116_b200/__init__.py); the diagonal chain (getrf, trsm) runs at the
-// highest stream priority
+// paper_2408_17116_b200/__init__.py); priorities follow the critical path (CBIE_PROFILE
+// crit_ms): recompression lanes and concatenations first, the diagonal chain next
 struct StreamPool {
   cudaStream_t kind[NVK] = {}, lane2[TRUNC_LANES] = {}, side = nullptr;
 };
@@ -1254,10 +1254,12 @@ StreamPool& stream_pool() {
   int lo = 0, hi = 0;   // hi = greatest priority (numerically lowest)
   CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
   for (int q = 0; q < NVK; ++q) {
-    const int pr = (q == OP_GETRF || q == OP_TRSM) ? hi : lo;
+    const bool rc = q == OP_TRUNC || q == OP_CONCAT || q >= OP_NKIND;
+    const bool diag = q == OP_GETRF || q == OP_TRSM;
+    const int pr = rc ? hi : diag ? std::min(lo, hi + 1) : lo;
     CK(cudaStreamCreateWithPriority(&P.kind[q], cudaStreamNonBlocking, pr));
   }
-  for (int l = 0; l < TRUNC_LANES; ++l) CK(cudaStreamCreateWithPriority(&P.lane2[l], cudaStreamNonBlocking, lo));
+  for (int l = 0; l < TRUNC_LANES; ++l) CK(cudaStreamCreateWithPriority(&P.lane2[l], cudaStreamNonBlocking, hi));
   CK(cudaStreamCreateWithPriority(&P.side, cudaStreamNonBlocking, lo));
   return P;
 }
