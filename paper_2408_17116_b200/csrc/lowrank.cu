@@ -425,7 +425,9 @@ static void launch_unblocked_list(zc* arena, zc* arena_out, int* ranks, const Tr
                                   int kmax, int64_t per, double tol, unsigned long long* overflow,
                                   TruncWork& work, cudaStream_t s, const int* list) {
   DBuf<zc>& dscratch = work.dscratch;
-  const int grid = std::min(nd, 74);
+  // one CTA per SM (grid-stride over the list) unless the scratch would exceed 4 GB
+  const int64_t cap_mem = std::max<int64_t>(74, ((int64_t)4 << 30) / std::max<int64_t>(per * (int64_t)sizeof(zc), 1));
+  const int grid = (int)std::min<int64_t>(nd, std::min<int64_t>(148, cap_mem));
   if (dscratch.n < (size_t)grid * per) dscratch.alloc((size_t)grid * per);
   const size_t smem = std::max((size_t)SMEM_J * SMEM_J * 3 * sizeof(zc) + SMEM_J * (sizeof(zc) + sizeof(double)),
                                (size_t)SMEM_J * SMEM_J * 2 * sizeof(zc) +
