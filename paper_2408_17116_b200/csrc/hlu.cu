@@ -1731,6 +1731,10 @@ static void hlu_record(cbie_hlu* F, Recorder& R, int64_t leaf_end, int64_t budge
   B.flush_all();
 }
 
+// temporaries of the cached solve tape (0 if none): the factor arena is sized for them so
+// that a solve does not reallocate and copy the factors
+static int64_t solve_cache_temps(int64_t leaf_end);
+
 static void hlu_factor_impl(cbie_hlu* F) {
   cbie_hmat* H = F->H;
   cbie_ctx* c = H->ctx;
@@ -1793,7 +1797,7 @@ static void hlu_factor_impl(cbie_hlu* F) {
   Exec ex = run_plan(PL, work.p, F->ranks.p, F->piv.p, F->rcond.p, flag.p, ovf.p, g_plan_cache->tw, F->tol, s);
   F->stat["factor_device_ms"] = tm.stop_ms(s);
   // the factors keep only their storage; the workspace stays with the plan cache
-  F->arena.alloc((size_t)leaf_end + 1);
+  F->arena.alloc((size_t)(leaf_end + solve_cache_temps(leaf_end)) + 1);
   CK(cudaMemcpyAsync(F->arena.p, work.p, sizeof(zc) * leaf_end, cudaMemcpyDeviceToDevice, s));
   CK(cudaStreamSynchronize(s));
   int hflag = 0;
@@ -1901,6 +1905,11 @@ struct SolveCache {
   TruncWork tw[2 * TRUNC_LANES];
 };
 std::unique_ptr<SolveCache> g_solve_cache;
+int64_t g_solve_leaf_end = -1;
+
+static int64_t solve_cache_temps(int64_t leaf_end) {
+  return (g_solve_cache && g_solve_leaf_end == leaf_end) ? g_solve_cache->pool_top : 0;
+}
 
 static void hlu_solve_impl(cbie_hlu* F, const zc* b, zc* x, int nrhs) {
   cbie_hmat* H = F->H;
@@ -1950,6 +1959,7 @@ static void hlu_solve_impl(cbie_hlu* F, const zc* b, zc* x, int nrhs) {
     sc->ovf.alloc(1);
     sc->key = key;
     g_solve_cache = std::move(sc);
+    g_solve_leaf_end = F->leaf_end;
   }
   SolveCache& SC = *g_solve_cache;
   // arena for the solve: factors (shared) + temps: allocate temps after the factor arena

@@ -1172,9 +1172,9 @@ void launch_gram(zc* arena, zc* aout, int* ranks, const TruncDesc* d_desc, int n
                  int* defer, const int* idx, int mn_max) {
   // mn_max > 0: problems with KG < k <= KMS and max(m, n) <= mn_max run the multi-stage path
   const int64_t per = gram_scratch_per() + (mn_max > 0 ? gram_ms_scratch(mn_max) : 0);
-  // one launch per group whenever 8 GB of scratch allow it (a second launch of the tail
+  // one launch per group whenever 2 GB of scratch allow it (a second launch of the tail
   // would wait for the whole first one on the stream)
-  const int wave = (int)std::max<int64_t>(1, ((int64_t)8 << 30) / (per * (int64_t)sizeof(zc)));
+  const int wave = (int)std::max<int64_t>(1, ((int64_t)2 << 30) / (per * (int64_t)sizeof(zc)));
   const size_t need = (size_t)std::min(wave, nd) * per;
   if (scratch.n < need) scratch.alloc(need);
   const int smem = (3 * GSQ + KG + 1) * (int)sizeof(zc);
