@@ -63,7 +63,7 @@ def _ncu_traffic(kernel="k_trunc_gram"):
     """DRAM bytes (read + write) per launch of the dominant kernel from the committed
     ncu --set full capture (profiles/r01d_k_trunc_gram_ncu_raw.csv), or None."""
     import csv
-    path = os.path.join(ROOT, "profiles", "r01d_k_trunc_gram_ncu_raw.csv")
+    path = os.path.join(ROOT, "profiles", "r01d_k_trunc_gram_ncu_raw.csv")   # full 148-problem launch
     try:
         rows = list(csv.reader(open(path)))
         h, units, v = rows[0], rows[1], rows[2]
