@@ -854,7 +854,7 @@ __device__ int herm_jacobi(zc* H, int n, zc* X, Smem& S) {
     for (int e = threadIdx.x; e < n * n; e += NT)
       if (e % n != e / n) off += zabs2(H[e]);
     off = bsum(off, S.red);
-    if (!(off > 1e-22 * f2)) break;
+    if (!(off > 1e-20 * f2)) break;
     for (int rd = 0; rd < ne - 1; ++rd) {
       // rotation of every pair (round-robin ordering); an index >= n pairs with identity
       if (threadIdx.x < np) {
