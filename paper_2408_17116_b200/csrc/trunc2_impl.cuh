@@ -629,6 +629,7 @@ constexpr int GCH = 64;             // rows staged per Gram chunk
 constexpr int GSQ = KG * KG;        // one k x k region (zc)
 constexpr int GLD = KG + 1;         // staged row stride (bank spread)
 constexpr double CHOL_EPS = 1e-13;  // pivoted-Cholesky stop (squared, relative)
+constexpr double GDELTA = 0.2;      // core reduction: directions below GDELTA * tol * s_0 dropped before the Jacobi
 
 __host__ __device__ inline int64_t gram_scratch_per() { return 4 * (int64_t)GSQ + 64; }
 
@@ -998,7 +999,7 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   }
   for (int e = threadIdx.x; e < kk1 * kk2; e += NT) Mg[e] = X2[e];
   __syncthreads();
-  const int kp = pchol(H, kk1, S.perm, (DELTA * tol) * (DELTA * tol), S);
+  const int kp = pchol(H, kk1, S.perm, (GDELTA * tol) * (GDELTA * tol), S);
   zc* Gp = Gv;   // R R^H (kp x kp)
   zc* Z = X2;    // eigenvectors (kp x kp)
   for (int e = threadIdx.x; e < kp * kp; e += NT) {
