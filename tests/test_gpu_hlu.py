@@ -161,3 +161,18 @@ def test_distributed_hlu_nccl_world1():
         assert _rel(Fd.solve(b), x1) <= 1e-8
     finally:
         cdist.finalize(gen)
+
+
+def test_cfg1_large_leaves_solution():
+    """Leaf size 256 (dense leaves up to 216 dofs): the dense x dense Schur products take
+    the 64 x 64-tile GEMM (k_gemm64) and the diagonal leaves the blocked LU; the solution
+    still matches the reference's config-1 solution to 10 x aca_tol."""
+    from paper_2408_17116_b200 import geometry as geo, kernels as ker
+    from paper_2408_17116_b200.solver import Problem, solve_direct
+    g = golden("cfg1_solve.npz")
+    vac = ker.Medium.from_relative(1.0, 1.0, 1.0)
+    prob = Problem(geo.unit_sphere_patches(0.5, 1, (6, 6)), ker.FormulationSpec(ker.MFIE_PEC, vac),
+                   ker.PlaneWave([0, 0, 1], [1, 0, 0], 1.0), aca_tol=1e-6, eta=1.0, n_leaf=256)
+    r = solve_direct(prob)
+    assert _rel(r.solution, g["x_direct"]) <= 10 * prob.aca_tol
+    assert r.residual <= 10 * prob.aca_tol
