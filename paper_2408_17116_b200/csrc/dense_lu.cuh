@@ -478,11 +478,15 @@ __global__ void __launch_bounds__(LU_NT, 2) k_trsm_blk(zc* __restrict__ ar, cons
   const zc* A = ar + d.T;
   // variant 0: P^T L  -> row swaps then mode 0;  1: U -> mode 1;  2: U^T (lower, no conj)
   if (d.variant == 0) {
+    // pivots staged in shared memory first (one coalesced load): the swap chain below is
+    // sequential, and a dependent global load per step made it the slowest part
+    __shared__ int spv[LU_NMAX];
+    for (int k2 = tid; k2 < n; k2 += LU_NT) spv[k2] = pivs[d.piv + k2];
+    __syncthreads();
     if (tid < nc) {
       zc* s = S + tid * n;
-      const int* pv = pivs + d.piv;
       for (int k2 = 0; k2 < n; ++k2) {
-        const int q = pv[k2];
+        const int q = spv[k2];
         if (q != k2) {
           const zc t = s[k2];
           s[k2] = s[q];
