@@ -251,6 +251,8 @@ def run_gpu(args):
             "traffic_source": "ncu --set full, one k_trunc_gram launch (profiles/r01d_k_trunc_gram_ncu_raw.csv)",
             "flops_per_launch": tf / max(tl, 1), "avg_launch_ms": tms / max(tl, 1),
             "share_of_step": tms / args.steps / ms,
+            "share_note": "sum of per-launch event times over the concurrent recompression "
+                          "streams / step time; > 1 means the launches overlap each other",
             "hbm_alg_bytes_per_launch": tb / max(tl, 1),
             "hlu_fp64_tflops": flops / (hlu_ms / 1e3) / 1e12,
             "hlu_fp64_frac": flops / (hlu_ms / 1e3) / 1e12 / fp64_peak}
