@@ -61,9 +61,9 @@ def _fp64_peak():
 
 def _ncu_traffic(kernel="k_trunc_gram"):
     """DRAM bytes (read + write) per launch of the dominant kernel from the committed
-    ncu --set full capture (profiles/r01d_k_trunc_gram_ncu_raw.csv), or None."""
+    ncu --set full capture (profiles/r01j_k_trunc_gram_ncu_raw.csv), or None."""
     import csv
-    path = os.path.join(ROOT, "profiles", "r01d_k_trunc_gram_ncu_raw.csv")   # full 148-problem launch
+    path = os.path.join(ROOT, "profiles", "r01j_k_trunc_gram_ncu_raw.csv")   # 280-problem launch
     try:
         rows = list(csv.reader(open(path)))
         h, units, v = rows[0], rows[1], rows[2]
@@ -248,7 +248,7 @@ def run_gpu(args):
             "B200 DMMA and DFMA share the FP64 peak)",
             "achieved": achieved, "peak": fp64_peak, "unit": "TFLOP/s", "frac": achieved / fp64_peak,
             "peak_source": fp64_src, "traffic": _ncu_traffic(),
-            "traffic_source": "ncu --set full, one k_trunc_gram launch (profiles/r01d_k_trunc_gram_ncu_raw.csv)",
+            "traffic_source": "ncu --set full, one k_trunc_gram launch (profiles/r01j_k_trunc_gram_ncu_raw.csv, 280 problems)",
             "flops_per_launch": tf / max(tl, 1), "avg_launch_ms": tms / max(tl, 1),
             "share_of_step": tms / args.steps / ms,
             "share_note": "sum of per-launch event times over the concurrent recompression "
