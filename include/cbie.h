@@ -18,6 +18,8 @@
 #ifndef CBIE_H
 #define CBIE_H
 
+#define CBIE_STAR_TABLE 140
+
 #include <stddef.h>
 #include <stdint.h>
 
@@ -65,7 +67,9 @@ void* cbie_stream(cbie_ctx* ctx);
  *   chart_kind   [npatch]              CBIE_CHART_*
  *   chart_params [npatch][8]           cube sphere: radius, face, u_lo, u_hi, v_lo, v_hi
  *                                      (geometry.py:63-68); star: radius, face, u_lo..v_hi
- *   star_coef    [25] real Y_lm coefficients (l<=4) for CBIE_CHART_STAR, else NULL
+ *   star_coef    [CBIE_STAR_TABLE = 140] star-chart monomial tables for CBIE_CHART_STAR, else
+ *                NULL: coefficients of f = sum c_lm Y_lm (l <= 4) and of df/dx, df/dy, df/dz
+ *                over the 35 monomials x^a y^b z^c of degree <= 4 (geometry.py star_tables)
  *   cheb_coef    [npatch][6][3][nu][nv] Chebyshev coefficient tensors of the samples
  *                (position, d/du, d/dv, d2/du2, d2/dudv, d2/dv2; Patch.position_coeffs +
  *                deriv_coeffs, geometry.py:137-143, 228-238) or NULL to compute them

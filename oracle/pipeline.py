@@ -44,6 +44,16 @@ def case(cfg: int) -> Case:
     if cfg == 3:
         mu = ph.Form("muller", vac, ph.Medium.relative(16.0, 1.0, 1.0))
         return Case(sf.sphere_mesh(1.0, 4, (8, 8)), mu, (0, 0, 1), (1, 0, 0), 1e-5, 1.0, 256)
+    if cfg == 4:
+        from paper_2408_17116_b200 import configs
+        from paper_2408_17116_b200.geometry import star_coefficients
+        coef, rng = star_coefficients(configs.STAR_SEED)
+        d = rng.standard_normal(3)
+        d /= np.linalg.norm(d)
+        p = rng.standard_normal(3)
+        p -= (p @ d) * d
+        p /= np.linalg.norm(p)
+        return Case(sf.star_mesh(2.5, 8, (8, 8), coef), mf, tuple(d), tuple(p), 1e-4, 1.0, 256)
     if cfg == 5:
         return Case(sf.sphere_mesh(8.0, 20, (8, 8)), mf, (0, 0, 1), (1, 0, 0), 1e-4, 1.0, 512)
     raise ValueError(f"config {cfg} not available in the oracle")

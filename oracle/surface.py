@@ -156,3 +156,41 @@ def sphere_mesh(radius: float, nsub: int, order: tuple[int, int], edges=None):
                 smp = ch.pos(uu, vv).reshape(nv, nu, 3).transpose(1, 0, 2).copy()
                 out.append(Surf(smp, ch))
     return out
+
+
+class StarChart:
+    """Config-4 star chart: the chart definition of paper_2408_17116_b200.geometry
+    (star_tables / star_eval, pure numpy; the same chart the reference is run with in
+    tests/golden/make_golden_big.py)."""
+
+    def __init__(self, a, face, ulo, uhi, vlo, vhi, tables):
+        self.box = (a, face, ulo, uhi, vlo, vhi)
+        self.tables = tables
+
+    def pos(self, u, v):
+        from paper_2408_17116_b200.geometry import star_eval
+        return star_eval(*self.box, self.tables, np.ravel(u), np.ravel(v))[0]
+
+    def tangents(self, u, v):
+        from paper_2408_17116_b200.geometry import star_eval
+        _, au, av = star_eval(*self.box, self.tables, np.ravel(u), np.ravel(v))
+        return au, av
+
+
+def star_mesh(a: float, nsub: int, order: tuple[int, int], coef):
+    from paper_2408_17116_b200.geometry import star_tables
+    tab = star_tables(coef)
+    nu, nv = order
+    xu, _ = sp.fejer(nu)
+    xv, _ = sp.fejer(nv)
+    uu = np.tile(xu, nv)
+    vv = np.repeat(xv, nu)
+    e = np.linspace(-1.0, 1.0, nsub + 1)
+    out = []
+    for f in range(6):
+        for iu in range(nsub):
+            for iv in range(nsub):
+                ch = StarChart(a, f, e[iu], e[iu + 1], e[iv], e[iv + 1], tab)
+                smp = ch.pos(uu, vv).reshape(nv, nu, 3).transpose(1, 0, 2).copy()
+                out.append(Surf(smp, ch))
+    return out

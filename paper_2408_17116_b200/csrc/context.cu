@@ -134,8 +134,8 @@ void ctx_set_geometry(cbie_ctx* c, int npatch, int nu, int nv, const double* sam
   c->h_kind.assign(kind, kind + npatch);
   c->h_cpar.assign(cpar, cpar + 8 * (size_t)npatch);
   c->h_samples.assign(samples, samples + (size_t)npatch * np * 3);
-  c->h_star.assign(25, 0.0);
-  if (star) c->h_star.assign(star, star + 25);
+  c->h_star.assign(CBIE_STAR_TABLE, 0.0);
+  if (star) c->h_star.assign(star, star + CBIE_STAR_TABLE);
   for (int q = 0; q < npatch; ++q)
     if (kind[q] < 0 || kind[q] > 2) throw cbie_error(CBIE_EINVALID, "unknown chart kind");
   // bbox + diameter of the samples (geometry.py:128-135, quadrature.py:73)

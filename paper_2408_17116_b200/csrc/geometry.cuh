@@ -72,60 +72,27 @@ __device__ __forceinline__ void cube_sphere(const double* __restrict__ par, doub
   }
 }
 
-// Real orthonormal spherical harmonics l = 0..4 (25 functions) as polynomials of
-// the unit vector and their Cartesian gradients (extended homogeneously: the
-// polynomial form is differentiated, then the tangential chain rule above
-// projects it).  Index i = l*l + (m + l).
-__device__ __forceinline__ void star_basis(const double xh[3], double Y[25], double dY[25][3]) {
-  const double x = xh[0], y = xh[1], z = xh[2];
-  const double PI = 3.14159265358979323846;
-  // normalisation constants
-  const double c00 = 0.5 * sqrt(1.0 / PI);
-  const double c1 = sqrt(3.0 / (4.0 * PI));
-  const double c2a = 0.5 * sqrt(15.0 / PI), c2b = 0.25 * sqrt(5.0 / PI), c2c = 0.25 * sqrt(15.0 / PI);
-  const double c3a = 0.25 * sqrt(35.0 / (2.0 * PI)), c3b = 0.5 * sqrt(105.0 / PI),
-               c3c = 0.25 * sqrt(21.0 / (2.0 * PI)), c3d = 0.25 * sqrt(7.0 / PI),
-               c3e = 0.25 * sqrt(105.0 / PI);
-  const double c4a = 0.75 * sqrt(35.0 / PI), c4b = 0.75 * sqrt(35.0 / (2.0 * PI)),
-               c4c = 0.75 * sqrt(5.0 / PI), c4d = 0.75 * sqrt(5.0 / (2.0 * PI)),
-               c4e = (3.0 / 16.0) * sqrt(1.0 / PI), c4f = (3.0 / 8.0) * sqrt(5.0 / PI),
-               c4g = (3.0 / 16.0) * sqrt(35.0 / PI);
-  for (int i = 0; i < 25; ++i) dY[i][0] = dY[i][1] = dY[i][2] = 0.0;
-  // l = 0
-  Y[0] = c00;
-  // l = 1 : m=-1 y, m=0 z, m=1 x
-  Y[1] = c1 * y; dY[1][1] = c1;
-  Y[2] = c1 * z; dY[2][2] = c1;
-  Y[3] = c1 * x; dY[3][0] = c1;
-  // l = 2
-  Y[4] = c2a * x * y; dY[4][0] = c2a * y; dY[4][1] = c2a * x;
-  Y[5] = c2a * y * z; dY[5][1] = c2a * z; dY[5][2] = c2a * y;
-  Y[6] = c2b * (3 * z * z - 1); dY[6][2] = c2b * 6 * z;
-  Y[7] = c2a * x * z; dY[7][0] = c2a * z; dY[7][2] = c2a * x;
-  Y[8] = c2c * (x * x - y * y); dY[8][0] = c2c * 2 * x; dY[8][1] = -c2c * 2 * y;
-  // l = 3
-  Y[9] = c3a * y * (3 * x * x - y * y); dY[9][0] = c3a * 6 * x * y; dY[9][1] = c3a * (3 * x * x - 3 * y * y);
-  Y[10] = c3b * x * y * z; dY[10][0] = c3b * y * z; dY[10][1] = c3b * x * z; dY[10][2] = c3b * x * y;
-  Y[11] = c3c * y * (5 * z * z - 1); dY[11][1] = c3c * (5 * z * z - 1); dY[11][2] = c3c * 10 * y * z;
-  Y[12] = c3d * z * (5 * z * z - 3); dY[12][2] = c3d * (15 * z * z - 3);
-  Y[13] = c3c * x * (5 * z * z - 1); dY[13][0] = c3c * (5 * z * z - 1); dY[13][2] = c3c * 10 * x * z;
-  Y[14] = c3e * z * (x * x - y * y); dY[14][0] = c3e * 2 * x * z; dY[14][1] = -c3e * 2 * y * z; dY[14][2] = c3e * (x * x - y * y);
-  Y[15] = c3a * x * (x * x - 3 * y * y); dY[15][0] = c3a * (3 * x * x - 3 * y * y); dY[15][1] = -c3a * 6 * x * y;
-  // l = 4
-  Y[16] = c4a * x * y * (x * x - y * y); dY[16][0] = c4a * (3 * x * x * y - y * y * y); dY[16][1] = c4a * (x * x * x - 3 * x * y * y);
-  Y[17] = c4b * y * z * (3 * x * x - y * y); dY[17][0] = c4b * 6 * x * y * z; dY[17][1] = c4b * z * (3 * x * x - 3 * y * y); dY[17][2] = c4b * y * (3 * x * x - y * y);
-  Y[18] = c4c * x * y * (7 * z * z - 1); dY[18][0] = c4c * y * (7 * z * z - 1); dY[18][1] = c4c * x * (7 * z * z - 1); dY[18][2] = c4c * 14 * x * y * z;
-  Y[19] = c4d * y * z * (7 * z * z - 3); dY[19][1] = c4d * z * (7 * z * z - 3); dY[19][2] = c4d * y * (21 * z * z - 3);
-  Y[20] = c4e * (35 * z * z * z * z - 30 * z * z + 3); dY[20][2] = c4e * (140 * z * z * z - 60 * z);
-  Y[21] = c4d * x * z * (7 * z * z - 3); dY[21][0] = c4d * z * (7 * z * z - 3); dY[21][2] = c4d * x * (21 * z * z - 3);
-  Y[22] = c4f * (x * x - y * y) * (7 * z * z - 1); dY[22][0] = c4f * 2 * x * (7 * z * z - 1); dY[22][1] = -c4f * 2 * y * (7 * z * z - 1); dY[22][2] = c4f * (x * x - y * y) * 14 * z;
-  Y[23] = c4b * x * z * (x * x - 3 * y * y); dY[23][0] = c4b * z * (3 * x * x - 3 * y * y); dY[23][1] = -c4b * 6 * x * y * z; dY[23][2] = c4b * x * (x * x - 3 * y * y);
-  Y[24] = c4g * (x * x * (x * x - 3 * y * y) - y * y * (3 * x * x - y * y)); dY[24][0] = c4g * (4 * x * x * x - 12 * x * y * y); dY[24][1] = c4g * (4 * y * y * y - 12 * x * x * y);
+// Star body (config 4): r(xhat) = a (1 + f(xhat)) xhat, f = sum_lm c_lm Y_lm, l <= 4,
+// composed with the cube -> sphere direction map.  The host expands f and its
+// Cartesian gradient into the 35 monomials x^a y^b z^c of degree <= 4
+// (geometry.py star_tables: star[0..34] = f, [35..69] = df/dx, [70..104] = df/dy,
+// [105..139] = df/dz) and evaluates them with the same explicitly rounded
+// operation order (geometry.py star_eval), so chart positions and tangents are
+// bit-identical on host and device.
+__device__ __forceinline__ double star_poly(const double* __restrict__ F, const double px[5],
+                                            const double py[5], const double pz[5]) {
+  double s = 0.0;
+  int m = 0;
+#pragma unroll
+  for (int deg = 0; deg <= 4; ++deg)
+#pragma unroll
+    for (int a = deg; a >= 0; --a)
+#pragma unroll
+      for (int b = deg - a; b >= 0; --b, ++m)
+        s = RN_ADD(s, RN_MUL(RN_MUL(RN_MUL(F[m], px[a]), py[b]), pz[deg - a - b]));
+  return s;
 }
 
-// Star body: r(xhat) = a (1 + amp * f(xhat)) xhat with f a real Y_lm sum, l <= 4,
-// composed with the cube -> sphere direction map.  star[0] = a*amp scale folded
-// on the host: rad(xhat) = par[0] * (1 + sum_i star[i] Y_i(xhat)).
 __device__ __forceinline__ void star_chart(const double* __restrict__ par,
                                            const double* __restrict__ star, double u, double v,
                                            double pos[3], double au[3], double av[3]) {
@@ -135,35 +102,40 @@ __device__ __forceinline__ void star_chart(const double* __restrict__ par,
   const int ax = kFace[face][0], ua = kFace[face][2], va = kFace[face][3];
   double x[3];
   x[ax] = (double)kFace[face][1];
-  x[ua] = ulo + (u + 1.0) * 0.5 * (uhi - ulo);
-  x[va] = vlo + (v + 1.0) * 0.5 * (vhi - vlo);
-  const double hu = 0.5 * (uhi - ulo), hv = 0.5 * (vhi - vlo);
-  const double nrm = sqrt(x[0] * x[0] + x[1] * x[1] + x[2] * x[2]);
+  x[ua] = RN_ADD(ulo, RN_MUL(RN_MUL(RN_ADD(u, 1.0), 0.5), RN_SUB(uhi, ulo)));
+  x[va] = RN_ADD(vlo, RN_MUL(RN_MUL(RN_ADD(v, 1.0), 0.5), RN_SUB(vhi, vlo)));
+  const double hu = RN_MUL(0.5, RN_SUB(uhi, ulo)), hv = RN_MUL(0.5, RN_SUB(vhi, vlo));
+  const double nrm =
+      __dsqrt_rn(RN_ADD(RN_ADD(RN_MUL(x[0], x[0]), RN_MUL(x[1], x[1])), RN_MUL(x[2], x[2])));
   double xh[3], tu[3], tv[3];
 #pragma unroll
-  for (int i = 0; i < 3; ++i) xh[i] = x[i] / nrm;
+  for (int i = 0; i < 3; ++i) xh[i] = RN_DIV(x[i], nrm);
+#pragma unroll
+  for (int i = 0; i < 3; ++i) {    // d xhat / du, d xhat / dv
+    tu[i] = RN_DIV(RN_SUB((i == ua) ? hu : 0.0, RN_MUL(RN_MUL(xh[i], xh[ua]), hu)), nrm);
+    tv[i] = RN_DIV(RN_SUB((i == va) ? hv : 0.0, RN_MUL(RN_MUL(xh[i], xh[va]), hv)), nrm);
+  }
+  double px[5], py[5], pz[5];
+  px[0] = py[0] = pz[0] = 1.0;
+  px[1] = xh[0]; py[1] = xh[1]; pz[1] = xh[2];
+#pragma unroll
+  for (int k = 2; k <= 4; ++k) {
+    px[k] = RN_MUL(px[k - 1], xh[0]);
+    py[k] = RN_MUL(py[k - 1], xh[1]);
+    pz[k] = RN_MUL(pz[k - 1], xh[2]);
+  }
+  const double f = star_poly(star, px, py, pz);
+  const double gx = star_poly(star + 35, px, py, pz);
+  const double gy = star_poly(star + 70, px, py, pz);
+  const double gz = star_poly(star + 105, px, py, pz);
+  const double r = RN_MUL(a, RN_ADD(1.0, f));
+  const double dru = RN_MUL(a, RN_ADD(RN_ADD(RN_MUL(gx, tu[0]), RN_MUL(gy, tu[1])), RN_MUL(gz, tu[2])));
+  const double drv = RN_MUL(a, RN_ADD(RN_ADD(RN_MUL(gx, tv[0]), RN_MUL(gy, tv[1])), RN_MUL(gz, tv[2])));
 #pragma unroll
   for (int i = 0; i < 3; ++i) {
-    tu[i] = (((i == ua) ? hu : 0.0) - xh[i] * xh[ua] * hu) / nrm;   // d xhat / du
-    tv[i] = (((i == va) ? hv : 0.0) - xh[i] * xh[va] * hv) / nrm;
-  }
-  double Y[25], dY[25][3];
-  star_basis(xh, Y, dY);
-  double f = 0.0, gf[3] = {0.0, 0.0, 0.0};
-  for (int i = 0; i < 25; ++i) {
-    f += star[i] * Y[i];
-    gf[0] += star[i] * dY[i][0];
-    gf[1] += star[i] * dY[i][1];
-    gf[2] += star[i] * dY[i][2];
-  }
-  const double r = a * (1.0 + f);
-  const double dru = a * (gf[0] * tu[0] + gf[1] * tu[1] + gf[2] * tu[2]);
-  const double drv = a * (gf[0] * tv[0] + gf[1] * tv[1] + gf[2] * tv[2]);
-#pragma unroll
-  for (int i = 0; i < 3; ++i) {
-    pos[i] = r * xh[i];
-    au[i] = dru * xh[i] + r * tu[i];
-    av[i] = drv * xh[i] + r * tv[i];
+    pos[i] = RN_MUL(r, xh[i]);
+    au[i] = RN_ADD(RN_MUL(dru, xh[i]), RN_MUL(r, tu[i]));
+    av[i] = RN_ADD(RN_MUL(drv, xh[i]), RN_MUL(r, tv[i]));
   }
 }
 

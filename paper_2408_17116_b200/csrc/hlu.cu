@@ -14,6 +14,7 @@
 #include <chrono>
 #include <cstring>
 #include <map>
+#include <mutex>
 
 #include "hlu_kernels.cuh"
 #include <array>
@@ -511,6 +512,7 @@ struct cbie_hlu {
   int64_t leaf_end = 0;
   int64_t npiv = 0;
   int nslot_leaf = 0;
+  int cap_boost = 1;               // factor leaf capacity multiplier (raised on truncation overflow)
   std::map<std::string, double> stat;
 };
 
@@ -1576,6 +1578,21 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
       }
       ex.crit_ms = best >= 0 ? fin[best] : 0.0;
       for (int g = best; g >= 0; g = from[g]) ex.crit_kind_ms[P.groups[g].kind] += ex.gms[g];
+      if (getenv("CBIE_CRIT_DUMP")) {   // debug: the groups on the critical path
+        for (int g = best; g >= 0; g = from[g]) {
+          const auto& gr = P.groups[g];
+          int mx = 0, kx = 0, nd = 0;
+          if (gr.kind == OP_TRUNC)
+            for (int i = 0; i < gr.count; ++i) {
+              const TruncDesc& td = P.tr[gr.start + i];
+              mx = std::max(mx, std::max(td.m, td.n));
+              kx = std::max(kx, td.k);
+              nd += td.in_v < 0;
+            }
+          fprintf(stderr, "CRIT g=%d L=%d K=%d n=%d ms=%.3f mn=%d k=%d dense=%d\n", g, gr.level, gr.kind, gr.count,
+                  ex.gms[g], mx, kx, nd);
+        }
+      }
     }
   }
   if (ms) {
@@ -1633,7 +1650,14 @@ struct PlanCache {
   TruncWork tw[2 * TRUNC_LANES];   // recompression workspaces (two per lane)
   int64_t leaf_end = 0;
 };
-std::unique_ptr<PlanCache> g_plan_cache;
+// per device (a process may drive contexts on several GPUs), guarded by g_hlu_mutex
+std::map<int, std::unique_ptr<PlanCache>> g_plan_caches;
+std::recursive_mutex g_hlu_mutex;
+int cur_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
 
 uint64_t fnv(uint64_t h, int64_t v) {
   for (int i = 0; i < 8; ++i) {
@@ -1648,6 +1672,8 @@ uint64_t fnv(uint64_t h, int64_t v) {
 
 // drop the cached H-LU workspace when HBM is needed elsewhere
 void hlu_trim_cache(bool force) {
+  std::lock_guard<std::recursive_mutex> lk(g_hlu_mutex);
+  auto& g_plan_cache = g_plan_caches[cur_device()];
   if (!g_plan_cache) return;
   size_t fr = 0, tot = 0;
   fr = mem_free_bytes(&tot);
@@ -1679,7 +1705,7 @@ static int64_t hlu_layout(cbie_hlu* F, std::vector<CopySeg>& segs) {
       segs.push_back(CopySeg{L0.off_d, L.off_d, (int64_t)L.m * L.n});
     } else {
       const int r = H->h_rank[li];
-      L.cap = std::max(1, std::min(std::max(1, std::min(L.m, L.n) / 2), 2 * r + 48));
+      L.cap = std::max(1, std::min(std::max(1, std::min(L.m, L.n) / 2), F->cap_boost * (2 * r + 48)));
       L.off_u = leaf_end;
       leaf_end += (int64_t)L.m * L.cap;
       L.off_v = leaf_end;
@@ -1753,6 +1779,7 @@ static void hlu_factor_impl(cbie_hlu* F) {
   }
   key = fnv(key, (int64_t)(F->tol * 1e15));
   const bool use_cache = getenv("CBIE_NO_PLAN_CACHE") == nullptr;
+  auto& g_plan_cache = g_plan_caches[c->device];
   auto t0 = std::chrono::steady_clock::now();
   if (!(use_cache && g_plan_cache && g_plan_cache->key == key)) {
     g_plan_cache.reset();   // release the previous plan's workspace first
@@ -1854,6 +1881,13 @@ static void hlu_factor_impl(cbie_hlu* F) {
       F->stat["dense_lr_mean_l"] = dk.empty() ? 0.0 : s / dk.size();
     }
     F->stat["trunc_alg_bytes"] = bytes;
+    // HLUFactors.stored_scalars (hmatrix.py:818-821): dense / LU leaves m n, low-rank (m + n) r
+    double stored = 0.0;
+    for (int li = 0; li < nleaf; ++li) {
+      const auto& L = T.leaves[li];
+      stored += L.kind == BLK_DENSE ? (double)L.m * L.n : (double)(L.m + L.n) * rk[li];
+    }
+    F->stat["stored_scalars"] = stored;
   }
   {
     const char* nm[OP_NKIND] = {"gemm", "ew", "concat", "trsm", "getrf", "trunc", "dense_lr"};
@@ -1904,11 +1938,13 @@ struct SolveCache {
   DBuf<unsigned long long> ovf;
   TruncWork tw[2 * TRUNC_LANES];
 };
-std::unique_ptr<SolveCache> g_solve_cache;
-int64_t g_solve_leaf_end = -1;
+std::map<int, std::unique_ptr<SolveCache>> g_solve_caches;
+std::map<int, int64_t> g_solve_leaf_ends;
 
 static int64_t solve_cache_temps(int64_t leaf_end) {
-  return (g_solve_cache && g_solve_leaf_end == leaf_end) ? g_solve_cache->pool_top : 0;
+  const int d = cur_device();
+  auto& g_solve_cache = g_solve_caches[d];
+  return (g_solve_cache && g_solve_leaf_ends[d] == leaf_end) ? g_solve_cache->pool_top : 0;
 }
 
 static void hlu_solve_impl(cbie_hlu* F, const zc* b, zc* x, int nrhs) {
@@ -1925,6 +1961,7 @@ static void hlu_solve_impl(cbie_hlu* F, const zc* b, zc* x, int nrhs) {
       const int64_t ni = (int64_t)p * C + c, oi = (int64_t)T.pperm[p] * C + c;
       for (int r = 0; r < nrhs; ++r) bp[(size_t)r * N + ni] = b[(size_t)oi * nrhs + r];
     }
+  auto& g_solve_cache = g_solve_caches[H->ctx->device];
   uint64_t key = 1469598103934665603ull;
   key = fnv(key, nleaf);
   key = fnv(key, nrhs);
@@ -1940,7 +1977,9 @@ static void hlu_solve_impl(cbie_hlu* F, const zc* b, zc* x, int nrhs) {
     auto sc = std::make_unique<SolveCache>();
     Recorder& R = sc->plan.R;
     R.leaf_end = F->leaf_end;
-    R.pool_budget = (int64_t)1 << 40;
+    // temporaries are right-hand-side-sized vectors; the solve runs level by level on one
+    // stream, so chunk reuse costs no parallelism: a few dozen vectors' worth suffices
+    R.pool_budget = std::max<int64_t>((int64_t)N * nrhs * 32, (int64_t)1 << 24);
     for (int li = 0; li < nleaf; ++li) {
       R.new_buf();
       R.new_slot(0, li);
@@ -1959,7 +1998,7 @@ static void hlu_solve_impl(cbie_hlu* F, const zc* b, zc* x, int nrhs) {
     sc->ovf.alloc(1);
     sc->key = key;
     g_solve_cache = std::move(sc);
-    g_solve_leaf_end = F->leaf_end;
+    g_solve_leaf_ends[H->ctx->device] = F->leaf_end;
   }
   SolveCache& SC = *g_solve_cache;
   // arena for the solve: factors (shared) + temps: allocate temps after the factor arena
@@ -2013,10 +2052,23 @@ int cbie_hlu_factor(cbie_hmat* h, double trunc_tol, cbie_hlu** out) {
     cudaSetDevice(h->ctx->device);
     if (!(trunc_tol > 0.0 && trunc_tol < 1.0)) throw cbie_error(CBIE_EINVALID, "trunc_tol in (0,1)");
     if (h->partial) throw cbie_error(CBIE_ESTATE, "partial (sharded) H-matrix: exchange the shards first");
+    std::lock_guard<std::recursive_mutex> lk(g_hlu_mutex);
     F = new cbie_hlu();
     F->H = h;
     F->tol = trunc_tol;
-    hlu_factor_impl(F);
+    // a recompression whose kept rank exceeds its leaf's factor capacity (2 r + 48) is
+    // clipped and counted; re-factor with larger capacities until none is clipped (the
+    // reference keeps every singular value above tol * s_0).  At the demotion budget
+    // min(m, n) / 2 everywhere a clipped truncation is a RankOverflow.
+    for (int attempt = 0;; ++attempt) {
+      hlu_factor_impl(F);
+      if (F->stat["trunc_overflow"] == 0) break;
+      if (F->cap_boost >= (1 << 12))
+        throw cbie_error(CBIE_ERANK_OVERFLOW, "H-LU recompression rank exceeds the leaf budget");
+      F->cap_boost *= 4;
+      F->stat["cap_retries"] = attempt + 1;
+    }
+    F->stat["cap_boost"] = F->cap_boost;
     *out = F;
   } catch (const cbie_error& e) {
     h->ctx->err = e.what();
@@ -2033,10 +2085,13 @@ static int hlu_factor_dist_entry(cbie_hmat* h, double trunc_tol, int world, bool
     cudaSetDevice(h->ctx->device);
     if (!(trunc_tol > 0.0 && trunc_tol < 1.0)) throw cbie_error(CBIE_EINVALID, "trunc_tol in (0,1)");
     if (h->partial) throw cbie_error(CBIE_ESTATE, "partial (sharded) H-matrix: exchange the shards first");
+    std::lock_guard<std::recursive_mutex> lk(g_hlu_mutex);
     F = new cbie_hlu();
     F->H = h;
     F->tol = trunc_tol;
     hlu_factor_dist_impl(F, world, emulated);
+    if (F->stat["trunc_overflow"] > 0)
+      throw cbie_error(CBIE_ERANK_OVERFLOW, "distributed H-LU: a recompression was clipped at its leaf capacity");
     *out = F;
   } catch (const cbie_error& e) {
     h->ctx->err = e.what();
@@ -2158,6 +2213,7 @@ int cbie_hlu_leaf(cbie_hlu* f, int64_t leaf, int* kind, int* rank, cbie_c128* D_
 
 int cbie_hlu_solve(cbie_hlu* f, const cbie_c128* b, cbie_c128* x, int nrhs) {
   try {
+    std::lock_guard<std::recursive_mutex> lk(g_hlu_mutex);
     cudaSetDevice(f->H->ctx->device);
     hlu_solve_impl(f, reinterpret_cast<const zc*>(b), reinterpret_cast<zc*>(x), nrhs);
   } catch (const cbie_error& e) {

@@ -629,7 +629,10 @@ constexpr int GCH = 64;             // rows staged per Gram chunk
 constexpr int GSQ = KG * KG;        // one k x k region (zc)
 constexpr int GLD = KG + 1;         // staged row stride (bank spread)
 constexpr double CHOL_EPS = 1e-13;  // pivoted-Cholesky stop (squared, relative)
-constexpr double GDELTA = 0.2;      // core reduction: directions below GDELTA * tol * s_0 dropped before the Jacobi
+// core reduction before the Jacobi: the pivoted Cholesky of H = M M^H stops once the
+// remaining directions together carry at most GDELTA * tol * s_0 (Frobenius, the trace
+// of the Schur complement), so what is dropped stays well inside the tol * s_0 cut
+constexpr double GDELTA = 0.2;
 
 __host__ __device__ inline int64_t gram_scratch_per() { return 4 * (int64_t)GSQ + 64; }
 
@@ -713,8 +716,10 @@ __device__ void gram_acc(const zc* __restrict__ X, int m, int k, int ldx, zc* G,
 
 // pivoted Cholesky of the Hermitian G (k x k, ld k, shared) in place: row j < kk of G
 // holds row j of R (columns in pivoted order, entries >= j); perm[j] = original
-// column of pivot j.  Returns kk (pivots above thr_rel * max diagonal).
-__device__ int pchol(zc* G, int k, int* perm, double thr_rel, Smem& S) {
+// column of pivot j.  Returns kk: stops when the largest remaining pivot is <= thr_rel *
+// max diagonal, or (trace_stop) when the remaining trace -- the squared Frobenius norm of
+// what the remaining directions carry when G = M M^H -- is <= thr_rel * max diagonal.
+__device__ int pchol(zc* G, int k, int* perm, double thr_rel, Smem& S, bool trace_stop = false) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int c = threadIdx.x; c < k; c += NT) perm[c] = c;
   double dmax = 0.0;
@@ -724,10 +729,11 @@ __device__ int pchol(zc* G, int k, int* perm, double thr_rel, Smem& S) {
   int j = 0;
   for (; j < k; ++j) {
     if (w == 0) {
-      double best = -1.0;
+      double best = -1.0, tr = 0.0;
       int bi = k;
       for (int c = j + lane; c < k; c += 32) {
         const double v = G[c * k + c].x;
+        tr += fmax(v, 0.0);
         if (v > best) {
           best = v;
           bi = c;
@@ -737,12 +743,13 @@ __device__ int pchol(zc* G, int k, int* perm, double thr_rel, Smem& S) {
       for (int o = 16; o > 0; o >>= 1) {
         const double ob = __shfl_xor_sync(FULL, best, o);
         const int oi = __shfl_xor_sync(FULL, bi, o);
+        tr += __shfl_xor_sync(FULL, tr, o);
         if (ob > best || (ob == best && oi < bi)) {
           best = ob;
           bi = oi;
         }
       }
-      const bool go = best > thr && best > 0.0;
+      const bool go = (trace_stop ? tr > thr : best > thr) && best > 0.0;
       if (lane == 0) S.flag = go ? 0 : 1;
       if (go) {
         if (bi != j) {
@@ -985,8 +992,9 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   __syncthreads();
   const int kk1 = ku, kk2 = kv;
   // 5. SVD of the core through H = M M^H, preconditioned: pivoted Cholesky
-  //    P^T H P = R^H R (stopped at (DELTA tol)^2 of the largest pivot, as the old
-  //    pivoted-QR reduction), then the graded G = R R^H = Z S^2 Z^H by two-sided
+  //    P^T H P = R^H R (stopped once the remaining trace is <= (GDELTA tol)^2 of the
+  //    largest diagonal, i.e. the dropped directions carry <= GDELTA tol s_0 together),
+  //    then the graded G = R R^H = Z S^2 Z^H by two-sided
   //    Jacobi (few sweeps).  Left singular vectors times S: W = P R^H Z; right
   //    singular vectors: Vhat = M^H W / S^2.  Singular values below ~sqrt(eps) s_0
   //    are not resolved, far below tol * s_0.
@@ -999,7 +1007,7 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   }
   for (int e = threadIdx.x; e < kk1 * kk2; e += NT) Mg[e] = X2[e];
   __syncthreads();
-  const int kp = pchol(H, kk1, S.perm, (GDELTA * tol) * (GDELTA * tol), S);
+  const int kp = pchol(H, kk1, S.perm, (GDELTA * tol) * (GDELTA * tol), S, true);
   zc* Gp = Gv;   // R R^H (kp x kp)
   zc* Z = X2;    // eigenvectors (kp x kp)
   for (int e = threadIdx.x; e < kp * kp; e += NT) {

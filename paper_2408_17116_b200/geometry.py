@@ -58,13 +58,33 @@ class CubeSphereFace:
                          0.0, 0.0])
 
 
-def real_sh(xyz: np.ndarray) -> np.ndarray:
+class _ShList:
+    """Y[:, i] = value assignment sink for real_sh's polynomial mode."""
+
+    def __init__(self, items):
+        self.items = items
+
+    def __setitem__(self, key, val):
+        self.items[key[1]] = val
+
+
+def real_sh(xyz, polys=None):
     """25 real orthonormal spherical harmonics l <= 4 at unit vectors (n,3);
-    index l*l + (m+l), same polynomial forms as csrc/geometry.cuh star_basis."""
-    x, y, z = xyz[:, 0], xyz[:, 1], xyz[:, 2]
+    index l*l + (m+l).  With ``polys=(X, Y, Z)`` the same forms are built as
+    _Poly objects (exact monomial expansion, star_tables)."""
+    if polys is not None:
+        x, y, z = polys
+        Y = [None] * 25
+    else:
+        x, y, z = xyz[:, 0], xyz[:, 1], xyz[:, 2]
+        Y = np.empty((xyz.shape[0], 25))
     pi = np.pi
-    Y = np.empty((xyz.shape[0], 25))
-    Y[:, 0] = 0.5 * np.sqrt(1 / pi)
+    Y0 = 0.5 * np.sqrt(1 / pi)
+    if polys is not None:
+        Y = _ShList(Y)
+        Y[:, 0] = x * 0.0 + Y0
+    else:
+        Y[:, 0] = Y0
     c1 = np.sqrt(3 / (4 * pi))
     Y[:, 1], Y[:, 2], Y[:, 3] = c1 * y, c1 * z, c1 * x
     c2a, c2b, c2c = 0.5 * np.sqrt(15 / pi), 0.25 * np.sqrt(5 / pi), 0.25 * np.sqrt(15 / pi)
@@ -91,23 +111,159 @@ def real_sh(xyz: np.ndarray) -> np.ndarray:
     Y[:, 22] = c4f * (x * x - y * y) * (7 * z * z - 1)
     Y[:, 23] = c4b * x * z * (x * x - 3 * y * y)
     Y[:, 24] = c4g * (x * x * (x * x - 3 * y * y) - y * y * (3 * x * x - y * y))
-    return Y
+    return Y.items if polys is not None else Y
+
+
+def _monomials():
+    """The 35 monomials x^a y^b z^c of degree <= 4, in the device's order."""
+    return [(a, b, deg - a - b) for deg in range(5) for a in range(deg, -1, -1)
+            for b in range(deg - a, -1, -1)]
+
+
+class _Poly(dict):
+    """Polynomial in x, y, z as {(a, b, c): coefficient} (exact expansion of real_sh)."""
+
+    def __add__(self, o):
+        o = o if isinstance(o, _Poly) else _Poly({(0, 0, 0): float(o)})
+        r = _Poly(self)
+        for k, v in o.items():
+            r[k] = r.get(k, 0.0) + v
+        return r
+
+    __radd__ = __add__
+
+    def __neg__(self):
+        return _Poly({k: -v for k, v in self.items()})
+
+    def __sub__(self, o):
+        return self + (-o if isinstance(o, _Poly) else -float(o))
+
+    def __rsub__(self, o):
+        return (-self) + o
+
+    def __mul__(self, o):
+        if not isinstance(o, _Poly):
+            return _Poly({k: v * o for k, v in self.items()})
+        r = _Poly()
+        for k1, v1 in self.items():
+            for k2, v2 in o.items():
+                k = (k1[0] + k2[0], k1[1] + k2[1], k1[2] + k2[2])
+                r[k] = r.get(k, 0.0) + v1 * v2
+        return r
+
+    __rmul__ = __mul__
+
+    def __pow__(self, n):
+        r = _Poly({(0, 0, 0): 1.0})
+        for _ in range(n):
+            r = r * self
+        return r
+
+    def diff(self, axis):
+        r = _Poly()
+        for k, v in self.items():
+            if k[axis]:
+                kk = list(k)
+                kk[axis] -= 1
+                r[tuple(kk)] = r.get(tuple(kk), 0.0) + v * k[axis]
+        return r
+
+
+_STAR_TABLES: dict = {}
+
+
+def star_tables(coef) -> np.ndarray:
+    """[4 * 35] monomial coefficients of f = sum_i coef_i Y_i and of its Cartesian
+    gradient (the CBIE_STAR_TABLE layout of include/cbie.h).  Y_i are real_sh's
+    polynomial forms expanded exactly; the tables *define* the star chart on
+    host and device alike."""
+    key = np.asarray(coef, float).tobytes()
+    if key in _STAR_TABLES:
+        return _STAR_TABLES[key]
+    X = _Poly({(1, 0, 0): 1.0})
+    Y = _Poly({(0, 1, 0): 1.0})
+    Z = _Poly({(0, 0, 1): 1.0})
+    f = _Poly()
+    for c, p in zip(np.asarray(coef, float), real_sh(None, polys=(X, Y, Z))):
+        f = f + p * float(c)
+    mons = _monomials()
+    out = np.zeros((4, len(mons)))
+    for t, poly in enumerate((f, f.diff(0), f.diff(1), f.diff(2))):
+        for m, k in enumerate(mons):
+            out[t, m] = poly.get(k, 0.0)
+    _STAR_TABLES[key] = out.ravel()
+    return _STAR_TABLES[key]
+
+
+def _star_poly(F, px, py, pz):
+    s = np.zeros_like(px[1])
+    for m, (a, b, c) in enumerate(_monomials()):
+        s = s + ((F[m] * px[a]) * py[b]) * pz[c]
+    return s
+
+
+def star_eval(a, face, ulo, uhi, vlo, vhi, tables, u, v):
+    """Star chart position and tangents (csrc/geometry.cuh star_chart; every
+    operation elementwise in the same order, so both round identically).
+    u, v: 1-D arrays; returns (pos, a_u, a_v), each (n, 3)."""
+    ax, sg, ua, va = _FACES[face]
+    u = np.atleast_1d(np.asarray(u, float))
+    v = np.atleast_1d(np.asarray(v, float))
+    x = [None, None, None]
+    x[ax] = np.full(u.shape, float(sg))
+    x[ua] = ulo + ((u + 1.0) * 0.5) * (uhi - ulo)
+    x[va] = vlo + ((v + 1.0) * 0.5) * (vhi - vlo)
+    hu, hv = 0.5 * (uhi - ulo), 0.5 * (vhi - vlo)
+    nrm = np.sqrt((x[0] * x[0] + x[1] * x[1]) + x[2] * x[2])
+    xh = [xi / nrm for xi in x]
+    tu = [((hu if i == ua else 0.0) - (xh[i] * xh[ua]) * hu) / nrm for i in range(3)]
+    tv = [((hv if i == va else 0.0) - (xh[i] * xh[va]) * hv) / nrm for i in range(3)]
+    one = np.ones(u.shape)
+    px, py, pz = [one, xh[0]], [one, xh[1]], [one, xh[2]]
+    for _ in range(3):
+        px.append(px[-1] * xh[0])
+        py.append(py[-1] * xh[1])
+        pz.append(pz[-1] * xh[2])
+    T = np.asarray(tables, float).reshape(4, 35)
+    f = _star_poly(T[0], px, py, pz)
+    gx = _star_poly(T[1], px, py, pz)
+    gy = _star_poly(T[2], px, py, pz)
+    gz = _star_poly(T[3], px, py, pz)
+    r = a * (1.0 + f)
+    dru = a * ((gx * tu[0] + gy * tu[1]) + gz * tu[2])
+    drv = a * ((gx * tv[0] + gy * tv[1]) + gz * tv[2])
+    pos = np.stack([r * xh[i] for i in range(3)], -1)
+    au = np.stack([dru * xh[i] + r * tu[i] for i in range(3)], -1)
+    av = np.stack([drv * xh[i] + r * tv[i] for i in range(3)], -1)
+    return pos, au, av
 
 
 @dataclass
 class StarFace(CubeSphereFace):
-    """Seeded smooth star-shaped body r(xhat) = a (1 + sum_i s_i Y_i(xhat)) on a
+    """Seeded smooth star-shaped body r(xhat) = a (1 + sum_i c_i Y_i(xhat)) xhat on a
     cube-sphere face (config 4; not expressible by the reference's API, built as
     a Chart per SURVEY.md section 7 hard part 6).  ``coef`` already carries the
-    0.2 / max|sum c Y| normalisation."""
+    0.2 / max|sum c Y| normalisation; the chart is evaluated from its monomial
+    tables (``star_tables``), identically on host and device."""
     coef: Optional[np.ndarray] = None
     kind = CHART_STAR
 
+    def tables(self):
+        t = getattr(self, "_tables", None)
+        if t is None:
+            t = self._tables = star_tables(self.coef)
+        return t
+
     def positions(self, u, v):
-        xh = self.direction(u, v)
-        shp = xh.shape
-        f = real_sh(xh.reshape(-1, 3)) @ self.coef
-        return (self.radius * (1.0 + f)).reshape(shp[:-1] + (1,)) * xh
+        u = np.asarray(u, float)
+        return star_eval(self.radius, self.face, self.u_lo, self.u_hi, self.v_lo, self.v_hi,
+                         self.tables(), u.ravel(), np.asarray(v, float).ravel())[0].reshape(
+                             u.shape + (3,))
+
+    def derivatives(self, u, v):
+        _, au, av = star_eval(self.radius, self.face, self.u_lo, self.u_hi, self.v_lo, self.v_hi,
+                              self.tables(), u, v)
+        return au, av
 
 
 @dataclass
@@ -241,5 +397,5 @@ def device_arrays(patches: list[Patch]):
         kind[i] = p.chart.kind
         par[i] = p.chart.params()
         if p.chart.kind == CHART_STAR:
-            star = np.ascontiguousarray(p.chart.coef, dtype=float)
+            star = np.ascontiguousarray(p.chart.tables(), dtype=float)
     return smp, kind, par, star, np.ascontiguousarray(cheb_coefficients(patches))

@@ -122,12 +122,32 @@ class HMatrix:
         return 1.0 - self.stored_scalars() / float(self.N) ** 2
 
     def diagnostics(self) -> dict:
+        """Per-level leaf counts, rank histogram, memory by leaf kind (HMatrix.diagnostics,
+        hmatrix.py:290-308; same keys)."""
         perm, lv = self.tree()
-        ranks: dict[str, int] = {}
+        npts = self.N // self.C
+        ranks: dict[int, int] = {}
+        levels: dict[int, dict[str, int]] = {}
+        mem = {"dense": 0, "lowrank": 0}
         for row in lv:
+            lo, hi, lvl = 0, npts, 0          # depth of the row cluster (median split, hmatrix.py:62-75)
+            while (lo, hi) != (int(row[0]), int(row[1])):
+                mid = lo + (hi - lo) // 2
+                lo, hi = (lo, mid) if row[0] < mid else (mid, hi)
+                lvl += 1
+            m, n = int(row[1] - row[0]) * self.C, int(row[3] - row[2]) * self.C
+            kind = "lowrank" if row[4] == 1 else "dense"
+            lk = levels.setdefault(lvl, {})
+            lk[kind] = lk.get(kind, 0) + 1
             if row[4] == 1:
-                ranks[str(int(row[5]))] = ranks.get(str(int(row[5])), 0) + 1
-        return {"rank_histogram": dict(sorted(ranks.items(), key=lambda t: int(t[0]))),
+                r = int(row[5])
+                ranks[r] = ranks.get(r, 0) + 1
+                mem["lowrank"] += (m + n) * r * 16
+            else:
+                mem["dense"] += m * n * 16
+        return {"levels": {str(k): v for k, v in sorted(levels.items())},
+                "rank_histogram": {str(k): v for k, v in sorted(ranks.items())},
+                "memory_bytes": mem,
                 "compression_rate": self.compression_rate(),
                 "demoted_blocks": self.demoted,
                 "n_leaves": int(lv.shape[0])}
@@ -170,6 +190,13 @@ class HLUFactors:
 
     def stats(self) -> dict:
         return dict(self._stats)
+
+    def stored_scalars(self) -> int:
+        """Scalars held by the factors (HLUFactors.stored_scalars, hmatrix.py:818-821)."""
+        return int(self._stats["stored_scalars"])
+
+    def memory_bytes(self) -> int:
+        return self.stored_scalars() * 16
 
     def solve_stats(self) -> dict:
         """Device statistics of the last solve (levels, launches, device ms)."""

@@ -76,11 +76,45 @@ class PlaneWave:
         object.__setattr__(self, "polarization", p)
 
 
-def rhs_rows(spec: FormulationSpec, exc: PlaneWave, pos, a_u, a_v) -> np.ndarray:
-    """Tested incident rows per point, (n, C) (kernels.py:141-149, 334-349)."""
+@dataclass(frozen=True)
+class Dipole:
+    """Infinitesimal electric dipole with moment p (C m) (kernels.py:126-135)."""
+    position: np.ndarray
+    moment: np.ndarray
+
+    def __post_init__(self):
+        object.__setattr__(self, "position", np.asarray(self.position, float))
+        object.__setattr__(self, "moment", np.asarray(self.moment, float))
+
+
+def incident_fields(exc, medium: Medium, points: np.ndarray):
+    """(E, H) of the excitation at the points, (n, 3) each (kernels.py:141-166)."""
+    pts = np.atleast_2d(np.asarray(points, float))
+    k = medium.k
+    if isinstance(exc, PlaneWave):
+        E = exc.amplitude * np.exp(-1j * k * (pts @ exc.direction))[:, None] * exc.polarization[None, :]
+        return E, np.cross(exc.direction, E) / medium.eta
+    if isinstance(exc, Dipole):
+        from .errors import SingularPoint
+        rel = pts - exc.position
+        R = np.linalg.norm(rel, axis=1)
+        if np.any(R < 1e-14):
+            raise SingularPoint("field point coincides with the dipole")
+        rhat = rel / R[:, None]
+        ekr = np.exp(-1j * k * R)
+        rxp = np.cross(rhat, exc.moment)
+        H = (-1j * medium.omega) * ((1 + 1j * k * R) * ekr / (4 * np.pi * R * R))[:, None] * rxp
+        rad = 3.0 * rhat * (rhat @ exc.moment)[:, None] - exc.moment[None, :]
+        E = (ekr / (4 * np.pi * medium.eps))[:, None] * (
+            (k * k / R)[:, None] * np.cross(rxp, rhat) + (1.0 / R ** 3 + 1j * k / R ** 2)[:, None] * rad)
+        return E, H
+    raise TypeError(f"unknown excitation {type(exc)!r}")
+
+
+def rhs_rows(spec: FormulationSpec, exc, pos, a_u, a_v) -> np.ndarray:
+    """Tested incident rows per point, (n, C) (kernels.py:334-349)."""
     m = spec.outer
-    E = exc.amplitude * np.exp(-1j * m.k * (pos @ exc.direction))[:, None] * exc.polarization[None, :]
-    H = np.cross(exc.direction, E) / m.eta
+    E, H = incident_fields(exc, m, pos)
     hu = -np.sum(a_v * H, axis=1)
     hv = np.sum(a_u * H, axis=1)
     if spec.kind == MFIE_PEC:

@@ -66,12 +66,57 @@ class SolveResult:
     converged: bool = True
 
 
+def _chart_from_reference(ch):
+    """Device chart for a reference ``Chart`` (geometry.py:38-97)."""
+    from . import geometry as geo
+    if ch is None or isinstance(ch, (geo.CubeSphereFace,)):
+        return ch
+    box = tuple(getattr(ch, a, None) for a in ("radius", "face", "u_lo", "u_hi", "v_lo", "v_hi"))
+    if None in box:
+        raise ValueError(f"chart {type(ch).__name__} has no device evaluator "
+                         "(supported: CubeSphereFace, the config-4 star chart, chart-less patches)")
+    if getattr(ch, "coef", None) is not None:               # star chart (config 4)
+        return geo.StarFace(*box, coef=np.asarray(ch.coef, float))
+    if type(ch).__name__ == "CubeSphereFace":
+        return geo.CubeSphereFace(*box)
+    raise ValueError(f"chart {type(ch).__name__} has no device evaluator")
+
+
+def from_reference(problem) -> "Problem":
+    """This package's Problem for a reference ``chebscat.solver.Problem`` (solver.py:30-73)
+    built from chebscat's own Patch / CubeSphereFace / FormulationSpec / Medium /
+    PlaneWave / Dipole objects.  Samples, chart parameters, media and solver settings
+    are taken over unchanged; a Problem of this package is returned as is."""
+    from . import geometry as geo
+    from . import kernels as ker
+    if isinstance(problem, Problem):
+        return problem
+    patches = [geo.Patch(int(p.id), np.array(p.samples, float), chart=_chart_from_reference(p.chart))
+               for p in problem.patches]
+
+    def med(m):
+        return None if m is None else ker.Medium(complex(m.eps), complex(m.mu), float(m.omega))
+
+    spec = ker.FormulationSpec(str(problem.spec.kind), med(problem.spec.outer), med(problem.spec.inner))
+    exc = problem.excitation
+    if hasattr(exc, "polarization"):
+        exc = ker.PlaneWave(np.array(exc.direction, float), np.array(exc.polarization, float),
+                            float(exc.amplitude))
+    else:
+        exc = ker.Dipole(np.array(exc.position, float), np.array(exc.moment, float))
+    keys = ("aca_tol", "trunc_tol", "gmres_tol", "gmres_restart", "gmres_max_iters", "eta", "n_leaf",
+            "tau", "grading", "oversample", "dense_cap", "workers")
+    kw = {k: getattr(problem, k) for k in keys if hasattr(problem, k)}
+    return Problem(patches, spec, exc, **kw)
+
+
 def _peak_rss_bytes() -> int:
     return resource.getrusage(resource.RUSAGE_SELF).ru_maxrss * 1024
 
 
 def build_hmatrix(problem: Problem, gen: Optional[asm.GpuGenerator] = None):
     """Classification + near field + H-matrix fill of the scaled system."""
+    problem = from_reference(problem)
     t0 = time.perf_counter()
     gen = gen or problem.generator()
     t1 = time.perf_counter()
@@ -87,6 +132,7 @@ def build_hmatrix(problem: Problem, gen: Optional[asm.GpuGenerator] = None):
 
 def solve_direct(problem: Problem) -> SolveResult:
     """H-matrix fill, H-LU, forward/backward substitution (solver.py:148-175)."""
+    problem = from_reference(problem)
     H, gen, scaled, times = build_hmatrix(problem)
     b = gen.rhs(problem.excitation)
     b_scaled = b * scaled.row_scale
@@ -105,6 +151,7 @@ def solve_direct(problem: Problem) -> SolveResult:
         "solve_s": t_solve,
         "n_dofs": problem.n_dofs,
         "hmatrix_bytes": H.memory_bytes(),
+        "hlu_bytes": F.memory_bytes(),
         "compression_rate": H.compression_rate(),
         "peak_rss_bytes": _peak_rss_bytes(),
         "memory_method": "ru_maxrss sampling + logical leaf accounting",
@@ -122,6 +169,7 @@ def solve_gmres(problem: Problem, restart: Optional[int] = None,
     (cbie_gmres, csrc/gmres.cu)."""
     import ctypes as ct
     from . import _ffi
+    problem = from_reference(problem)
     restart = restart if restart is not None else problem.gmres_restart
     max_iters = max_iters if max_iters is not None else problem.gmres_max_iters
     H, gen, scaled, times = build_hmatrix(problem)
@@ -145,6 +193,7 @@ def solve_dense(problem: Problem) -> SolveResult:
     is the product path; the LU here is scipy on the host (reference oracle
     path, not the north-star hot path)."""
     import scipy.linalg as sla
+    problem = from_reference(problem)
     gen = problem.generator()
     t0 = time.perf_counter()
     A = asm.assemble_dense(gen, cap=problem.dense_cap)

@@ -122,8 +122,9 @@ def test_chebyshev_sample_patches_match_oracle():
 
 
 def test_star_chart_frames_match_finite_differences():
-    """Config-4 star chart on the device: positions equal the host chart, tangents
-    equal central differences of the host chart."""
+    """Config-4 star chart on the device: positions and tangents are bit-identical
+    to the host chart (geometry.star_eval, the chart the reference is run with in
+    tests/golden/make_golden_big.py), tangents equal central differences."""
     from paper_2408_17116_b200 import geometry as geo, kernels as ker
     from paper_2408_17116_b200.assembly import GpuGenerator
     coef, _ = geo.star_coefficients(2408)
@@ -136,7 +137,10 @@ def test_star_chart_frames_match_finite_differences():
     for q, p in enumerate(patches):
         ch = p.chart
         sl = slice(q * 25, (q + 1) * 25)
-        assert np.abs(gen.pos[sl] - ch.positions(uu, vv)).max() < 1e-13
+        pos, au, av = geo.star_eval(ch.radius, ch.face, ch.u_lo, ch.u_hi, ch.v_lo, ch.v_hi,
+                                    ch.tables(), uu, vv)
+        assert np.array_equal(gen.pos[sl], pos)
+        assert np.array_equal(gen.a_u[sl], au) and np.array_equal(gen.a_v[sl], av)
         du = (ch.positions(uu + h, vv) - ch.positions(uu - h, vv)) / (2 * h)
         dv = (ch.positions(uu, vv + h) - ch.positions(uu, vv - h)) / (2 * h)
         assert np.abs(gen.a_u[sl] - du).max() < 1e-7

@@ -134,3 +134,31 @@ def test_cfg1_direct_matches_reference():
     x, res, H, _ = pl.solve_direct(pl.case(1))
     assert H.demoted == int(g["demoted"])
     assert np.linalg.norm(x - g["x_direct"]) <= 1e-9 * np.linalg.norm(g["x_direct"])
+
+
+@pytest.mark.parametrize("cfg", [2, 4])
+def test_oracle_classification_matches_reference_at_scale(cfg):
+    """Oracle pinned on BASELINE configs 2 and 4 (config 4: the star chart) against
+    the reference's full classification tables (tests/golden/make_golden_big.py)."""
+    g = golden(f"cfg{cfg}_class.npz")
+    d = pl.case(cfg).disc()
+    d.classify_all()
+    rec = _table(d)
+    assert rec.shape[0] == g["point"].size
+    assert np.array_equal(rec[:, 0], g["point"]) and np.array_equal(rec[:, 1], g["patch"])
+    assert np.array_equal(rec[:, 2], g["tag"])
+    assert np.array_equal(rec[:, 5], g["ok"])
+    assert np.abs(rec[:, 3] - g["u"]).max() < 1e-12
+    assert d.fallbacks == int(g["fallbacks"])
+
+
+def test_oracle_sampled_leaves_match_reference_cfg2():
+    g = golden("cfg2_class.npz")
+    cs = pl.case(2)
+    d = cs.disc()
+    gen = nf.Scaled(d)
+    worst = 0.0
+    for rows, cols, ref in list(zip(g["leaf_rows"], g["leaf_cols"], g["leaf_vals"]))[::8]:
+        got = gen.block(rows, cols)
+        worst = max(worst, np.abs(got - ref).max() / np.abs(ref).max())
+    assert worst <= 1e-12, worst
