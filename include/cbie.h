@@ -118,6 +118,17 @@ int cbie_fill_block(cbie_ctx* ctx, const int64_t* rows, int64_t m, const int64_t
  * if N > cap.  out: N x N row-major host buffer. */
 int cbie_fill_dense(cbie_ctx* ctx, int64_t cap, cbie_c128* out);
 
+/* Dense path solve_dense (solver.py:178-203) on the device: assemble_dense into HBM,
+ * LU with partial pivoting (scipy.linalg.lu_factor / zgetrf, solver.py:186), lu_solve
+ * (zgetrs) and the residual |A x - b| / |b| (solver.py:197-198) from the kept matrix.
+ *   b, x      [N][nrhs] row-major host arrays
+ *   residual  out, may be NULL
+ *   lu_out    [N][N] row-major packed L\U (scipy's lu) or NULL; piv_out [N] 0-based
+ *             interchanges (scipy's piv) or NULL
+ * CBIE_ECAP_EXCEEDED if N > cap; CBIE_ESINGULAR_DIAGONAL on an exactly singular U. */
+int cbie_dense_solve(cbie_ctx* ctx, int64_t cap, const cbie_c128* b, int nrhs, cbie_c128* x,
+                     double* residual, cbie_c128* lu_out, int32_t* piv_out);
+
 /* H-matrix of the equilibrated system: cluster tree, block tree, dense leaves,
  * batched ACA + recompression, demotion.  Replaces build_hmatrix
  * (solver.py:132-145): build_cluster_tree (hmatrix.py:82), build_block_tree

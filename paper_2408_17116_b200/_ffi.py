@@ -43,6 +43,7 @@ _SIGS = {
     "cbie_pair_block": (ct.c_int, [P, ct.c_int64, ct.c_int, P]),
     "cbie_fill_block": (ct.c_int, [P, P, ct.c_int64, P, ct.c_int64, ct.c_int, P]),
     "cbie_fill_dense": (ct.c_int, [P, ct.c_int64, P]),
+    "cbie_dense_solve": (ct.c_int, [P, ct.c_int64, P, ct.c_int, P, ct.POINTER(ct.c_double), P, P]),
     "cbie_hmatrix_build": (ct.c_int, [P, ct.c_int, ct.c_double, ct.c_double, ct.POINTER(P)]),
     "cbie_hmatrix_destroy": (None, [P]),
     "cbie_hmatrix_tree": (ct.c_int, [P, P, P, I64P]),

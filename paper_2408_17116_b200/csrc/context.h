@@ -74,6 +74,7 @@ void ctx_near_fill(cbie_ctx* c);
 void ctx_fill_block(cbie_ctx* c, const int64_t* rows, int64_t m, const int64_t* cols, int64_t n,
                     int scaled, zc* out_host);
 void ctx_fill_dense(cbie_ctx* c, zc* out_host);
+void ctx_fill_dense_device(cbie_ctx* c, zc* d_out);
 void ctx_pair_block(cbie_ctx* c, int64_t point, int patch, zc* out_host);
 
 // entry generation for a list of H-matrix dense leaves / arbitrary tiles (fill.cu)

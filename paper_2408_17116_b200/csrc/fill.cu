@@ -118,6 +118,17 @@ void ctx_pair_block(cbie_ctx* c, int64_t point, int patch, zc* out_host) {
   ctx_fill_block(c, rows.data(), C, cols.data(), (int64_t)np * C, 0, out_host);
 }
 
+// whole unscaled matrix, row-major, into device memory (the dense solve keeps it there)
+void ctx_fill_dense_device(cbie_ctx* c, zc* d_out) {
+  cudaStream_t s = c->stream;
+  const int64_t work = (int64_t)c->npts * c->npts;
+  if (c->C == 2)
+    k_fill_dense<2><<<ceil_div(work, 128), 128, 0, s>>>(c->tab, c->geom(), c->ph, c->near(), 0, c->npts, d_out);
+  else
+    k_fill_dense<4><<<ceil_div(work, 128), 128, 0, s>>>(c->tab, c->geom(), c->ph, c->near(), 0, c->npts, d_out);
+  CKL();
+}
+
 void ctx_fill_dense(cbie_ctx* c, zc* out_host) {
   cudaStream_t s = c->stream;
   const int64_t N = c->N;

@@ -99,6 +99,8 @@ enum OpKind { OP_GEMM, OP_EW, OP_CONCAT, OP_TRSM, OP_GETRF, OP_TRUNC, OP_DLR, OP
 // TRUNC_LANES streams (lane = level % TRUNC_LANES, each with its own workspaces) so
 // independent recompression groups of different levels overlap
 constexpr int TRUNC_LANES = 3;
+constexpr int TRUNC_MN_SMALL = 384;   // larger blocks: cluster recompression (Grp::cbig)
+constexpr int TW_PER_LANE = 3;        // recompression workspaces per lane (streams s, s2, s3)
 constexpr int NVK = 16;
 static_assert(OP_NKIND + TRUNC_LANES - 1 <= NVK, "virtual kinds");
 inline int vkind(int kind, int level) {
@@ -1094,6 +1096,9 @@ struct Grp {
   int kind, start, count, level, kmax;
   int split = 0;       // OP_TRUNC: descriptors [start, start + split) form the first part
   bool gram = false;   // OP_TRUNC: the first part runs the Gram path
+  // OP_TRUNC, Gram path: [start, start + nsmall) small blocks, [nsmall, split) large blocks
+  // recompressed by clusters of cbig CTAs per problem (mn_small: largest small side)
+  int nsmall = -1, cbig = 1, mn_small = 0;
   std::vector<int> deps;   // groups of OTHER kinds this group waits for (multi-stream executor)
 };
 
@@ -1192,6 +1197,29 @@ void make_plan(Plan& P, cudaStream_t s, const Recorder* Rx = nullptr, const std:
       std::stable_partition(tr.begin() + gr.start, tr.end(), first);
       gr.split = (int)std::count_if(tr.begin() + gr.start, tr.end(), first);
       gr.gram = gram;
+      if (gram) {
+        // large blocks after the small ones: their per-problem latency (Gram + applies over
+        // m rows on one SM) sets the group's time, so they get clusters of CTAs
+        auto small = [](const TruncDesc& d) { return std::max(d.m, d.n) <= TRUNC_MN_SMALL; };
+        auto b = tr.begin() + gr.start, e = tr.begin() + gr.start + gr.split;
+        std::stable_partition(b, e, small);
+        const int ns = (int)std::count_if(b, e, small);
+        const int nb = gr.split - ns;
+        int mnb = 0, mns = 1;
+        for (auto it = b; it != e; ++it) {
+          const int mn = std::max(it->m, it->n);
+          if (mn > TRUNC_MN_SMALL) mnb = std::max(mnb, mn);
+          else mns = std::max(mns, mn);
+        }
+        int cb = 1;
+        const int useful = std::min(8, (mnb + 191) / 192);
+        while (nb > 0 && 2 * cb <= useful && 2 * cb * nb + std::min(ns, 74) <= 148) cb *= 2;
+        if (nb > 0 && cb > 1) {
+          gr.nsmall = ns;
+          gr.cbig = cb;
+          gr.mn_small = mns;
+        }
+      }
     }
     groups.push_back(gr);
     i = j;
@@ -1244,7 +1272,7 @@ void make_plan(Plan& P, cudaStream_t s, const Recorder* Rx = nullptr, const std:
 // paper_2408_17116_b200/__init__.py); priorities follow the critical path (CBIE_PROFILE
 // crit_ms): recompression lanes and concatenations first, the diagonal chain next
 struct StreamPool {
-  cudaStream_t kind[NVK] = {}, lane2[TRUNC_LANES] = {}, side = nullptr;
+  cudaStream_t kind[NVK] = {}, lane2[TRUNC_LANES] = {}, lane3[TRUNC_LANES] = {}, side = nullptr;
 };
 StreamPool& stream_pool() {
   static std::map<int, StreamPool> pools;
@@ -1261,7 +1289,10 @@ StreamPool& stream_pool() {
     const int pr = rc ? hi : diag ? std::min(lo, hi + 1) : lo;
     CK(cudaStreamCreateWithPriority(&P.kind[q], cudaStreamNonBlocking, pr));
   }
-  for (int l = 0; l < TRUNC_LANES; ++l) CK(cudaStreamCreateWithPriority(&P.lane2[l], cudaStreamNonBlocking, hi));
+  for (int l = 0; l < TRUNC_LANES; ++l) {
+    CK(cudaStreamCreateWithPriority(&P.lane2[l], cudaStreamNonBlocking, hi));
+    CK(cudaStreamCreateWithPriority(&P.lane3[l], cudaStreamNonBlocking, hi));
+  }
   CK(cudaStreamCreateWithPriority(&P.side, cudaStreamNonBlocking, lo));
   return P;
 }
@@ -1356,7 +1387,7 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
     const int lane = ms ? trunc_lane(gr.level) : 0;
     cudaStream_t s2 = s2l[lane];
     cudaEvent_t fork_ev = fork_l[lane], join_ev = join_l[lane];
-    TruncWork* tw = twl + 2 * lane;
+    TruncWork* tw = twl + TW_PER_LANE * lane;
     if (ms)
       for (int d : gr.deps) CK(cudaStreamWaitEvent(s, gev[d], 0));
     if (gr.level != lvl) {
@@ -1480,8 +1511,14 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
             kcm = std::max(kcm, tr[gr.start + i].k);
             mnm = std::max(mnm, std::max(tr[gr.start + i].m, tr[gr.start + i].n));
           }
+          TruncBig big;
+          big.nsmall = gr.nsmall;
+          big.cbig = gr.cbig;
+          big.mn_small = gr.mn_small;
+          big.work3 = &tw[2];
+          big.s3 = stream_pool().lane3[lane];
           launch_truncate_routed(arena, ranks, dtr.p + gr.start, gr.split, gr.kmax, tol, ovf, tw[0], s, kcm, mnm,
-                                 &tw[1], s2);
+                                 &tw[1], s2, nullptr, &big);
           if (gr.split < gr.count) {
             CK(cudaEventRecord(join_ev, s2));
             CK(cudaStreamWaitEvent(s, join_ev, 0));
@@ -1647,7 +1684,7 @@ struct PlanCache {
   uint64_t key = 0;
   Plan plan;
   DBuf<zc> work;
-  TruncWork tw[2 * TRUNC_LANES];   // recompression workspaces (two per lane)
+  TruncWork tw[TW_PER_LANE * TRUNC_LANES];   // recompression workspaces (per lane: s, s2, s3)
   int64_t leaf_end = 0;
 };
 // per device (a process may drive contexts on several GPUs), guarded by g_hlu_mutex
@@ -1778,6 +1815,7 @@ static void hlu_factor_impl(cbie_hlu* F) {
     key = fnv(key, L.cap * 7919ll + T.cl[L.r].lo * 31ll + T.cl[L.c].lo);
   }
   key = fnv(key, (int64_t)(F->tol * 1e15));
+  key = fnv(key, (int64_t)(getenv("CBIE_POOL_GB") ? atof(getenv("CBIE_POOL_GB")) * 1000 : -1));
   const bool use_cache = getenv("CBIE_NO_PLAN_CACHE") == nullptr;
   auto& g_plan_cache = g_plan_caches[c->device];
   auto t0 = std::chrono::steady_clock::now();
@@ -1824,7 +1862,11 @@ static void hlu_factor_impl(cbie_hlu* F) {
   Exec ex = run_plan(PL, work.p, F->ranks.p, F->piv.p, F->rcond.p, flag.p, ovf.p, g_plan_cache->tw, F->tol, s);
   F->stat["factor_device_ms"] = tm.stop_ms(s);
   // the factors keep only their storage; the workspace stays with the plan cache
-  F->arena.alloc((size_t)(leaf_end + solve_cache_temps(leaf_end)) + 1);
+  // + room for the temporaries of a one-rhs solve (its tape bounds them, hlu_solve_impl), so
+  // the first solve does not reallocate and copy the factors
+  const int64_t N = H->N;
+  F->arena.alloc((size_t)(leaf_end + std::max(solve_cache_temps(leaf_end),
+                                              std::max<int64_t>(N * 32, (int64_t)1 << 24) + 4 * N)) + 1);
   CK(cudaMemcpyAsync(F->arena.p, work.p, sizeof(zc) * leaf_end, cudaMemcpyDeviceToDevice, s));
   CK(cudaStreamSynchronize(s));
   int hflag = 0;
@@ -1837,8 +1879,13 @@ static void hlu_factor_impl(cbie_hlu* F) {
   F->stat["frees_during_run"] = (double)ex.frees;
   F->stat["trunc_kernel_ms"] = ex.trunc_kernel_ms;
   if (getenv("CBIE_PROFILE")) {
-    unsigned long long h[16] = {};
+    unsigned long long h[32] = {};
     trunc_prof_read(h);
+    {   // Gram path sub-phases (k_trunc_gram gram_stage), mean cycles per problem
+      const char* fn[7] = {"pchol_uv", "core_H", "pchol_H", "gp", "w_vhat", "trisolve_u", "apply_u"};
+      for (int i = 0; i < 7; ++i)
+        F->stat[std::string("gram_cyc_") + fn[i]] = h[14] ? (double)h[16 + i] / h[14] : 0;
+    }
     const char* nm[4] = {"qr", "core", "svd", "apply"};
     for (int i = 0; i < 4; ++i) F->stat[std::string("trunc_cyc_") + nm[i]] = h[4] ? (double)h[i] / h[4] : 0;
     F->stat["trunc_mean_sweeps"] = h[4] ? (double)h[5] / h[4] : 0;
@@ -1936,7 +1983,7 @@ struct SolveCache {
   DBuf<int> ranks, flag;
   DBuf<double> rc;
   DBuf<unsigned long long> ovf;
-  TruncWork tw[2 * TRUNC_LANES];
+  TruncWork tw[TW_PER_LANE * TRUNC_LANES];
 };
 std::map<int, std::unique_ptr<SolveCache>> g_solve_caches;
 std::map<int, int64_t> g_solve_leaf_ends;

@@ -247,7 +247,7 @@ struct RankState {
   DBuf<int> ranks, piv, flag;
   DBuf<double> rcond;
   DBuf<unsigned long long> ovf;
-  TruncWork tw[2 * TRUNC_LANES];
+  TruncWork tw[TW_PER_LANE * TRUNC_LANES];
   Plan plan;
 };
 

@@ -118,13 +118,21 @@ void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int
 // others handed on to the blocked (k <= 128, max(m, n) <= 384) / unblocked kernels
 // With a second stream / workspace the Householder share runs concurrently with the
 // Gram kernel: a routing kernel splits the problems by their device-side rank first.
+// big: descriptors [nsmall, nd) are large blocks (host-partitioned); their Gram-path
+// problems run with clusters of cbig CTAs per problem on stream s3 (workspace work3),
+// concurrently with the small ones (nsmall < 0: no split)
+struct TruncBig {
+  int nsmall = -1, cbig = 1, mn_small = 0;
+  TruncWork* work3 = nullptr;
+  cudaStream_t s3 = nullptr;
+};
 void launch_truncate_routed(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
                             unsigned long long* overflow, TruncWork& work, cudaStream_t s, int kc_max,
                             int mn_max, TruncWork* work2 = nullptr, cudaStream_t s2 = nullptr,
-                            zc* arena_out = nullptr);
+                            zc* arena_out = nullptr, const TruncBig* big = nullptr);
 void launch_truncate_gram(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, double tol,
                           unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, zc* arena_out,
-                          int* defer, const int* idx = nullptr, int mn_multi = 0);
+                          int* defer, const int* idx = nullptr, int mn_multi = 0, int csize = 1);
 bool launch_truncate_blocked(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, double tol,
                              unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, int kc_max,
                              int mn_max, zc* arena_out, int* defer, const int* idx = nullptr);

@@ -411,13 +411,13 @@ unsigned long long* g_trunc_prof = nullptr;   // debug cycle counters (CBIE_PROF
 
 void trunc_prof_enable(bool on, int onesided) {
   if (on && !g_trunc_prof) {
-    cudaMalloc(&g_trunc_prof, 16 * sizeof(unsigned long long));
-    cudaMemset(g_trunc_prof, 0, 16 * sizeof(unsigned long long));
+    cudaMalloc(&g_trunc_prof, 32 * sizeof(unsigned long long));
+    cudaMemset(g_trunc_prof, 0, 32 * sizeof(unsigned long long));
   }
   cudaMemcpyToSymbol(prof_onesided_flag_dev, &onesided, sizeof(int));
 }
 void trunc_prof_read(unsigned long long* h) {
-  if (g_trunc_prof) cudaMemcpy(h, g_trunc_prof, 16 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
+  if (g_trunc_prof) cudaMemcpy(h, g_trunc_prof, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost);
 }
 
 // unblocked kernel over a device-side list of problems (list[0] = count): strided grid
@@ -440,14 +440,19 @@ static void launch_unblocked_list(zc* arena, zc* arena_out, int* ranks, const Tr
 
 namespace {
 // split problems by device-side rank: k <= kg (and no-ops) -> la (Gram kernel), the rest -> lb
+// (i >= nsmall: Gram problems of the large blocks -> lg, when lg != nullptr)
 __global__ void k_route(const int* __restrict__ ranks, const TruncDesc* __restrict__ ds, int nd, int kg, int* la,
-                        int* lb) {
+                        int* lb, int* lg, int nsmall) {
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nd; i += gridDim.x * blockDim.x) {
     const TruncDesc& d = ds[i];
     const int k = d.k_slot >= 0 ? ranks[d.k_slot] : d.k;
     const bool skip = d.skip_slot >= 0 && ranks[d.skip_slot] == 0;
-    if (skip || k <= kg) la[1 + atomicAdd(la, 1)] = i;
-    else lb[1 + atomicAdd(lb, 1)] = i;
+    if (skip || k <= kg) {
+      int* l = (lg && i >= nsmall) ? lg : la;
+      l[1 + atomicAdd(l, 1)] = i;
+    } else {
+      lb[1 + atomicAdd(lb, 1)] = i;
+    }
   }
 }
 }  // namespace
@@ -485,25 +490,49 @@ static void householder_list(zc* arena, int* ranks, const TruncDesc* d_desc, int
 // kernels on the second stream, concurrently.
 void launch_truncate_routed(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int kmax, double tol,
                             unsigned long long* overflow, TruncWork& work, cudaStream_t s, int kc_max,
-                            int mn_max, TruncWork* work2, cudaStream_t s2, zc* arena_out) {
+                            int mn_max, TruncWork* work2, cudaStream_t s2, zc* arena_out, const TruncBig* big) {
   if (nd == 0) return;
   zc* aout = arena_out ? arena_out : arena;
   const bool multi = getenv("CBIE_NO_MULTISTAGE") == nullptr;
   const int kg = multi ? 256 : 64;
+  // large blocks in their own cluster launch on s3, concurrently with the small ones
+  const bool split = big && big->s3 && big->work3 && big->nsmall >= 0 && big->nsmall < nd && big->cbig > 1 &&
+                     getenv("CBIE_NO_CLUSTER") == nullptr;
+  cudaEvent_t f3 = nullptr, j3 = nullptr;
+  if (split) {
+    CK(cudaEventCreateWithFlags(&f3, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&j3, cudaEventDisableTiming));
+  }
   if (kc_max <= 64) {   // no capacity can exceed the single-stage Gram path
-    launch_truncate_gram(arena, ranks, d_desc, nd, tol, overflow, work.scratch, s, aout, nullptr);
+    if (!split) {
+      launch_truncate_gram(arena, ranks, d_desc, nd, tol, overflow, work.scratch, s, aout, nullptr);
+      return;
+    }
+    CK(cudaEventRecord(f3, s));
+    CK(cudaStreamWaitEvent(big->s3, f3, 0));
+    launch_truncate_gram(arena, ranks, d_desc + big->nsmall, nd - big->nsmall, tol, overflow, big->work3->scratch,
+                         big->s3, aout, nullptr, nullptr, 0, big->cbig);
+    launch_truncate_gram(arena, ranks, d_desc, big->nsmall, tol, overflow, work.scratch, s, aout, nullptr);
+    CK(cudaEventRecord(j3, big->s3));
+    CK(cudaStreamWaitEvent(s, j3, 0));
+    cudaEventDestroy(f3);
+    cudaEventDestroy(j3);
     return;
   }
   TruncWork& wb = work2 ? *work2 : work;
   cudaStream_t sb = work2 && s2 ? s2 : s;
-  // lists: la (Gram), lb (Householder, stream sb), lf (Gram failures, stream s)
-  if (work.gdefer.n < 3 * (size_t)nd + 3) work.gdefer.alloc(std::max<size_t>(3 * nd + 3, 3 * 4096));
+  // lists: la (Gram), lb (Householder, stream sb), lf (Gram failures, stream s), lg (Gram,
+  // large blocks, stream s3)
+  if (work.gdefer.n < 4 * (size_t)nd + 4) work.gdefer.alloc(std::max<size_t>(4 * nd + 4, 4 * 4096));
   int* la = work.gdefer.p;
   int* lf = la + nd + 1;
   int* lb = lf + nd + 1;
+  int* lg = lb + nd + 1;
   CK(cudaMemsetAsync(la, 0, sizeof(int) * (2 * nd + 2), s));   // counts of la and lf (and la's payload)
   CK(cudaMemsetAsync(lb, 0, sizeof(int), s));
-  k_route<<<std::min((nd + 255) / 256, 148), 256, 0, s>>>(ranks, d_desc, nd, kg, la, lb);
+  CK(cudaMemsetAsync(lg, 0, sizeof(int), s));
+  k_route<<<std::min((nd + 255) / 256, 148), 256, 0, s>>>(ranks, d_desc, nd, kg, la, lb, split ? lg : nullptr,
+                                                          split ? big->nsmall : nd);
   CKL();
   cudaEvent_t fork = nullptr, join = nullptr;
   const bool two = sb != s && kc_max > kg;
@@ -513,18 +542,30 @@ void launch_truncate_routed(zc* arena, int* ranks, const TruncDesc* d_desc, int 
     CK(cudaEventRecord(fork, s));
     CK(cudaStreamWaitEvent(sb, fork, 0));
   }
+  if (split) {
+    CK(cudaEventRecord(f3, s));
+    CK(cudaStreamWaitEvent(big->s3, f3, 0));
+    launch_truncate_gram(arena, ranks, d_desc, nd - big->nsmall, tol, overflow, big->work3->scratch, big->s3, aout,
+                         multi ? lf : nullptr, lg, multi ? mn_max : 0, big->cbig);
+  }
   if (kc_max > kg)
     householder_list(arena, ranks, d_desc, nd, kmax, tol, overflow, two ? wb : work, two ? sb : s, kc_max, mn_max,
                      lb, aout);
-  launch_truncate_gram(arena, ranks, d_desc, nd, tol, overflow, work.scratch, s, aout, multi ? lf : nullptr, la,
-                       multi ? mn_max : 0);
+  launch_truncate_gram(arena, ranks, d_desc, split ? big->nsmall : nd, tol, overflow, work.scratch, s, aout,
+                       multi ? lf : nullptr, la, multi ? (split ? big->mn_small : mn_max) : 0);
   if (two) {
     CK(cudaEventRecord(join, sb));
     CK(cudaStreamWaitEvent(s, join, 0));
     cudaEventDestroy(fork);
     cudaEventDestroy(join);
   }
-  // multi-stage failures (kept rank filled the Gram capacity), after the join so that
+  if (split) {
+    CK(cudaEventRecord(j3, big->s3));
+    CK(cudaStreamWaitEvent(s, j3, 0));
+    cudaEventDestroy(f3);
+    cudaEventDestroy(j3);
+  }
+  // multi-stage failures (kept rank filled the Gram capacity), after the joins so that
   // they reuse the Householder workspaces of the second stream
   if (multi) householder_list(arena, ranks, d_desc, nd, kmax, tol, overflow, wb, s, kc_max, mn_max, lf, aout);
 }

@@ -19,6 +19,8 @@
 //      of M are Vhat = P B / sigma;
 //   4. U' = Q_u (M Vhat)  (= Q_u U_M Sigma),  Vt' = Q_v conj(Vhat), both Q's
 //      applied with the stored block reflectors.
+#include <cooperative_groups.h>
+
 #include "hmatrix.h"
 #include "lowrank.cuh"
 
@@ -52,10 +54,10 @@ extern unsigned long long* g_trunc_prof;
 // multi-stage Gram path and only its failures are deferred
 void launch_truncate_gram(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, double tol,
                           unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, zc* arena_out,
-                          int* defer, const int* idx, int mn_multi) {
+                          int* defer, const int* idx, int mn_multi, int csize) {
   if (nd == 0) return;
   t2b::launch_gram(arena, arena_out ? arena_out : arena, ranks, d_desc, nd, tol, overflow, scratch, s,
-                   g_trunc_prof, defer, idx, mn_multi);
+                   g_trunc_prof, defer, idx, mn_multi, csize);
 }
 
 bool launch_truncate_blocked(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, double tol,

@@ -3,6 +3,7 @@
 // complex elements, T2_MINB resident CTAs per SM.  No include guard on purpose.
 namespace {
 namespace T2NS {
+namespace cg = cooperative_groups;
 
 constexpr int NT = T2_NT;
 constexpr int NW = NT / 32;
@@ -12,6 +13,11 @@ constexpr int PWMAX = 32;      // widest panel
 constexpr int ELEMS = T2_ELEMS;  // dynamic shared region (zc): panels / core / Jacobi block
 constexpr double DELTA = 0.05; // pivoted-QR drop threshold relative to tol * s_0
 constexpr unsigned FULL = 0xffffffffu;
+
+// cluster rank / size of this CTA (1-CTA launches: 0 / 1) and the row slice of rank r of c
+__device__ __forceinline__ int cl_rank() { return (int)cg::this_cluster().block_rank(); }
+__device__ __forceinline__ int cl_size() { return (int)cg::this_cluster().num_blocks(); }
+__device__ __forceinline__ int slice_lo(int m, int r, int c) { return (int)(((int64_t)m * r) / c); }
 
 // shared region layout for a QR / Q application on m rows:
 //   [panel: (m|1) x pw][Z chunk: (m|1) x CH][W: pw x CH][split partials: NT]
@@ -435,9 +441,12 @@ __global__ void __launch_bounds__(NT, T2_MINB)
   __shared__ Smem S;
   extern __shared__ __align__(16) unsigned char smraw[];
   zc* sm = reinterpret_cast<zc*>(smraw);
-  // idx: run the problems listed in idx[1 + base + blockIdx.x] (count idx[0]) of descs
-  if (idx && base + (int)blockIdx.x >= idx[0]) return;
-  const int tix = idx ? idx[1 + base + blockIdx.x] : (int)blockIdx.x;
+  // one problem per cluster (csize CTAs, cluster_gram_sum); pb = problem of this cluster
+  const int crank = cl_rank(), csize = cl_size();
+  const int pb = (int)blockIdx.x / csize;
+  // idx: run the problems listed in idx[1 + base + pb] (count idx[0]) of descs
+  if (idx && base + pb >= idx[0]) return;
+  const int tix = idx ? idx[1 + base + pb] : pb;
   const TruncDesc d = descs[tix];
   const long long tc0 = clock64();
   if (d.skip_slot >= 0 && ranks[d.skip_slot] == 0) return;
@@ -569,7 +578,7 @@ __global__ void __launch_bounds__(NT, T2_MINB)
     blk_apply_q(U, m, kk1, d.ldu, S.kap1, SgU, Uo, m, r, sm, S);
     blk_apply_q(Vt, n, kk2, d.ldv, S.kap2, SgV, Vo, n, r, sm, S);
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && crank == 0) {
     ranks[d.out_slot] = r;
     if (prof) {
       const long long tc4 = clock64();
@@ -641,7 +650,9 @@ __host__ __device__ inline int64_t gram_scratch_per() { return 4 * (int64_t)GSQ 
 // (conjugate-FMA, 4 DFMA per complex term), the lower part is mirrored; thread groups
 // split the rows; the next 64-row chunk is loaded into registers while the current
 // one is consumed from shared memory.
-__device__ void gram_acc(const zc* __restrict__ X, int m, int k, int ldx, zc* G, zc* Xs) {
+// rows [r_lo, r_hi) only (a cluster CTA's slice; the partial Grams are summed across the
+// cluster by cluster_gram_sum).
+__device__ void gram_acc(const zc* __restrict__ X, int r_lo, int r_hi, int k, int ldx, zc* G, zc* Xs) {
   constexpr int PER = GCH * KG / NT;   // staged elements per thread
   const int tb = (k + 3) / 4, ntile = tb * (tb + 1) / 2;
   const int groups = max(1, min(8, NT / ntile));   // row groups, summed in a fixed order below
@@ -659,16 +670,16 @@ __device__ void gram_acc(const zc* __restrict__ X, int m, int k, int ldx, zc* G,
     for (int qb = 0; qb < 4; ++qb) ar[qa][qb] = ai[qa][qb] = 0.0;
   zc v[PER];
   auto fetch = [&](int r0) {
-    const int rows = min(GCH, m - r0);
+    const int rows = min(GCH, r_hi - r0);
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
       const int e = threadIdx.x + u * NT;
-      v[u] = (r0 < m && e < rows * k) ? X[(int64_t)(e / rows) * ldx + r0 + e % rows] : zmk(0.0, 0.0);
+      v[u] = (r0 < r_hi && e < rows * k) ? X[(int64_t)(e / rows) * ldx + r0 + e % rows] : zmk(0.0, 0.0);
     }
   };
-  fetch(0);
-  for (int r0 = 0; r0 < m; r0 += GCH) {
-    const int rows = min(GCH, m - r0);
+  fetch(r_lo);
+  for (int r0 = r_lo; r0 < r_hi; r0 += GCH) {
+    const int rows = min(GCH, r_hi - r0);
     __syncthreads();
 #pragma unroll
     for (int u = 0; u < PER; ++u) {
@@ -817,12 +828,12 @@ __device__ void tri_solve_cols(const zc* R, int k, int kk, zc* Z, int r, const d
   __syncthreads();
 }
 
-// O (mo x r, ld mo, global) = X[:, perm[0..kk)] T (kk x r, ld kk, shared)
-__device__ void apply_sel(const zc* __restrict__ X, int mo, int ldx, const int* perm, int kk, const zc* T,
-                          int r, zc* __restrict__ O) {
-  const int ng = (r + 7) / 8;
-  for (int e = threadIdx.x; e < mo * ng; e += NT) {
-    const int i = e % mo, l0 = 8 * (e / mo);
+// O (mo x r, ld mo, global) = X[:, perm[0..kk)] T (kk x r, ld kk, shared), rows [i_lo, i_hi)
+__device__ void apply_sel(const zc* __restrict__ X, int mo, int ldx, int i_lo, int i_hi, const int* perm, int kk,
+                          const zc* T, int r, zc* __restrict__ O) {
+  const int ng = (r + 7) / 8, mr = i_hi - i_lo;
+  for (int e = threadIdx.x; e < mr * ng; e += NT) {
+    const int i = i_lo + e % mr, l0 = 8 * (e / mr);
     zc acc[8];
 #pragma unroll
     for (int q = 0; q < 8; ++q) acc[q] = zmk(0.0, 0.0);
@@ -929,6 +940,32 @@ __device__ int herm_jacobi(zc* H, int n, zc* X, Smem& S) {
   return sweep;
 }
 
+// Cluster execution (k_trunc_gram launched with clusters of csize CTAs per problem):
+// every CTA accumulates the Gram partials of its row slice, the partials are summed
+// in cluster-rank order through distributed shared memory (each CTA gets the same
+// bits), every CTA then runs the identical k x k work redundantly (no further
+// exchange), and the final applies are again split by rows.  csize = 1: the plain
+// one-CTA-per-problem kernel.
+
+// G (k x k, shared) <- sum over the cluster's CTAs of their G (rank order); tmp: k x k shared
+__device__ void cluster_gram_sum(zc* G, int k, zc* tmp) {
+  cg::cluster_group cl = cg::this_cluster();
+  const int C = (int)cl.num_blocks();
+  if (C == 1) return;
+  cl.sync();
+  for (int e = threadIdx.x; e < k * k; e += NT) {
+    zc acc = zmk(0.0, 0.0);
+    for (int q = 0; q < C; ++q) {
+      const zc v = cl.map_shared_rank(G, q)[e];
+      acc = zmk(acc.x + v.x, acc.y + v.y);
+    }
+    tmp[e] = acc;
+  }
+  cl.sync();   // every CTA has read every partial
+  for (int e = threadIdx.x; e < k * k; e += NT) G[e] = tmp[e];
+  __syncthreads();
+}
+
 // One Gram-path recompression (steps 1-5 above) of U (m x k, ldu) Vt (n x k, ldv),
 // k <= KG: writes Uo (m x r, ld m), Vo (n x r, ld n) and returns r (0: zero product);
 // r is clipped at cap (counted in overflow).  sc: per-CTA scratch (4 GSQ).
@@ -940,7 +977,10 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   zc* Gu = sm;
   zc* Gv = sm + GSQ;
   zc* X2 = sm + 2 * GSQ;
-  if (threadIdx.x == 0) flop_add(8.0 * (m + n) * (double)k * k);
+  const int crank = cl_rank(), csize = cl_size();
+  const int mu0 = slice_lo(m, crank, csize), mu1 = slice_lo(m, crank + 1, csize);
+  const int nv0 = slice_lo(n, crank, csize), nv1 = slice_lo(n, crank + 1, csize);
+  if (threadIdx.x == 0 && crank == 0) flop_add(8.0 * (m + n) * (double)k * k);
   zc* Rug = sc;
   zc* Rvg = sc + GSQ;
   zc* Mg = sc + 2 * GSQ;
@@ -949,8 +989,10 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   // 1. Gram matrices
   for (int e = threadIdx.x; e < 2 * GSQ; e += NT) sm[e] = zmk(0.0, 0.0);
   __syncthreads();
-  gram_acc(U, m, k, ldu, Gu, X2);
-  gram_acc(Vt, n, k, ldv, Gv, X2);
+  gram_acc(U, mu0, mu1, k, ldu, Gu, X2);
+  gram_acc(Vt, nv0, nv1, k, ldv, Gv, X2);
+  cluster_gram_sum(Gu, k, X2);
+  cluster_gram_sum(Gv, k, X2);
   // 2. balancing
   for (int c = threadIdx.x; c < k; c += NT) {
     const double du = Gu[c * k + c].x, dv = Gv[c * k + c].x;
@@ -966,9 +1008,16 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   }
   __syncthreads();
   tc[1] = clock64();
+  long long tf = tc[1];
+  auto stamp = [&](int slot) {
+    const long long t = clock64();
+    tc[slot] += t - tf;
+    tf = t;
+  };
   // 3. pivoted Cholesky
   const int ku = pchol(Gu, k, pu, CHOL_EPS, S);
   const int kv = pchol(Gv, k, pv, CHOL_EPS, S);
+  stamp(5);
   if (ku == 0 || kv == 0) return 0;
   for (int c = threadIdx.x; c < k; c += NT) {
     posu[pu[c]] = c;
@@ -1007,7 +1056,9 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   }
   for (int e = threadIdx.x; e < kk1 * kk2; e += NT) Mg[e] = X2[e];
   __syncthreads();
+  stamp(6);
   const int kp = pchol(H, kk1, S.perm, (GDELTA * tol) * (GDELTA * tol), S, true);
+  stamp(7);
   zc* Gp = Gv;   // R R^H (kp x kp)
   zc* Z = X2;    // eigenvectors (kp x kp)
   for (int e = threadIdx.x; e < kp * kp; e += NT) {
@@ -1018,6 +1069,7 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
     Z[b * kp + a] = zmk(a == b ? 1.0 : 0.0, 0.0);
   }
   __syncthreads();
+  stamp(8);
   tc[2] = clock64();
   const int sweeps = herm_jacobi(Gp, kp, Z, S);
   for (int c = threadIdx.x; c < kp; c += NT) S.sig[c] = sqrt(fmax(Gp[c * kp + c].x, 0.0));
@@ -1038,7 +1090,7 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
     r = max(r, 1);
   }
   if (r > cap) {
-    if (threadIdx.x == 0) atomicAdd(overflow, 1ull);
+    if (threadIdx.x == 0 && crank == 0) atomicAdd(overflow, 1ull);
     r = cap;
   }
   // W = P R^H Z_r (kk1 x r) in Gv's region (G dead: S.sig holds its diagonal)
@@ -1064,18 +1116,22 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   for (int j = threadIdx.x; j < kk2; j += NT) scv[j] = ainv[pv[j]];
   for (int e = threadIdx.x; e < k * k; e += NT) X2[e] = Rug[e];
   __syncthreads();
+  tf = clock64();
+  tc[9] += tf - tc[3];
   // 6a. U' = U_sel D R_u11^{-1} W
   tri_solve_cols(X2, k, kk1, W, r, scu);
-  if (r > 0) apply_sel(U, m, ldu, pu, kk1, W, r, Uo);
+  stamp(10);
+  if (r > 0) apply_sel(U, m, ldu, mu0, mu1, pu, kk1, W, r, Uo);
   __syncthreads();
+  stamp(11);
   // 6b. Vt' = Vt_sel D^{-1} R_v11^{-1} conj(Vhat)
   zc* W2 = Gu;
   for (int e = threadIdx.x; e < k * k; e += NT) X2[e] = Rvg[e];
   for (int e = threadIdx.x; e < kk2 * r; e += NT) W2[e] = Vhg[e];
   __syncthreads();
   tri_solve_cols(X2, k, kk2, W2, r, scv);
-  if (r > 0) apply_sel(Vt, n, ldv, pv, kk2, W2, r, Vo);
-  if (threadIdx.x == 0)
+  if (r > 0) apply_sel(Vt, n, ldv, nv0, nv1, pv, kk2, W2, r, Vo);
+  if (threadIdx.x == 0 && crank == 0)
     // applies, pivoted Choleskys, M and H products, Jacobi sweeps (Gram counted above)
     flop_add(8.0 * ((double)m * kk1 + (double)n * kk2) * r + 16.0 * k * (double)k * k / 3.0 +
              8.0 * kk1 * (double)kk2 * (k + kk1) + 32.0 * sweeps * (double)kp * kp * kp);
@@ -1102,34 +1158,40 @@ __global__ void __launch_bounds__(NT, 1)
   __shared__ Smem S;
   extern __shared__ __align__(16) unsigned char smraw[];
   zc* sm = reinterpret_cast<zc*>(smraw);
-  // idx: run the problems listed in idx[1 + base + blockIdx.x] (count idx[0]) of descs
-  if (idx && base + (int)blockIdx.x >= idx[0]) return;
-  const int tix = idx ? idx[1 + base + blockIdx.x] : (int)blockIdx.x;
+  // one problem per cluster (csize CTAs, cluster_gram_sum); pb = problem of this cluster
+  const int crank = cl_rank(), csize = cl_size();
+  const int pb = (int)blockIdx.x / csize;
+  // idx: run the problems listed in idx[1 + base + pb] (count idx[0]) of descs
+  if (idx && base + pb >= idx[0]) return;
+  const int tix = idx ? idx[1 + base + pb] : pb;
   const TruncDesc d = descs[tix];
-  long long tc[5];
+  long long tc[12] = {};
   tc[0] = clock64();
   if (d.skip_slot >= 0 && ranks[d.skip_slot] == 0) return;
   const int k = d.k_slot >= 0 ? ranks[d.k_slot] : d.k;
   const int m = d.m, n = d.n;
   if (k <= 0 || m == 0 || n == 0) {
-    if (threadIdx.x == 0) ranks[d.out_slot] = 0;
+    if (threadIdx.x == 0 && crank == 0) ranks[d.out_slot] = 0;
     return;
   }
   const bool multi = k > KG && k <= KMS && max(m, n) <= mn_max;
   if (k > KG && !multi) {   // handed to the Householder kernels
-    if (threadIdx.x == 0) defer[1 + atomicAdd(defer, 1)] = idx ? tix : base + blockIdx.x;
+    if (threadIdx.x == 0 && crank == 0) defer[1 + atomicAdd(defer, 1)] = idx ? tix : base + pb;
     return;
   }
   const zc* U = arena + d.in_u;
   const zc* Vt = arena + d.in_v;
-  zc* sc = scratch + (int64_t)blockIdx.x * per;
+  zc* sc = scratch + (int64_t)blockIdx.x * per;                  // private k x k scratch
+  zc* sc0 = scratch + (int64_t)(blockIdx.x - crank) * per;      // the cluster's shared bases
+  const int mu0 = slice_lo(m, crank, csize), mu1 = slice_lo(m, crank + 1, csize);
+  const int nv0 = slice_lo(n, crank, csize), nv1 = slice_lo(n, crank + 1, csize);
   zc* Uo = aout + d.out_u;
   zc* Vo = aout + d.out_v;
   int sweeps = 0, r = 0;
   if (!multi) {
     r = gram_stage(U, d.ldu, Vt, d.ldv, m, n, k, Uo, Vo, d.cap, tol, sc, overflow, S, sm, tc, &sweeps);
   } else {
-    zc* bu[2] = {sc + 4 * GSQ, sc + 4 * GSQ + (int64_t)2 * mn_max * KG};
+    zc* bu[2] = {sc0 + 4 * GSQ, sc0 + 4 * GSQ + (int64_t)2 * mn_max * KG};
     zc* bv[2] = {bu[0] + (int64_t)mn_max * KG, bu[1] + (int64_t)mn_max * KG};
     int cur = 0, done = KG;
     r = gram_stage(U, d.ldu, Vt, d.ldv, m, n, KG, bu[0], bv[0], KG, tol, sc, overflow, S, sm, tc, &sweeps);
@@ -1138,16 +1200,18 @@ __global__ void __launch_bounds__(NT, 1)
       // too little room left for the remaining columns (each stage costs a full Gram
       // recompression): Householder kernels -- nothing was written to the output yet
       if (add < min(16, k - done)) {
-        if (threadIdx.x == 0) defer[1 + atomicAdd(defer, 1)] = idx ? tix : base + blockIdx.x;
+        if (threadIdx.x == 0 && crank == 0) defer[1 + atomicAdd(defer, 1)] = idx ? tix : base + pb;
         return;
       }
-      // append the next columns behind the kept basis
-      for (int e = threadIdx.x; e < add * m; e += NT) {
-        const int c = e / m, i = e % m;
+      // append the next columns behind the kept basis (this CTA's rows; the next Gram
+      // stage reads the same rows)
+      const int mr = mu1 - mu0, nr = nv1 - nv0;
+      for (int e = threadIdx.x; e < add * mr; e += NT) {
+        const int c = e / mr, i = mu0 + e % mr;
         bu[cur][(int64_t)(r + c) * m + i] = U[(int64_t)(done + c) * d.ldu + i];
       }
-      for (int e = threadIdx.x; e < add * n; e += NT) {
-        const int c = e / n, i = e % n;
+      for (int e = threadIdx.x; e < add * nr; e += NT) {
+        const int c = e / nr, i = nv0 + e % nr;
         bv[cur][(int64_t)(r + c) * n + i] = Vt[(int64_t)(done + c) * d.ldv + i];
       }
       __syncthreads();
@@ -1160,7 +1224,7 @@ __global__ void __launch_bounds__(NT, 1)
       cur ^= 1;
     }
   }
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0 && crank == 0) {
     ranks[d.out_slot] = r;
     if (prof) {
       const long long tc4 = clock64();
@@ -1172,26 +1236,40 @@ __global__ void __launch_bounds__(NT, 1)
       atomicAdd(prof + 5, (unsigned long long)sweeps);
       atomicAdd(prof + 14, 1ull);
       atomicAdd(prof + 15, (unsigned long long)(tc4 - tc[0]));
+      for (int q = 5; q < 12; ++q) atomicAdd(prof + 11 + q, (unsigned long long)tc[q]);
     }
   }
 }
 
 void launch_gram(zc* arena, zc* aout, int* ranks, const TruncDesc* d_desc, int nd, double tol,
                  unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, unsigned long long* prof,
-                 int* defer, const int* idx, int mn_max) {
+                 int* defer, const int* idx, int mn_max, int csize) {
   // mn_max > 0: problems with KG < k <= KMS and max(m, n) <= mn_max run the multi-stage path
   const int64_t per = gram_scratch_per() + (mn_max > 0 ? gram_ms_scratch(mn_max) : 0);
+  csize = std::max(1, std::min(csize, 8));
   // one launch per group whenever 2 GB of scratch allow it (a second launch of the tail
   // would wait for the whole first one on the stream)
-  const int wave = (int)std::max<int64_t>(1, ((int64_t)2 << 30) / (per * (int64_t)sizeof(zc)));
-  const size_t need = (size_t)std::min(wave, nd) * per;
+  const int wave = (int)std::max<int64_t>(1, ((int64_t)2 << 30) / (per * csize * (int64_t)sizeof(zc)));
+  const size_t need = (size_t)std::min(wave, nd) * csize * per;
   if (scratch.n < need) scratch.alloc(need);
   const int smem = (3 * GSQ + KG + 1) * (int)sizeof(zc);
   CK(cudaFuncSetAttribute(k_trunc_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
   for (int b0 = 0; b0 < nd; b0 += wave) {
     const int nb = std::min(wave, nd - b0);
-    k_trunc_gram<<<nb, NT, smem, s>>>(arena, aout, ranks, idx ? d_desc : d_desc + b0, scratch.p, per, tol,
-                                      overflow, prof, defer, b0, idx, mn_max);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(nb * csize));
+    cfg.blockDim = dim3(NT);
+    cfg.dynamicSmemBytes = (size_t)smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = (unsigned)csize;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    CK(cudaLaunchKernelEx(&cfg, k_trunc_gram, arena, aout, ranks, idx ? d_desc : d_desc + b0, scratch.p, per, tol,
+                          overflow, prof, defer, b0, idx, mn_max));
     CKL();
   }
 }

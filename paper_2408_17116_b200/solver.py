@@ -189,22 +189,24 @@ def solve_gmres(problem: Problem, restart: Optional[int] = None,
 
 
 def solve_dense(problem: Problem) -> SolveResult:
-    """Dense GPU fill + LU of the unscaled system (solver.py:178-203).  The fill
-    is the product path; the LU here is scipy on the host (reference oracle
-    path, not the north-star hot path)."""
-    import scipy.linalg as sla
+    """Dense fill + LU with partial pivoting + solve of the unscaled system, all on the
+    device (solver.py:178-203; cbie_dense_solve, csrc/dense_solve.cu)."""
+    import ctypes as ct
+    from . import _ffi
     problem = from_reference(problem)
     gen = problem.generator()
+    b = np.ascontiguousarray(gen.rhs(problem.excitation).reshape(-1, 1))
+    x = np.empty_like(b)
+    res = ct.c_double()
     t0 = time.perf_counter()
-    A = asm.assemble_dense(gen, cap=problem.dense_cap)
-    t_fill = time.perf_counter() - t0
-    b = gen.rhs(problem.excitation)
-    t0 = time.perf_counter()
-    lu = sla.lu_factor(A)
-    t_factor = time.perf_counter() - t0
-    x = sla.lu_solve(lu, b)
-    bnorm = np.linalg.norm(b)
-    residual = float(np.linalg.norm(A @ x - b) / bnorm) if bnorm else 0.0
-    return SolveResult(x, residual, {"fill_s": t_fill, "factor_s": t_factor,
-                                     "n_dofs": problem.n_dofs,
-                                     "newton_fallbacks": gen.newton_fallbacks})
+    gen.dev.check(gen.dev.lib.cbie_dense_solve(gen.dev.h, int(problem.dense_cap), _ffi.ptr(b), 1, _ffi.ptr(x),
+                                               ct.byref(res), None, None))
+    wall = time.perf_counter() - t0
+    st = gen.stats()
+    return SolveResult(x[:, 0], float(res.value),
+                       {"fill_s": st.get("dense_fill_ms", 0.0) / 1e3, "factor_s": st.get("dense_lu_ms", 0.0) / 1e3,
+                        "solve_s": st.get("dense_solve_ms", 0.0) / 1e3, "wall_s": wall,
+                        "n_dofs": problem.n_dofs, "dense_bytes": 16 * problem.n_dofs ** 2,
+                        "peak_rss_bytes": _peak_rss_bytes(),
+                        "memory_method": "ru_maxrss sampling + logical array accounting",
+                        "newton_fallbacks": gen.newton_fallbacks})
