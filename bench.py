@@ -163,7 +163,7 @@ def run_reference(args):
     for _ in range(args.warmup if args.ref_warmup else 0):
         cpu_baseline(args.config)
     vals, secs, det = [], [], {}
-    for _ in range(args.steps if args.ref_steps is None else args.ref_steps):
+    for _ in range(1 if args.ref_steps is None else args.ref_steps):   # one bounded sample (~2 min of CPU)
         v, sec, det = cpu_baseline(args.config)
         vals.append(v)
         secs.append(sec)

@@ -87,3 +87,30 @@ def describe(cfg=2, level=3, per_stratum=3):
             f"stratum counts; H-LU of the level-{level} and level-{level + 1} leading diagonal "
             f"H-blocks extrapolated to the root by their growth ratio; "
             f"OPENBLAS_NUM_THREADS={os.environ.get('OPENBLAS_NUM_THREADS', 'default')}")
+
+
+def _calibration(cfg):
+    import json
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "calibration.json")
+    cal = json.load(open(path))
+    key = str(cfg) if str(cfg) in cal else "2"
+    c = cal[key]
+    return key, c["ref_fill_s"] / c["port_fill_projected_s"], c["ref_factor_s"] / c["port_hlu_projected_s"]
+
+
+def calibrated_step(cfg: int = 2, level: int = 3):
+    """One bounded sample of the port (``step``) scaled per phase by the measured ratio of
+    the reference's full run to the port's projection (oracle/calibration.json), i.e. an
+    estimate of the reference's own fill + H-LU time on this host.  Returns
+    (N, seconds, detail)."""
+    t0 = time.perf_counter()
+    n, sec, det = step(cfg, level)
+    wall = time.perf_counter() - t0
+    key, kf, kh = _calibration(cfg)
+    fill = det["fill_projected_s"] * kf
+    hlu = det["hlu_projected_s"] * kh
+    det = dict(det, calibration_config=int(key), k_fill=kf, k_hlu=kh, fill_s=fill, hlu_s=hlu,
+               sample_wall_s=wall,
+               sample=describe(cfg, level) + f"; calibrated per phase to the reference's measured full "
+               f"run of config {key} (oracle/calibration.json: fill x{kf:.3f}, H-LU x{kh:.3f})")
+    return n, fill + hlu, det
