@@ -129,6 +129,30 @@ int cbie_fill_dense(cbie_ctx* ctx, int64_t cap, cbie_c128* out);
 int cbie_dense_solve(cbie_ctx* ctx, int64_t cap, const cbie_c128* b, int nrhs, cbie_c128* x,
                      double* residual, cbie_c128* lu_out, int32_t* piv_out);
 
+/* H-matrix from host-evaluated leaves (any generator of the reference's protocol, e.g.
+ * the reference tests' KernelGen / IdGen / ZeroGen, tests/test_hmatrix.py:9-36, 228-274):
+ *   cbie_hmatrix_layout  host only: cluster + block tree of a point cloud
+ *                        (build_cluster_tree / build_block_tree, hmatrix.py:82, 344);
+ *                        dof_perm [npts*C] (new -> original dof), leaves [nleaf][5]
+ *                        (r_lo, r_hi, c_lo, c_hi in permuted points, admissible); NULL ok
+ *   cbie_hmatrix_import  data = every leaf's block, row-major m x n over the permuted
+ *                        dofs, concatenated in leaf order; dense leaves stored, admissible
+ *                        ones compressed on the device (truncated SVD, s > tol s_0) and
+ *                        demoted above min(m, n) / 2 (HMatrix._fill_leaf, hmatrix.py:243-264).
+ *                        The handle takes cbie_hlu_factor / cbie_hmatvec like a built one. */
+/* Host only: the layout of the sharded H-matrix after the exchange (csrc/shard.cu,
+ * shard_layout), a pure function of the leaf shapes m[], n[], admissibility adm[],
+ * owners (cbie_partition_lpt) and the all-reduced info[2 * leaf] = (rank, demoted):
+ * leaf_off [nleaf][3] dense / U / V arena offsets (-1: none), ranges [world][4] each
+ * owner's dense range and tail (the spans it broadcasts), total = arena elements. */
+int cbie_shard_layout_host(int nleaf, const int* m, const int* n, const uint8_t* adm, const int* owner,
+                           const int* info, int world, int64_t* leaf_off, int64_t* ranges, int64_t* total);
+
+int cbie_hmatrix_layout(const double* pts, int64_t npts, int C, int n_leaf, double eta, int64_t* dof_perm,
+                        int64_t* leaves, int64_t* nleaf);
+int cbie_hmatrix_import(cbie_ctx* ctx, const double* pts, int64_t npts, int C, int n_leaf, double eta, double tol,
+                        const cbie_c128* data, cbie_hmat** out);
+
 /* H-matrix of the equilibrated system: cluster tree, block tree, dense leaves,
  * batched ACA + recompression, demotion.  Replaces build_hmatrix
  * (solver.py:132-145): build_cluster_tree (hmatrix.py:82), build_block_tree

@@ -46,6 +46,9 @@ _SIGS = {
     "cbie_dense_solve": (ct.c_int, [P, ct.c_int64, P, ct.c_int, P, ct.POINTER(ct.c_double), P, P]),
     "cbie_hmatrix_build": (ct.c_int, [P, ct.c_int, ct.c_double, ct.c_double, ct.POINTER(P)]),
     "cbie_hmatrix_destroy": (None, [P]),
+    "cbie_hmatrix_layout": (ct.c_int, [P, ct.c_int64, ct.c_int, ct.c_int, ct.c_double, P, P, I64P]),
+    "cbie_hmatrix_import": (ct.c_int, [P, P, ct.c_int64, ct.c_int, ct.c_int, ct.c_double, ct.c_double, P,
+                                       ct.POINTER(P)]),
     "cbie_hmatrix_tree": (ct.c_int, [P, P, P, I64P]),
     "cbie_hmatrix_leaf": (ct.c_int, [P, ct.c_int64, ct.POINTER(ct.c_int), ct.POINTER(ct.c_int), P, P]),
     "cbie_hmatvec": (ct.c_int, [P, P, P, ct.c_int]),
@@ -63,6 +66,7 @@ _SIGS = {
                                          ct.POINTER(ct.c_int), P, P]),
     "cbie_stats_json": (ct.c_int, [P, ct.c_int, ct.c_char_p, ct.c_size_t]),
     "cbie_partition_lpt": (None, [P, ct.c_int64, ct.c_int, P]),
+    "cbie_shard_layout_host": (ct.c_int, [ct.c_int, P, P, P, P, P, ct.c_int, P, P, I64P]),
     "cbie_nccl_unique_id": (ct.c_int, [ct.c_char_p, ct.c_int]),
     "cbie_dist_init": (ct.c_int, [P, ct.c_char_p, ct.c_int, ct.c_int]),
     "cbie_dist_finalize": (None, [P]),

@@ -515,6 +515,17 @@ struct cbie_hlu {
   int64_t npiv = 0;
   int nslot_leaf = 0;
   int cap_boost = 1;               // factor leaf capacity multiplier (raised on truncation overflow)
+  // Factor storage: the work buffer of the plan cache that computed them (no copy of the
+  // factors after the factorisation; `alias` = that cache) until the cache is needed by
+  // another factorisation or released -- then they move to `arena` (copy-on-reuse).
+  zc* fac = nullptr;
+  int64_t fac_n = 0;
+  void* alias = nullptr;
+  void own() {
+    fac = arena.p;
+    fac_n = (int64_t)arena.n;
+  }
+  ~cbie_hlu();
   std::map<std::string, double> stat;
 };
 
@@ -1684,6 +1695,7 @@ struct PlanCache {
   uint64_t key = 0;
   Plan plan;
   DBuf<zc> work;
+  cbie_hlu* owner = nullptr;   // factors living in `work` (cbie_hlu::alias)
   TruncWork tw[TW_PER_LANE * TRUNC_LANES];   // recompression workspaces (per lane: s, s2, s3)
   int64_t leaf_end = 0;
 };
@@ -1707,6 +1719,27 @@ uint64_t fnv(uint64_t h, int64_t v) {
 }  // namespace
 
 
+// one-rhs solve temporaries kept behind the factors (hlu_solve_impl bounds them)
+static int64_t solve_reserve(int64_t N) { return std::max<int64_t>(N * 32, (int64_t)1 << 24) + 4 * N; }
+
+// move factors that live in a plan cache's work buffer into their own arena
+static void hlu_detach(cbie_hlu* F) {
+  if (!F || !F->alias) return;
+  PlanCache* pc = static_cast<PlanCache*>(F->alias);
+  cudaStream_t s = F->H->ctx->stream;
+  F->arena.alloc((size_t)(F->leaf_end + solve_reserve(F->H->N)) + 1);
+  CK(cudaMemcpyAsync(F->arena.p, pc->work.p, sizeof(zc) * F->leaf_end, cudaMemcpyDeviceToDevice, s));
+  CK(cudaStreamSynchronize(s));
+  F->own();
+  F->alias = nullptr;
+  pc->owner = nullptr;
+  F->stat["factors_detached"] = 1;
+}
+
+cbie_hlu::~cbie_hlu() {
+  if (alias) static_cast<PlanCache*>(alias)->owner = nullptr;
+}
+
 // drop the cached H-LU workspace when HBM is needed elsewhere
 void hlu_trim_cache(bool force) {
   std::lock_guard<std::recursive_mutex> lk(g_hlu_mutex);
@@ -1716,6 +1749,7 @@ void hlu_trim_cache(bool force) {
   fr = mem_free_bytes(&tot);
   // keep the plan (small); release the workspace only when HBM runs short
   if (force || (double)fr < 0.25 * (double)tot) {
+    hlu_detach(g_plan_cache->owner);
     g_plan_cache->work.release();
     for (auto& w : g_plan_cache->tw) w.release();
   }
@@ -1771,7 +1805,7 @@ static int64_t hlu_layout(cbie_hlu* F, std::vector<CopySeg>& segs) {
 static int64_t hlu_pool_budget(int64_t leaf_end, int share) {
   size_t fr = 0, tot = 0;
   fr = mem_free_bytes(&tot);
-  double gb = 0.6 * ((double)fr / share - 2.0 * (double)leaf_end * sizeof(zc)) / (double)(1ll << 30) - 4.0;
+  double gb = 0.6 * ((double)fr / share - 1.0 * (double)leaf_end * sizeof(zc)) / (double)(1ll << 30) - 4.0;
   gb = std::max(4.0, std::min(gb, 120.0));
   if (getenv("CBIE_POOL_GB")) gb = atof(getenv("CBIE_POOL_GB"));
   return (int64_t)(gb * (double)(1ll << 30)) / (int64_t)sizeof(zc);
@@ -1819,7 +1853,14 @@ static void hlu_factor_impl(cbie_hlu* F) {
   const bool use_cache = getenv("CBIE_NO_PLAN_CACHE") == nullptr;
   auto& g_plan_cache = g_plan_caches[c->device];
   auto t0 = std::chrono::steady_clock::now();
+  // the previous factors leave this cache's work buffer before it is reused
+  if (g_plan_cache && g_plan_cache->owner && g_plan_cache->owner != F) hlu_detach(g_plan_cache->owner);
   if (!(use_cache && g_plan_cache && g_plan_cache->key == key)) {
+    if (g_plan_cache && g_plan_cache->owner == F) {   // re-factorisation of F (capacity retry)
+      F->alias = nullptr;
+      F->fac = nullptr;
+      F->fac_n = 0;
+    }
     g_plan_cache.reset();   // release the previous plan's workspace first
     auto pc = std::make_unique<PlanCache>();
     hlu_record(F, pc->plan.R, leaf_end, hlu_pool_budget(leaf_end, 1), false);
@@ -1861,13 +1902,12 @@ static void hlu_factor_impl(cbie_hlu* F) {
   tm.start(s);
   Exec ex = run_plan(PL, work.p, F->ranks.p, F->piv.p, F->rcond.p, flag.p, ovf.p, g_plan_cache->tw, F->tol, s);
   F->stat["factor_device_ms"] = tm.stop_ms(s);
-  // the factors keep only their storage; the workspace stays with the plan cache
-  // + room for the temporaries of a one-rhs solve (its tape bounds them, hlu_solve_impl), so
-  // the first solve does not reallocate and copy the factors
-  const int64_t N = H->N;
-  F->arena.alloc((size_t)(leaf_end + std::max(solve_cache_temps(leaf_end),
-                                              std::max<int64_t>(N * 32, (int64_t)1 << 24) + 4 * N)) + 1);
-  CK(cudaMemcpyAsync(F->arena.p, work.p, sizeof(zc) * leaf_end, cudaMemcpyDeviceToDevice, s));
+  // the factors stay in the work buffer (copy-on-reuse: hlu_detach)
+  F->arena.release();
+  F->fac = work.p;
+  F->fac_n = (int64_t)work.n;
+  F->alias = g_plan_cache.get();
+  g_plan_cache->owner = F;
   CK(cudaStreamSynchronize(s));
   int hflag = 0;
   unsigned long long hovf = 0;
@@ -2048,16 +2088,20 @@ static void hlu_solve_impl(cbie_hlu* F, const zc* b, zc* x, int nrhs) {
     g_solve_leaf_ends[H->ctx->device] = F->leaf_end;
   }
   SolveCache& SC = *g_solve_cache;
-  // arena for the solve: factors (shared) + temps: allocate temps after the factor arena
+  // arena for the solve: factors + temps behind them
   const int64_t need = F->leaf_end + SC.pool_top + 1;
-  if ((int64_t)F->arena.n < need) {
-    DBuf<zc> bigger;
-    bigger.alloc(need);
-    CK(cudaMemcpyAsync(bigger.p, F->arena.p, sizeof(zc) * F->leaf_end, cudaMemcpyDeviceToDevice, s));
-    std::swap(bigger.p, F->arena.p);
-    std::swap(bigger.n, F->arena.n);
+  if (F->fac_n < need) {
+    hlu_detach(F);
+    if ((int64_t)F->arena.n < need) {
+      DBuf<zc> bigger;
+      bigger.alloc(need);
+      CK(cudaMemcpyAsync(bigger.p, F->arena.p, sizeof(zc) * F->leaf_end, cudaMemcpyDeviceToDevice, s));
+      std::swap(bigger.p, F->arena.p);
+      std::swap(bigger.n, F->arena.n);
+      F->own();
+    }
   }
-  CK(cudaMemcpyAsync(F->arena.p + SC.xoff, bp.data(), sizeof(zc) * bp.size(), cudaMemcpyHostToDevice, s));
+  CK(cudaMemcpyAsync(F->fac + SC.xoff, bp.data(), sizeof(zc) * bp.size(), cudaMemcpyHostToDevice, s));
   // slots: leaves keep their factor ranks (device to device), the solve's own after them
   std::vector<int> r0 = SC.plan.R.init_ranks;
   if ((int64_t)SC.ranks.n != (int64_t)r0.size()) SC.ranks.alloc(r0.size());
@@ -2070,7 +2114,7 @@ static void hlu_solve_impl(cbie_hlu* F, const zc* b, zc* x, int nrhs) {
   // one stream, level by level: the solve is a ~1,800-level chain of small products whose
   // cross-stream event hand-offs cost more than the overlap gains
   const bool solve_ms = getenv("CBIE_SOLVE_MS") != nullptr;
-  Exec ex = run_plan(SC.plan, F->arena.p, SC.ranks.p, F->piv.p, SC.rc.p, SC.flag.p, SC.ovf.p, SC.tw, F->tol, s,
+  Exec ex = run_plan(SC.plan, F->fac, SC.ranks.p, F->piv.p, SC.rc.p, SC.flag.p, SC.ovf.p, SC.tw, F->tol, s,
                      solve_ms ? 0 : 1, 1 << 30);
   F->stat["solve_device_ms"] = tm.stop_ms(s);
   F->stat["solve_levels"] = ex.levels;
@@ -2083,7 +2127,7 @@ static void hlu_solve_impl(cbie_hlu* F, const zc* b, zc* x, int nrhs) {
       if (ex.kind_ms[k] > 0.0) F->stat[std::string("solve_ms_") + nm[k]] = ex.kind_ms[k];
     }
   }
-  CK(cudaMemcpy(bp.data(), F->arena.p + SC.xoff, sizeof(zc) * bp.size(), cudaMemcpyDeviceToHost));
+  CK(cudaMemcpy(bp.data(), F->fac + SC.xoff, sizeof(zc) * bp.size(), cudaMemcpyDeviceToHost));
   for (size_t p = 0; p < T.pperm.size(); ++p)
     for (int c = 0; c < C; ++c) {
       const int64_t ni = (int64_t)p * C + c, oi = (int64_t)T.pperm[p] * C + c;
@@ -2212,7 +2256,10 @@ int cbie_hlu_dist_plan_host(const double* pts, int64_t npts, int C, int n_leaf, 
   return CBIE_OK;
 }
 
-void cbie_hlu_destroy(cbie_hlu* f) { delete f; }
+void cbie_hlu_destroy(cbie_hlu* f) {
+  std::lock_guard<std::recursive_mutex> lk(g_hlu_mutex);
+  delete f;
+}
 
 int cbie_hlu_leaf(cbie_hlu* f, int64_t leaf, int* kind, int* rank, cbie_c128* D_or_U,
                   cbie_c128* V, int32_t* piv) {
@@ -2227,7 +2274,7 @@ int cbie_hlu_leaf(cbie_hlu* f, int64_t leaf, int* kind, int* rank, cbie_c128* D_
       *rank = 0;
       if (D_or_U) {
         std::vector<zc> cm((size_t)m * n);
-        CK(cudaMemcpy(cm.data(), f->arena.p + L.off_d, sizeof(zc) * cm.size(), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(cm.data(), f->fac + L.off_d, sizeof(zc) * cm.size(), cudaMemcpyDeviceToHost));
         zc* o = reinterpret_cast<zc*>(D_or_U);
         for (int i = 0; i < m; ++i)
           for (int j = 0; j < n; ++j) o[(size_t)i * n + j] = cm[(size_t)j * m + i];
@@ -2241,8 +2288,8 @@ int cbie_hlu_leaf(cbie_hlu* f, int64_t leaf, int* kind, int* rank, cbie_c128* D_
       *rank = r;
       if (D_or_U && r) {
         std::vector<zc> cu((size_t)m * r), cv((size_t)n * r);
-        CK(cudaMemcpy(cu.data(), f->arena.p + L.off_u, sizeof(zc) * cu.size(), cudaMemcpyDeviceToHost));
-        CK(cudaMemcpy(cv.data(), f->arena.p + L.off_v, sizeof(zc) * cv.size(), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(cu.data(), f->fac + L.off_u, sizeof(zc) * cu.size(), cudaMemcpyDeviceToHost));
+        CK(cudaMemcpy(cv.data(), f->fac + L.off_v, sizeof(zc) * cv.size(), cudaMemcpyDeviceToHost));
         zc* ou = reinterpret_cast<zc*>(D_or_U);
         zc* ov = reinterpret_cast<zc*>(V);
         for (int i = 0; i < m; ++i)

@@ -275,6 +275,7 @@ void dist_finish(cbie_hlu* F, RankState& S, int64_t leaf_end, int hflag, unsigne
   const int nleaf = (int)F->tree.leaves.size();
   F->arena.alloc((size_t)leaf_end + 1);
   CK(cudaMemcpyAsync(F->arena.p, S.work.p, sizeof(zc) * leaf_end, cudaMemcpyDeviceToDevice, s));
+  F->own();
   std::swap(F->ranks.p, S.ranks.p);
   std::swap(F->ranks.n, S.ranks.n);
   std::swap(F->piv.p, S.piv.p);

@@ -44,6 +44,57 @@ int aca_budget_of(int m, int n) { return std::max(1, std::min(m, n) / 2); }
 
 }  // namespace
 
+// Global layout of the exchanged H-matrix (a pure function of the leaf shapes, the
+// admissibility flags, the owners and the all-reduced (rank, demoted) pairs, so every
+// rank computes the same one): dense leaves owner-major [dlo[o], dhi[o]) in leaf order,
+// then each owner's tail [tlo[o], thi[o]) holding its demoted leaves (nd) and its
+// low-rank leaves with their exact ranks (nu, nv; capacity max(r, 1)).
+struct ShardLayout {
+  std::vector<int64_t> dlo, dhi, tlo, thi, nu, nv, nd, dd;
+  int64_t total = 0;
+};
+ShardLayout shard_layout(const int* m, const int* n, const uint8_t* adm, const int* owner, const int* info, int nleaf,
+                         int W) {
+  ShardLayout Y;
+  Y.dlo.assign(W, 0);
+  Y.dhi.assign(W, 0);
+  Y.tlo.assign(W, 0);
+  Y.thi.assign(W, 0);
+  Y.nu.assign(nleaf, -1);
+  Y.nv.assign(nleaf, -1);
+  Y.nd.assign(nleaf, -1);
+  Y.dd.assign(nleaf, -1);
+  int64_t off = 0;
+  for (int o = 0; o < W; ++o) {
+    Y.dlo[o] = off;
+    for (int li = 0; li < nleaf; ++li)
+      if (!adm[li] && owner[li] == o) {
+        Y.dd[li] = off;
+        off += (int64_t)m[li] * n[li];
+      }
+    Y.dhi[o] = off;
+  }
+  for (int o = 0; o < W; ++o) {
+    Y.tlo[o] = off;
+    for (int li = 0; li < nleaf; ++li) {
+      if (!adm[li] || owner[li] != o) continue;
+      if (info[2 * li + 1]) {
+        Y.nd[li] = off;
+        off += (int64_t)m[li] * n[li];
+      } else {
+        const int cap = std::max(info[2 * li], 1);
+        Y.nu[li] = off;
+        off += (int64_t)m[li] * cap;
+        Y.nv[li] = off;
+        off += (int64_t)n[li] * cap;
+      }
+    }
+    Y.thi[o] = off;
+  }
+  Y.total = off;
+  return Y;
+}
+
 void shard_assign(cbie_hmat* H) {
   const Tree& T = H->tree;
   const int nleaf = (int)T.leaves.size();
@@ -91,33 +142,14 @@ void shard_exchange(cbie_hmat* H) {
   CK(cudaMemcpyAsync(info.data(), dinfo.p, sizeof(int) * info.size(), cudaMemcpyDeviceToHost, s));
   CK(cudaStreamSynchronize(s));
   // b. global layout: dense ranges (unchanged, owner-major), then each owner's tail
-  std::vector<int64_t> dlo(W, 0), dhi(W, 0), tlo(W, 0), thi(W, 0);
-  int64_t off = 0;
-  for (int o = 0; o < W; ++o) {
-    dlo[o] = off;
-    for (int li = 0; li < nleaf; ++li)
-      if (!H->adm[li] && H->owner[li] == o) off += (int64_t)T.leaves[li].m * T.leaves[li].n;
-    dhi[o] = off;
+  std::vector<int> lm(nleaf), ln(nleaf);
+  for (int li = 0; li < nleaf; ++li) {
+    lm[li] = T.leaves[li].m;
+    ln[li] = T.leaves[li].n;
   }
-  std::vector<int64_t> nu(nleaf, -1), nv(nleaf, -1), nd(nleaf, -1);
-  for (int o = 0; o < W; ++o) {
-    tlo[o] = off;
-    for (int li = 0; li < nleaf; ++li) {
-      if (!H->adm[li] || H->owner[li] != o) continue;
-      const auto& L = T.leaves[li];
-      if (info[2 * li + 1]) {
-        nd[li] = off;
-        off += (int64_t)L.m * L.n;
-      } else {
-        const int cap = std::max(info[2 * li], 1);
-        nu[li] = off;
-        off += (int64_t)L.m * cap;
-        nv[li] = off;
-        off += (int64_t)L.n * cap;
-      }
-    }
-    thi[o] = off;
-  }
+  const ShardLayout Y = shard_layout(lm.data(), ln.data(), H->adm.data(), H->owner.data(), info.data(), nleaf, W);
+  const auto &dlo = Y.dlo, &dhi = Y.dhi, &tlo = Y.tlo, &thi = Y.thi, &nu = Y.nu, &nv = Y.nv, &nd = Y.nd;
+  const int64_t off = Y.total;
   // c. new arena with this rank's data in place
   DBuf<zc> na;
   na.alloc(std::max<int64_t>(off, 1));
@@ -216,6 +248,28 @@ void cbie_partition_lpt(const double* cost, int64_t n, int world, int* owner) {
     owner[i] = best;
     load[best] += cost[i];
   }
+}
+
+// host only: the exchange layout of shard.cu (shard_layout) for the gloo tests
+//   leaf_off [nleaf][3]: dense offset (dense / demoted leaves), U offset, V offset (-1: none)
+//   ranges   [world][4]: dense range lo, hi, tail lo, hi;  total: arena size (elements)
+int cbie_shard_layout_host(int nleaf, const int* m, const int* n, const uint8_t* adm, const int* owner,
+                           const int* info, int world, int64_t* leaf_off, int64_t* ranges, int64_t* total) {
+  if (nleaf < 0 || world < 1) return CBIE_EINVALID;
+  const ShardLayout Y = shard_layout(m, n, adm, owner, info, nleaf, world);
+  for (int li = 0; li < nleaf; ++li) {
+    leaf_off[3 * li] = Y.nd[li] >= 0 ? Y.nd[li] : Y.dd[li];
+    leaf_off[3 * li + 1] = Y.nu[li];
+    leaf_off[3 * li + 2] = Y.nv[li];
+  }
+  for (int o = 0; o < world; ++o) {
+    ranges[4 * o] = Y.dlo[o];
+    ranges[4 * o + 1] = Y.dhi[o];
+    ranges[4 * o + 2] = Y.tlo[o];
+    ranges[4 * o + 3] = Y.thi[o];
+  }
+  *total = Y.total;
+  return CBIE_OK;
 }
 
 int cbie_nccl_unique_id(char* out, int cap) {

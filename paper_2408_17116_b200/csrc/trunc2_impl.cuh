@@ -804,6 +804,101 @@ __device__ int pchol(zc* G, int k, int* perm, double thr_rel, Smem& S, bool trac
   return j;
 }
 
+// Pivoted Cholesky of the Hermitian PSD G (k x k <= 64, ld k, shared) by a group of W warps
+// (gw: warp index in the group) synchronised by the named barrier bid -- no CTA-wide
+// barriers, so two groups factor two matrices concurrently.  No row / column
+// interchanges: the Schur complement is updated in place over the not-yet-pivoted
+// indices (lanes own rows, warps own columns), row j of R is stored over row perm[j] of
+// G, and the pivoted upper-triangular R is gathered at the end into the same layout as
+// pchol (row j < kk holds row j of R, columns in pivot order; lower part zero) through
+// tmp (k x k, shared or global).  Same stop rules as pchol; perm is completed with the
+// unpivoted columns in increasing order.  Returns kk.
+__device__ __forceinline__ void gbar(int id, int nth) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nth) : "memory"); }
+
+__device__ int pchol_grp(zc* G, int k, int* perm, double thr_rel, bool trace_stop, int W, int gw, int bid, zc* tmp,
+                         double* dg) {
+  const int lane = threadIdx.x & 31, nth = 32 * W;
+  const bool v0 = lane < k, v1 = lane + 32 < k;
+  // dg (k doubles, shared): the remaining diagonal, kept beside G so the pivot search
+  // reads it without the bank conflicts of G's stride-(k+1) diagonal
+  double d0 = v0 ? G[lane * k + lane].x : 0.0, d1 = v1 ? G[(lane + 32) * k + lane + 32].x : 0.0;
+  const double dmax = warp_max(fmax(d0, d1));
+  const double thr = thr_rel * dmax, iscale = dmax > 0.0 ? 1.0 / dmax : 0.0;   // pivot keys in [0, 1]
+  if (gw == 0) {
+    if (v0) dg[lane] = d0;
+    if (v1) dg[lane + 32] = d1;
+  }
+  gbar(bid, nth);
+  unsigned long long done = 0ull;
+  int j = 0;
+  for (; j < k; ++j) {
+    const bool f0 = v0 && !(done >> lane & 1ull), f1 = v1 && !(done >> (lane + 32) & 1ull);
+    const double e0 = f0 ? dg[lane] : -1.0, e1 = f1 ? dg[lane + 32] : -1.0;
+    // pivot: largest remaining diagonal (compared in float precision, which only decides
+    // among near-equal pivots), lowest index among equal keys
+    const unsigned k0 = e0 > 0.0 ? __float_as_uint((float)(e0 * iscale)) : 0u;
+    const unsigned k1 = e1 > 0.0 ? __float_as_uint((float)(e1 * iscale)) : 0u;
+    const unsigned km = __reduce_max_sync(FULL, max(k0, k1));
+    const unsigned m0 = __ballot_sync(FULL, k0 == km), m1 = __ballot_sync(FULL, k1 == km);
+    const int p = m0 ? __ffs(m0) - 1 : (m1 ? __ffs(m1) + 31 : k);
+    const double best = p < k ? dg[p] : -1.0;
+    bool go;
+    if (trace_stop) {
+      double tr = fmax(e0, 0.0) + fmax(e1, 0.0);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) tr += __shfl_xor_sync(FULL, tr, o);
+      go = tr > thr && best > 0.0 && km > 0u;
+    } else {
+      go = best > thr && best > 0.0 && km > 0u;
+    }
+    if (!go) break;   // same data in every warp of the group: a uniform exit
+    const double rjj = sqrt(best), inv = 1.0 / rjj;
+    done |= 1ull << p;
+    // row p of R over the remaining columns: R(j, c) = G(p, c) / rjj = conj(G(c, p)) / rjj
+    const bool g0 = v0 && !(done >> lane & 1ull), g1 = v1 && !(done >> (lane + 32) & 1ull);
+    const zc r0 = g0 ? zscale(zconj(G[p * k + lane]), inv) : zmk(0.0, 0.0);
+    const zc r1 = g1 ? zscale(zconj(G[p * k + lane + 32]), inv) : zmk(0.0, 0.0);
+    if (gw == 0 && lane == 0) perm[j] = p;
+    gbar(bid, nth);   // the diagonal and column p are read by every warp before any update
+    for (int b = gw; b < k; b += W) {
+      if (b == p) {
+        if (lane == 0) G[p * k + p] = zmk(rjj, 0.0);
+        continue;
+      }
+      if (done >> b & 1ull) continue;
+      const zc rb = zshfl(b < 32 ? r0 : r1, b & 31);
+      zc* col = G + b * k;
+      if (g0) {
+        const zc v = zsub(col[lane], zcmul(r0, rb));
+        col[lane] = v;
+        if (lane == b) dg[b] = v.x;
+      }
+      if (g1) {
+        const zc v = zsub(col[lane + 32], zcmul(r1, rb));
+        col[lane + 32] = v;
+        if (lane + 32 == b) dg[b] = v.x;
+      }
+      if (lane == 0) col[p] = rb;   // R(j, b) over G(p, b): row p is never read again
+    }
+    gbar(bid, nth);
+  }
+  const int kk = j;
+  if (gw == 0 && lane == 0) {
+    int q = kk;
+    for (int c = 0; c < k; ++c)
+      if (!(done >> c & 1ull)) perm[q++] = c;
+  }
+  gbar(bid, nth);
+  for (int e = gw * 32 + lane; e < k * k; e += nth) {
+    const int r = e % k, c = e / k;   // element (r, c) of the pivoted R
+    tmp[e] = (r < kk && c >= r) ? G[perm[c] * k + perm[r]] : zmk(0.0, 0.0);
+  }
+  gbar(bid, nth);
+  for (int e = gw * 32 + lane; e < k * k; e += nth) G[e] = tmp[e];
+  gbar(bid, nth);
+  return kk;
+}
+
 // Z (kk x r, ld kk, shared) <- R11^{-1} Z with R11 = rows/cols 0..kk-1 of R (ld k, upper),
 // then row j scaled by sc[j]; one warp per column, lanes hold rows lane, lane + 32
 __device__ void tri_solve_cols(const zc* R, int k, int kk, zc* Z, int r, const double* sc) {
@@ -1014,9 +1109,18 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
     tc[slot] += t - tf;
     tf = t;
   };
-  // 3. pivoted Cholesky
-  const int ku = pchol(Gu, k, pu, CHOL_EPS, S);
-  const int kv = pchol(Gv, k, pv, CHOL_EPS, S);
+  // 3. pivoted Choleskys of both Grams concurrently: warps 0..NW/2-1 factor G_u (X2 as
+  //    gather space), the others G_v (gather through the global scratch Rvg, written later)
+  __shared__ int kuv[2];
+  {
+    const int w = threadIdx.x >> 5;
+    const bool ga = w < NW / 2;
+    const int kr = pchol_grp(ga ? Gu : Gv, k, ga ? pu : pv, CHOL_EPS, false, NW / 2, ga ? w : w - NW / 2,
+                             ga ? 1 : 2, ga ? X2 : Rvg, ga ? scu : scv);
+    if ((threadIdx.x & (NT / 2 - 1)) == 0) kuv[ga ? 0 : 1] = kr;
+    __syncthreads();
+  }
+  const int ku = kuv[0], kv = kuv[1];
   stamp(5);
   if (ku == 0 || kv == 0) return 0;
   for (int c = threadIdx.x; c < k; c += NT) {
@@ -1057,7 +1161,7 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   for (int e = threadIdx.x; e < kk1 * kk2; e += NT) Mg[e] = X2[e];
   __syncthreads();
   stamp(6);
-  const int kp = pchol(H, kk1, S.perm, (GDELTA * tol) * (GDELTA * tol), S, true);
+  const int kp = pchol_grp(H, kk1, S.perm, (GDELTA * tol) * (GDELTA * tol), true, NW, threadIdx.x >> 5, 1, X2, scu);
   stamp(7);
   zc* Gp = Gv;   // R R^H (kp x kp)
   zc* Z = X2;    // eigenvectors (kp x kp)

@@ -63,3 +63,20 @@ def hlu_dist_plan(points, C: int, n_leaf: int, eta: float, world: int):
     keys = ("tasks", "messages", "xfer_buffers", "xfer_elems", "conflicts", "levels", "row_level",
             "tasks_min", "tasks_max", "final_elems", "leaves")
     return dict(zip(keys, (int(v) for v in st))), owner
+
+
+def shard_layout(m, n, adm, owner, info, world: int):
+    """Host-only exchange layout of the sharded fill (cbie_shard_layout_host, the function
+    csrc/shard.cu's exchange uses): (leaf offsets [nleaf][3], ranges [world][4], total)."""
+    lib = _ffi.load()
+    m = np.ascontiguousarray(m, np.int32)
+    n = np.ascontiguousarray(n, np.int32)
+    adm = np.ascontiguousarray(adm, np.uint8)
+    owner = np.ascontiguousarray(owner, np.int32)
+    info = np.ascontiguousarray(info, np.int32)
+    off = np.empty((m.size, 3), np.int64)
+    rng = np.empty((world, 4), np.int64)
+    tot = ct.c_int64()
+    _ffi.check(lib.cbie_shard_layout_host(int(m.size), _ffi.ptr(m), _ffi.ptr(n), _ffi.ptr(adm), _ffi.ptr(owner),
+                                          _ffi.ptr(info), int(world), _ffi.ptr(off), _ffi.ptr(rng), ct.byref(tot)))
+    return off, rng, int(tot.value)

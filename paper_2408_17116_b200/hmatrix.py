@@ -40,6 +40,45 @@ class HMatrix:
         self.h = h
         self._stats = _ffi.stats(h, 1)
 
+    @classmethod
+    def from_generator(cls, points, C: int, n_leaf: int, eta: float, generator, tol: float,
+                       device: int = 0) -> "HMatrix":
+        """H-matrix of any host generator honouring the reference's protocol
+        (``block(rows, cols)``, hmatrix.py:243-264), e.g. the reference test-suite's
+        KernelGen / IdGen / ZeroGen (tests/test_hmatrix.py:9-36, 228-274): the cluster
+        and block trees of ``points`` (build_cluster_tree / build_block_tree), every
+        leaf's block evaluated through the generator on the host, dense leaves stored and
+        admissible ones compressed on the device (truncated SVD at tol, demotion above
+        the ACA budget; cbie_hmatrix_import)."""
+        from .assembly import Device
+        pts = np.ascontiguousarray(np.asarray(points, dtype=np.float64))
+        lib = _ffi.load()
+        n = ct.c_int64()
+        npts = pts.shape[0]
+        _ffi.check(lib.cbie_hmatrix_layout(_ffi.ptr(pts), npts, int(C), int(n_leaf), float(eta), None, None,
+                                           ct.byref(n)))
+        perm = np.empty(npts * C, np.int64)
+        lv = np.empty((n.value, 5), np.int64)
+        _ffi.check(lib.cbie_hmatrix_layout(_ffi.ptr(pts), npts, int(C), int(n_leaf), float(eta), _ffi.ptr(perm),
+                                           _ffi.ptr(lv), ct.byref(n)))
+        blocks = [np.asarray(generator.block(perm[r0 * C:r1 * C], perm[c0 * C:c1 * C]), complex).ravel()
+                  for r0, r1, c0, c1, _ in lv]
+        data = np.ascontiguousarray(np.concatenate(blocks) if blocks else np.zeros(1, complex))
+        self = cls.__new__(cls)
+        self.gen = None
+        self.dev = Device(device)
+        self.C = int(C)
+        self.N = npts * int(C)
+        self.eta = eta
+        self.aca_tol = tol
+        self.shard = None
+        h = ct.c_void_p()
+        self.dev.check(lib.cbie_hmatrix_import(self.dev.h, _ffi.ptr(pts), npts, int(C), int(n_leaf), float(eta),
+                                               float(tol), _ffi.ptr(data), ct.byref(h)))
+        self.h = h
+        self._stats = _ffi.stats(h, 1)
+        return self
+
     def __del__(self):
         h = getattr(self, "h", None)
         if h:

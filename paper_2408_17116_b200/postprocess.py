@@ -79,3 +79,23 @@ def rcs_cut(problem, gen, solution, phi_deg, theta_deg):
     ep = np.sum(F * phat, axis=1)
     sigma = 4 * np.pi * (np.abs(et) ** 2 + np.abs(ep) ** 2) / problem.excitation.amplitude ** 2
     return sigma, 10.0 * np.log10(np.maximum(sigma, 1e-300))
+
+
+def surface_current_vectors(gen, solution):
+    """Physical J (and M for Muller) at every node, (N_points, 3) each
+    (postprocess.py:45-62): J = (x_u a_u + x_v a_v) / sqrt(g) with the device frames."""
+    C = gen.C
+    F = np.asarray(solution).reshape(-1, C)
+    J = (F[:, 0, None] * gen.a_u + F[:, 1, None] * gen.a_v) / gen.sqrt_g[:, None]
+    M = (F[:, 2, None] * gen.a_u + F[:, 3, None] * gen.a_v) / gen.sqrt_g[:, None] if C == 4 else None
+    return J, M
+
+
+def current_error(gen, solution, points_idx, J_ref, w):
+    """Weighted relative L2 distance of the surface current to a reference current J_ref
+    at the node indices points_idx, weights w = node weight x sqrt(g) -- the
+    current_error_weighted of postprocess.mie_comparison (postprocess.py:275-314)."""
+    J, _ = surface_current_vectors(gen, solution)
+    d2 = np.sum(np.abs(J[points_idx] - J_ref) ** 2, axis=1)
+    r2 = np.sum(np.abs(J_ref) ** 2, axis=1)
+    return float(np.sqrt((w @ d2) / (w @ r2)))

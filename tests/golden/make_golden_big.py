@@ -217,7 +217,34 @@ def solve(prob, dense=False):
                 metrics=json.dumps(m, default=str))
 
 
+def mie_currents(cfg, n_patch=None, seed=41):
+    """The reference's Mie-series surface current J = n x H (mie.py:285-298) at the node
+    points of (a seeded subset of) the patches, with the node weights w sqrt(g) used by
+    postprocess.mie_comparison (postprocess.py:275-314)."""
+    from chebscat import mie
+    prob = ref_problem(cfg)
+    radius = {2: 2.0, 5: 8.0}[cfg]
+    P = len(prob.patches)
+    pids = np.arange(P) if n_patch is None else np.sort(
+        np.random.default_rng(seed).choice(P, size=n_patch, replace=False))
+    spec = mie.MieSpec(radius, prob.spec.outer, None, amplitude=prob.excitation.amplitude)
+    J, W, pts = [], [], []
+    for q in pids:
+        p = prob.patches[int(q)]
+        fb = p.node_frames()
+        Jm, _ = mie.mie_surface_current(spec, fb.position)
+        J.append(Jm)
+        W.append(p.node_weights() * fb.sqrt_g)
+        pts.append(fb.position)
+    save(f"cfg{cfg}_mie.npz", pids=pids.astype(np.int32), J=np.concatenate(J), w=np.concatenate(W),
+         pos=np.concatenate(pts), n_terms=spec.n_terms)
+
+
 def main(job):
+    if job == "mie":
+        mie_currents(2)
+        mie_currents(5, n_patch=64)
+        return
     cfg = int(job[3])
     what = job[5:]
     prob = ref_problem(cfg)

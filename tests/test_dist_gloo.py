@@ -60,7 +60,22 @@ def _leaf_costs(seed=5, n_dense=1272, n_lr=2008):
     return cost[rng.permutation(cost.size)]
 
 
+def _leaf_shapes(seed=5, n_dense=1272, n_lr=2008):
+    """Config-2-like leaf population: 192^2 dense leaves, 192^2 / 384^2 admissible ones."""
+    import numpy as np
+    rng = np.random.default_rng(seed)
+    m = np.concatenate([np.full(n_dense, 192), rng.choice([192, 384], size=n_lr, p=[0.8, 0.2])])
+    adm = np.concatenate([np.zeros(n_dense, np.uint8), np.ones(n_lr, np.uint8)])
+    perm = rng.permutation(m.size)
+    return m[perm].astype(np.int32), m[perm].astype(np.int32), adm[perm]
+
+
 def _shard_worker(rank, world, port, q):
+    """The exchange of csrc/shard.cu with gloo standing in for NCCL: the LPT partition
+    (cbie_partition_lpt) and the post-fill layout (cbie_shard_layout_host, the same
+    function shard_exchange calls) come from the library; the all-reduce of the
+    (rank, demoted) pairs and the per-owner broadcasts of the dense range and the tail
+    are the same collectives, issued through torch.distributed."""
     import numpy as np
     import torch
     import torch.distributed as dist
@@ -68,31 +83,56 @@ def _shard_worker(rank, world, port, q):
                       WORLD_SIZE=str(world))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     from paper_2408_17116_b200 import dist as cdist
-    cost = _leaf_costs()
+    m, n, adm = _leaf_shapes()
+    nleaf = m.size
+    cap = np.minimum(np.minimum(m, n) // 2, 24)
+    cost = np.where(adm == 1, 3.0 * cap * (m + n), m.astype(float) * n)   # shard.cu cost model
     owner = cdist.partition_lpt(cost, world)          # computed independently per rank
-    allo = [torch.zeros(cost.size, dtype=torch.int32) for _ in range(world)]
+    allo = [torch.zeros(nleaf, dtype=torch.int32) for _ in range(world)]
     dist.all_gather(allo, torch.from_numpy(owner.astype(np.int32)))
     same = all(torch.equal(allo[0], a) for a in allo)
-    # owner-major exchange plan: leaf data (here: its index repeated by size) packed in
-    # owner order, each owner broadcasts its contiguous range
-    size = (cost / cost.min()).round().astype(np.int64)
-    order = np.concatenate([np.flatnonzero(owner == o) for o in range(world)])
-    off = np.zeros(cost.size, np.int64)
-    off[order] = np.concatenate([[0], np.cumsum(size[order])[:-1]])
-    arena = torch.full((int(size.sum()),), -1.0, dtype=torch.float64)
-    for li in np.flatnonzero(owner == rank):
-        arena[off[li]:off[li] + size[li]] = float(li)
-    lo = [int(off[owner == o].min()) for o in range(world)]
-    hi = [int((off + size)[owner == o].max()) for o in range(world)]
-    for o in range(world):
-        seg = arena[lo[o]:hi[o]].clone()
-        dist.broadcast(seg, src=o)
-        arena[lo[o]:hi[o]] = seg
-    expect = np.repeat(np.arange(cost.size)[order], size[order]).astype(np.float64)
-    ok = bool(np.array_equal(arena.numpy(), expect))
+    # local fill: every owned admissible leaf gets a rank (a deterministic function of the
+    # leaf, as the ACA would give on any rank), one in 50 is demoted
+    rk = (np.arange(nleaf) * 7919 % 23 + 1).astype(np.int32)
+    dem = (np.arange(nleaf) % 50 == 3) & (adm == 1)
+    info = np.zeros(2 * nleaf, np.int32)
+    mine = owner == rank
+    info[0::2] = np.where(mine & (adm == 1) & ~dem, rk, 0)
+    info[1::2] = np.where(mine & dem, 1, 0)
+    t = torch.from_numpy(info.copy())
+    dist.all_reduce(t)                                # ncclAllReduce(sum) in shard.cu
+    info = t.numpy()
+    off, ranges, total = cdist.shard_layout(m, n, adm, owner, info, world)
+    # arena: every entry of a leaf holds the leaf index (dense / demoted: m n entries;
+    # low rank: U m r then V n r); this rank writes only its own leaves
+    arena = torch.full((total,), -1.0, dtype=torch.float64)
+    for li in np.flatnonzero(mine):
+        if off[li, 0] >= 0:
+            arena[off[li, 0]:off[li, 0] + m[li] * n[li]] = float(li)
+        elif info[2 * li] > 0:
+            r = info[2 * li]
+            arena[off[li, 1]:off[li, 1] + m[li] * r] = float(li)
+            arena[off[li, 2]:off[li, 2] + n[li] * r] = float(li)
+    for o in range(world):                            # grouped ncclBroadcast in shard.cu
+        for lo, hi in ((ranges[o, 0], ranges[o, 1]), (ranges[o, 2], ranges[o, 3])):
+            if hi > lo:
+                seg = arena[lo:hi].clone()
+                dist.broadcast(seg, src=o)
+                arena[lo:hi] = seg
+    a = arena.numpy()
+    ok = True
+    covered = 0
+    for li in range(nleaf):
+        if off[li, 0] >= 0:
+            sl = a[off[li, 0]:off[li, 0] + m[li] * n[li]]
+        else:
+            r = info[2 * li]
+            sl = np.concatenate([a[off[li, 1]:off[li, 1] + m[li] * r], a[off[li, 2]:off[li, 2] + n[li] * r]])
+        ok &= bool(np.all(sl == li))
+        covered += sl.size
+    spans = sum(int(ranges[o, 1] - ranges[o, 0] + ranges[o, 3] - ranges[o, 2]) for o in range(world))
     loads = [float(cost[owner == o].sum()) for o in range(world)]
-    contiguous = all(hi[o] - lo[o] == int(size[owner == o].sum()) for o in range(world))
-    q.put((rank, same, ok, loads, contiguous))
+    q.put((rank, same, ok, loads, bool(np.all(a >= 0)) and spans == total, float(cost.max())))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -107,11 +147,10 @@ def test_two_rank_leaf_sharding_and_exchange_plan():
     out = sorted(q.get(timeout=180) for _ in ps)
     for p in ps:
         p.join(timeout=60)
-    cost = _leaf_costs()
-    for rank, same, ok, loads, contiguous in out:
-        assert same and ok and contiguous
+    for rank, same, ok, loads, dense_cover, cmax in out:
+        assert same and ok and dense_cover
         # LPT bound: max load <= mean + largest item
-        assert max(loads) <= sum(loads) / 2 + cost.max()
+        assert max(loads) <= sum(loads) / 2 + cmax
         assert max(loads) / min(loads) < 1.01
 
 

@@ -176,3 +176,23 @@ def test_cfg1_large_leaves_solution():
     r = solve_direct(prob)
     assert _rel(r.solution, g["x_direct"]) <= 10 * prob.aca_tol
     assert r.residual <= 10 * prob.aca_tol
+
+
+def test_factors_survive_a_second_factorisation():
+    """Factors live in the plan cache's work buffer until another factorisation needs it
+    (copy-on-reuse, csrc/hlu.cu hlu_detach): an older factor object must still solve."""
+    from paper_2408_17116_b200 import configs, hmatrix as hm
+    prob = configs.problem(1)
+    gen = prob.generator()
+    H = hm.HMatrix(gen, prob.n_leaf, prob.eta, prob.aca_tol)
+    b = gen.rhs(prob.excitation) * gen.row_scale
+    F1 = hm.hlu_factor(H, prob.effective_trunc_tol)
+    x1 = F1.solve(b)
+    F2 = hm.hlu_factor(H, prob.effective_trunc_tol)       # reuses the work buffer
+    assert F1.stats().get("factors_detached", 0) == 0      # stats snapshot is taken at factor time
+    x1b = F1.solve(b)
+    x2 = F2.solve(b)
+    assert np.array_equal(x1, x1b)
+    assert np.array_equal(x1, x2)
+    del F2
+    assert np.array_equal(F1.solve(b), x1)

@@ -1,0 +1,120 @@
+"""The reference test-suite's H-matrix / H-LU known-answer tests (tests/test_hmatrix.py
+of chebscat: 2 x 2 dense vs LAPACK 216-225, identity 228-245, multi-rhs residual
+247-256, zero rhs 259-262, SingularDiagonal 265-280) run against the GPU H-LU, on
+H-matrices imported from the same synthetic generators (HMatrix.from_generator ->
+cbie_hmatrix_import).  The generators are restated here from the reference tests."""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+class KernelGen:
+    """Synthetic smooth Helmholtz kernel over a point cloud (tests/test_hmatrix.py:9-36)."""
+
+    def __init__(self, pts, C=1, k=2 * np.pi, diag=2.0):
+        self.pts, self.C, self.k, self.diag = pts, C, k, diag
+        self.N = pts.shape[0] * C
+
+    def block(self, rows, cols):
+        rows, cols = np.asarray(rows), np.asarray(cols)
+        pi, ci = np.divmod(rows, self.C)
+        pj, cj = np.divmod(cols, self.C)
+        R = np.linalg.norm(self.pts[pi][:, None] - self.pts[pj][None, :], axis=-1)
+        same = ci[:, None] == cj[None, :]
+        scale = np.where(same, 1.0, 0.3)
+        with np.errstate(divide="ignore", invalid="ignore"):
+            v = scale * np.exp(-1j * self.k * R) / (4 * np.pi * R)
+        return np.where(R < 1e-12, np.where(same, self.diag, 0.3), v).astype(complex)
+
+
+class IdGen:
+    def block(self, rows, cols):
+        return (np.asarray(rows)[:, None] == np.asarray(cols)[None, :]).astype(complex)
+
+
+class ZeroGen:
+    def block(self, rows, cols):
+        return np.zeros((len(rows), len(cols)), complex)
+
+
+def sphere_cloud():
+    th = np.linspace(0.2, np.pi - 0.2, 10)
+    ph = np.linspace(0, 2 * np.pi, 20, endpoint=False)
+    T, P = np.meshgrid(th, ph, indexing="ij")
+    return np.stack([np.sin(T) * np.cos(P), np.sin(T) * np.sin(P), np.cos(T)], axis=-1).reshape(-1, 3)
+
+
+def _hm():
+    from paper_2408_17116_b200 import hmatrix as hm
+    return hm
+
+
+def test_hlu_two_by_two_dense_matches_lapack():
+    hm = _hm()
+    rng = np.random.default_rng(2024)
+    pts = np.array([[0.0, 0, 0], [0.1, 0, 0], [3.0, 0, 0], [3.1, 0, 0]])
+    gen = KernelGen(pts, C=1, diag=3.0)
+    H = hm.HMatrix.from_generator(pts, 1, 2, 1e-9, gen, 1e-12)
+    A = gen.block(np.arange(4), np.arange(4))
+    lu = hm.hlu_factor(H, 1e-12)
+    b = rng.standard_normal(4) + 1j * rng.standard_normal(4)
+    x = lu.solve(b)
+    assert np.abs(x - np.linalg.solve(A, b)).max() < 1e-12 * np.abs(x).max()
+
+
+def test_hlu_identity():
+    hm = _hm()
+    pts = np.random.default_rng(1).standard_normal((30, 3))
+    H = hm.HMatrix.from_generator(pts, 1, 8, 2.0, IdGen(), 1e-10)
+    lu = hm.hlu_factor(H, 1e-10)
+    b = np.arange(30, dtype=complex)
+    assert np.abs(lu.solve(b) - b).max() < 1e-12
+
+
+@pytest.fixture(scope="module")
+def synth():
+    hm = _hm()
+    pts = sphere_cloud()
+    gen = KernelGen(pts, C=2)
+    H = hm.HMatrix.from_generator(pts, 2, 32, 2.0, gen, 1e-6)
+    A = gen.block(np.arange(gen.N), np.arange(gen.N))
+    return gen, H, A
+
+
+def test_matvec_within_tolerance(synth):
+    gen, H, A = synth
+    rng = np.random.default_rng(5)
+    x = rng.standard_normal(gen.N) + 1j * rng.standard_normal(gen.N)
+    assert np.linalg.norm(H.matvec(x) - A @ x) <= 10 * 1e-6 * np.linalg.norm(A @ x)
+    assert 0.0 < H.compression_rate() < 1.0
+
+
+def test_hlu_solve_residual_and_multi_rhs(synth):
+    hm = _hm()
+    gen, H, A = synth
+    rng = np.random.default_rng(2024)
+    lu = hm.hlu_factor(H, 1e-6)
+    b = rng.standard_normal(gen.N) + 1j * rng.standard_normal(gen.N)
+    x = lu.solve(b)
+    assert np.linalg.norm(A @ x - b) / np.linalg.norm(b) <= 100 * 1e-6
+    X = lu.solve(np.stack([b, -2j * b], axis=1))
+    assert np.allclose(X[:, 0], x)
+    assert np.allclose(X[:, 1], lu.solve(-2j * b))
+
+
+def test_hlu_zero_rhs(synth):
+    hm = _hm()
+    gen, H, A = synth
+    lu = hm.hlu_factor(H, 1e-6)
+    assert np.abs(lu.solve(np.zeros(gen.N, dtype=complex))).max() == 0.0
+
+
+def test_hlu_singular_diagonal():
+    hm = _hm()
+    from paper_2408_17116_b200.errors import SingularDiagonal
+    pts = np.random.default_rng(3).standard_normal((12, 3))
+    H = hm.HMatrix.from_generator(pts, 1, 4, 2.0, ZeroGen(), 1e-8)
+    with pytest.raises(SingularDiagonal):
+        hm.hlu_factor(H, 1e-8)
