@@ -148,6 +148,12 @@ int cbie_dense_solve(cbie_ctx* ctx, int64_t cap, const cbie_c128* b, int nrhs, c
 int cbie_shard_layout_host(int nleaf, const int* m, const int* n, const uint8_t* adm, const int* owner,
                            const int* info, int world, int64_t* leaf_off, int64_t* ranges, int64_t* total);
 
+/* Move the H-matrix leaf data to pinned host memory mapped into the device address
+ * space; the handle stays usable (factor / matvec read it over the host link) and its
+ * device memory is released -- for problems whose H-matrix and factors do not fit HBM
+ * together (config 5). */
+int cbie_hmatrix_offload(cbie_hmat* h);
+
 int cbie_hmatrix_layout(const double* pts, int64_t npts, int C, int n_leaf, double eta, int64_t* dof_perm,
                         int64_t* leaves, int64_t* nleaf);
 int cbie_hmatrix_import(cbie_ctx* ctx, const double* pts, int64_t npts, int C, int n_leaf, double eta, double tol,

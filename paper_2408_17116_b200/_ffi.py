@@ -46,6 +46,7 @@ _SIGS = {
     "cbie_dense_solve": (ct.c_int, [P, ct.c_int64, P, ct.c_int, P, ct.POINTER(ct.c_double), P, P]),
     "cbie_hmatrix_build": (ct.c_int, [P, ct.c_int, ct.c_double, ct.c_double, ct.POINTER(P)]),
     "cbie_hmatrix_destroy": (None, [P]),
+    "cbie_hmatrix_offload": (ct.c_int, [P]),
     "cbie_hmatrix_layout": (ct.c_int, [P, ct.c_int64, ct.c_int, ct.c_int, ct.c_double, P, P, I64P]),
     "cbie_hmatrix_import": (ct.c_int, [P, P, ct.c_int64, ct.c_int, ct.c_int, ct.c_double, ct.c_double, P,
                                        ct.POINTER(P)]),

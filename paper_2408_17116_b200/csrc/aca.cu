@@ -708,6 +708,30 @@ int cbie_hmatrix_build(cbie_ctx* c, int n_leaf, double eta, double aca_tol, cbie
 
 void cbie_hmatrix_destroy(cbie_hmat* h) { delete h; }
 
+// leaf data to pinned host memory, mapped into the device address space (see cbie_hmat::pinned)
+int cbie_hmatrix_offload(cbie_hmat* h) {
+  try {
+    cudaSetDevice(h->ctx->device);
+    if (h->pinned) return CBIE_OK;
+    const size_t n = h->arena.n;
+    zc* host = nullptr;
+    CK(cudaHostAlloc(reinterpret_cast<void**>(&host), sizeof(zc) * std::max<size_t>(n, 1), cudaHostAllocMapped));
+    CK(cudaMemcpy(host, h->arena.p, sizeof(zc) * n, cudaMemcpyDeviceToHost));
+    zc* dev = nullptr;
+    CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&dev), host, 0));
+    h->arena.release();
+    h->arena.p = dev;
+    h->arena.n = n;
+    h->arena.borrowed = true;
+    h->pinned = host;
+    h->stat["offloaded_bytes"] = (double)n * sizeof(zc);
+  } catch (const cbie_error& e) {
+    h->ctx->err = e.what();
+    return e.code;
+  }
+  return CBIE_OK;
+}
+
 int cbie_hmatrix_tree(cbie_hmat* h, int64_t* dof_perm, int64_t* leaves, int64_t* nleaf) {
   const Tree& T = h->tree;
   if (nleaf) *nleaf = (int64_t)T.leaves.size();

@@ -166,15 +166,17 @@ template <class T>
 struct DBuf {
   T* p = nullptr;
   size_t n = 0;
+  bool borrowed = false;   // p is not ours (mapped host memory, cbie_hmatrix_offload): never freed here
   DBuf() = default;
   DBuf(const DBuf&) = delete;
   DBuf& operator=(const DBuf&) = delete;
   ~DBuf() { release(); }
   void release() {
-    if (p) {
+    if (p && !borrowed) {
       cbie_free(p);
       ++g_cbie_frees;
     }
+    borrowed = false;
     p = nullptr;
     n = 0;
   }
@@ -182,6 +184,8 @@ struct DBuf {
     if (count == n && p) return;
     release();
     if (count == 0) return;
+    if (count * sizeof(T) >= ((size_t)1 << 28) && getenv("CBIE_MEMLOG"))   // debug: large allocations
+      fprintf(stderr, "[cbie] alloc %zu MiB (free %zu MiB)\n", (count * sizeof(T)) >> 20, mem_free_bytes() >> 20);
     cudaError_t e = cbie_malloc(reinterpret_cast<void**>(&p), count * sizeof(T));
     if (e != cudaSuccess) {
       p = nullptr;

@@ -238,10 +238,16 @@ __global__ void __launch_bounds__(GF_NT) k_getrf_blk(zc* __restrict__ ar, int* _
         continue;
       }
       const zc rinv = zdiv(zmk(1.0, 0.0), ajj);
-      for (int i = col + 1 + tid; i < n; i += GF_NT) {
-        const zc l = zmul(P[c * n + i], rinv);
-        P[c * n + i] = l;
-        for (int cc = c + 1; cc < jb; ++cc) P[cc * n + i] = zsub(P[cc * n + i], zmul(l, P[cc * n + col]));
+      for (int i = col + 1 + tid; i < n; i += GF_NT) P[c * n + i] = zmul(P[c * n + i], rinv);
+      __syncthreads();
+      // rank-1 update of the panel's remaining columns: one (row, column) item per thread
+      // (independent read-modify-writes instead of a per-row chain over the columns)
+      {
+        const int rows = n - col - 1, cols = jb - c - 1;
+        for (int e = tid; e < rows * cols; e += GF_NT) {
+          const int i = col + 1 + e % rows, cc = c + 1 + e / rows;
+          P[cc * n + i] = zsub(P[cc * n + i], zmul(P[c * n + i], P[cc * n + col]));
+        }
       }
       __syncthreads();
     }

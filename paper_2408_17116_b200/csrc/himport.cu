@@ -123,7 +123,7 @@ int cbie_hmatrix_import(cbie_ctx* c, const double* pts, int64_t npts, int C, int
       ovf.alloc(1);
       CK(cudaMemsetAsync(ovf.p, 0, 8, s));
       TruncWork work;
-      launch_truncate(scratch.p, H->rank.p, dtd.p, (int)td.size(), kc, tol, ovf.p, work, s, kc, mn,
+      launch_truncate(scratch.p, H->rank.p, dtd.p, (int)td.size(), std::max(kc, mn), tol, ovf.p, work, s, kc, mn,
                       staging.p, 0);
       CK(cudaStreamSynchronize(s));
       CK(cudaMemcpy(rk.data(), H->rank.p, sizeof(int) * nleaf, cudaMemcpyDeviceToHost));
@@ -140,7 +140,7 @@ int cbie_hmatrix_import(cbie_ctx* c, const double* pts, int64_t npts, int C, int
         T.nodes[L.node].kind = BLK_DENSE;
         L.cap = 0;
         L.off_d = used;
-        from_scratch.push_back(CopySeg{t.in_u, used, (int64_t)L.m * L.n});
+        from_scratch.push_back(CopySeg{t.in_u, used, (int64_t)L.m * L.n});   // src: offset in ha
         used += (int64_t)L.m * L.n;
         rk[t.out_slot] = 0;
         ++demoted;
@@ -162,7 +162,9 @@ int cbie_hmatrix_import(cbie_ctx* c, const double* pts, int64_t npts, int C, int
     }
     H->arena.alloc((size_t)std::max<int64_t>(used, 1));
     if (d_used) CK(cudaMemcpyAsync(H->arena.p, hd.data(), sizeof(zc) * d_used, cudaMemcpyHostToDevice, s));
-    if (!from_scratch.empty()) launch_copy_segments(from_scratch, scratch.p, H->arena.p, s);
+    // demoted leaves from the host copy (the recompression used its inputs as workspace)
+    for (const auto& g : from_scratch)
+      CK(cudaMemcpyAsync(H->arena.p + g.dst, ha.data() + g.src, sizeof(zc) * g.count, cudaMemcpyHostToDevice, s));
     if (!from_staging.empty()) launch_copy_segments(from_staging, staging.p, H->arena.p, s);
     CK(cudaMemcpyAsync(H->rank.p, rk.data(), sizeof(int) * nleaf, cudaMemcpyHostToDevice, s));
     H->d_pperm.upload(T.pperm, s);

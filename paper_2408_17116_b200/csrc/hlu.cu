@@ -515,6 +515,7 @@ struct cbie_hlu {
   int64_t npiv = 0;
   int nslot_leaf = 0;
   int cap_boost = 1;               // factor leaf capacity multiplier (raised on truncation overflow)
+  bool lean = false;               // lean capacity rule (factor storage would crowd out the temporaries)
   // Factor storage: the work buffer of the plan cache that computed them (no copy of the
   // factors after the factorisation; `alias` = that cache) until the cache is needed by
   // another factorisation or released -- then they move to `arena` (copy-on-reuse).
@@ -1767,6 +1768,22 @@ static int64_t hlu_layout(cbie_hlu* F, std::vector<CopySeg>& segs) {
   // factor storage: the H-matrix keeps exact ranks; the factors get room to grow
   // (cap = min(budget, 2 r + 48); truncations clipped at cap are counted)
   int64_t leaf_end = 0;
+  // capacity rule: 2 r + 48 (room for the fill-in of the updates); when the factor storage
+  // would not leave room for the H-LU temporaries (config 5: 177 GB), the lean rule
+  // r + max(16, r / 2) -- a clipped truncation re-factors with larger capacities
+  int64_t wide = 0;
+  for (int li = 0; li < nleaf; ++li) {
+    const auto& L = T.leaves[li];
+    const int r = H->h_rank[li];
+    wide += L.kind == BLK_DENSE ? (int64_t)L.m * L.n
+                                : (int64_t)(L.m + L.n) * std::min(std::max(1, std::min(L.m, L.n) / 2), 2 * r + 48);
+  }
+  {
+    size_t tot = 0;
+    const size_t fr = mem_free_bytes(&tot);
+    F->lean = getenv("CBIE_LEAN_CAP") != nullptr || (double)wide * sizeof(zc) > 0.5 * (double)fr;
+  }
+  F->stat["lean_capacity"] = F->lean ? 1 : 0;
   for (int li = 0; li < nleaf; ++li) {
     auto& L = T.leaves[li];
     const auto& L0 = H->tree.leaves[li];
@@ -1776,7 +1793,8 @@ static int64_t hlu_layout(cbie_hlu* F, std::vector<CopySeg>& segs) {
       segs.push_back(CopySeg{L0.off_d, L.off_d, (int64_t)L.m * L.n});
     } else {
       const int r = H->h_rank[li];
-      L.cap = std::max(1, std::min(std::max(1, std::min(L.m, L.n) / 2), F->cap_boost * (2 * r + 48)));
+      const int want = F->lean ? r + F->cap_boost * std::max(16, r / 2) : F->cap_boost * (2 * r + 48);
+      L.cap = std::max(1, std::min(std::max(1, std::min(L.m, L.n) / 2), want));
       L.off_u = leaf_end;
       leaf_end += (int64_t)L.m * L.cap;
       L.off_v = leaf_end;
@@ -1805,7 +1823,10 @@ static int64_t hlu_layout(cbie_hlu* F, std::vector<CopySeg>& segs) {
 static int64_t hlu_pool_budget(int64_t leaf_end, int share) {
   size_t fr = 0, tot = 0;
   fr = mem_free_bytes(&tot);
-  double gb = 0.6 * ((double)fr / share - 1.0 * (double)leaf_end * sizeof(zc)) / (double)(1ll << 30) - 4.0;
+  // keep room for the recompression workspaces, descriptors and the cluster launches'
+  // scratch (up to ~24 GB on the largest configurations)
+  const double reserve = std::max(8.0, std::min(24.0, 0.15 * (double)fr / (double)(1ll << 30))) * (double)(1ll << 30);
+  double gb = 0.6 * ((double)fr / share - 1.0 * (double)leaf_end * sizeof(zc) - reserve) / (double)(1ll << 30) - 4.0;
   gb = std::max(4.0, std::min(gb, 120.0));
   if (getenv("CBIE_POOL_GB")) gb = atof(getenv("CBIE_POOL_GB"));
   return (int64_t)(gb * (double)(1ll << 30)) / (int64_t)sizeof(zc);
@@ -1874,6 +1895,11 @@ static void hlu_factor_impl(cbie_hlu* F) {
   }
   Plan& PL = g_plan_cache->plan;
   Recorder& R = PL.R;
+  if (getenv("CBIE_MEMLOG"))
+    fprintf(stderr, "[cbie] H-LU: tasks %zu, leaf storage %lld MiB, pool budget %lld MiB, pool top %lld MiB, free %zu MiB\n",
+            R.tasks.size(), (long long)(leaf_end * (int64_t)sizeof(zc) >> 20),
+            (long long)(R.pool_budget * (int64_t)sizeof(zc) >> 20), (long long)(R.pool_top * (int64_t)sizeof(zc) >> 20),
+            mem_free_bytes() >> 20);
   F->stat["pool_budget_gb"] = (double)R.pool_budget * sizeof(zc) / (double)(1ll << 30);
   auto t1 = std::chrono::steady_clock::now();
   F->stat["record_ms"] = std::chrono::duration<double, std::milli>(t1 - t0).count();

@@ -69,6 +69,14 @@ struct cbie_hmat {
   bool partial = false;        // true until the shards were exchanged
   bool owns(int li) const { return owner.empty() || owner[li] == shard_rank; }
   std::shared_ptr<void> mv_plan;   // cached H-matvec gather plan (aca.cu hmat_apply)
+  // cbie_hmatrix_offload: the leaf data moved to pinned host memory, mapped into the device
+  // address space (arena.p is its device alias, arena.borrowed): kernels read it over the
+  // host link, the device memory is free for the H-LU of problems too large for both
+  zc* pinned = nullptr;
+  ~cbie_hmat() {
+    arena.release();
+    if (pinned) cudaFreeHost(pinned);
+  }
 };
 
 // shard.cu: LPT partition of the leaves over `world` processes by estimated fill cost

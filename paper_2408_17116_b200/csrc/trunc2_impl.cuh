@@ -953,86 +953,107 @@ __device__ void apply_sel(const zc* __restrict__ X, int mo, int ldx, int i_lo, i
 // Jacobi with the round-robin parallel ordering; X (ld n, shared) enters as I.  The
 // rotation of pair (p, q) is the one of jacobi_nw for the 2 x 2 Gram [h_pp h_pq; . h_qq].
 // Returns the number of sweeps.
+__device__ int g_jacobi_threads = NT;   // threads of the Jacobi sweeps (CBIE_JACOBI_T, launch_gram)
+__device__ int g_gram_onesided = 0;     // 1: one-sided Jacobi on R^H (CBIE_ONESIDED_JACOBI, launch_gram)
+
 __device__ int herm_jacobi(zc* H, int n, zc* X, Smem& S) {
+  // the first JT threads run the sweeps (named barrier 3); the others wait at the end
+  const int JT = g_jacobi_threads;
   __shared__ double rc[KG / 2 + 1];
   __shared__ zc rs[KG / 2 + 1];
   __shared__ int rp[KG / 2 + 1], rq[KG / 2 + 1];
+  __shared__ double red[NW];
+  __shared__ int nsw;
   if (n < 2) return 0;
-  const int ne = n + (n & 1), np = ne / 2;
-  double f2 = 0.0;
-  for (int e = threadIdx.x; e < n * n; e += NT) f2 += zabs2(H[e]);
-  f2 = bsum(f2, S.red);
-  int sweep = 0;
-  for (; sweep < 30; ++sweep) {
-    double off = 0.0;
-    for (int e = threadIdx.x; e < n * n; e += NT)
-      if (e % n != e / n) off += zabs2(H[e]);
-    off = bsum(off, S.red);
-    if (!(off > 1e-20 * f2)) break;
-    for (int rd = 0; rd < ne - 1; ++rd) {
-      // rotation of every pair (round-robin ordering); an index >= n pairs with identity
-      if (threadIdx.x < np) {
-        const int t = threadIdx.x;
-        const int pb = ne - 1 - t;
-        const int p = t == 0 ? 0 : ((t - 1 + rd) % (ne - 1)) + 1;
-        const int q = pb == 0 ? 0 : ((pb - 1 + rd) % (ne - 1)) + 1;
-        double cs = 1.0;
-        zc se = zmk(0.0, 0.0);
-        if (p < n && q < n) {
-          const double al = H[p * n + p].x, be = H[q * n + q].x;
-          const zc gm = H[q * n + p];   // h_pq
-          const double g = sqrt(zabs2(gm));
-          if (g > 1e-300 && g > 1e-17 * sqrt(fabs(al * be))) {
-            const double zeta = (be - al) / (2.0 * g);
-            const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-            cs = 1.0 / sqrt(1.0 + tt * tt);
-            const double sn = cs * tt, ig = 1.0 / g;
-            se = zmk(gm.x * ig * sn, gm.y * ig * sn);
+  if (threadIdx.x < JT) {
+    const int tid = threadIdx.x, lane = tid & 31, wj = tid >> 5;
+    auto jsum = [&](double v) {
+      v = warp_sum(v);
+      gbar(3, JT);
+      if (lane == 0) red[wj] = v;
+      gbar(3, JT);
+      double t = 0.0;
+      for (int i = 0; i < JT / 32; ++i) t += red[i];
+      return t;
+    };
+    const int ne = n + (n & 1), np = ne / 2;
+    double f2 = 0.0;
+    for (int e = tid; e < n * n; e += JT) f2 += zabs2(H[e]);
+    f2 = jsum(f2);
+    int sweep = 0;
+    for (; sweep < 30; ++sweep) {
+      double off = 0.0;
+      for (int e = tid; e < n * n; e += JT)
+        if (e % n != e / n) off += zabs2(H[e]);
+      off = jsum(off);
+      if (!(off > 1e-20 * f2)) break;
+      for (int rd = 0; rd < ne - 1; ++rd) {
+        // rotation of every pair (round-robin ordering); an index >= n pairs with identity
+        if (tid < np) {
+          const int t = tid;
+          const int pb = ne - 1 - t;
+          const int p = t == 0 ? 0 : ((t - 1 + rd) % (ne - 1)) + 1;
+          const int q = pb == 0 ? 0 : ((pb - 1 + rd) % (ne - 1)) + 1;
+          double cs = 1.0;
+          zc se = zmk(0.0, 0.0);
+          if (p < n && q < n) {
+            const double al = H[p * n + p].x, be = H[q * n + q].x;
+            const zc gm = H[q * n + p];   // h_pq
+            const double g = sqrt(zabs2(gm));
+            if (g > 1e-300 && g > 1e-17 * sqrt(fabs(al * be))) {
+              const double zeta = (be - al) / (2.0 * g);
+              const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+              cs = 1.0 / sqrt(1.0 + tt * tt);
+              const double sn = cs * tt, ig = 1.0 / g;
+              se = zmk(gm.x * ig * sn, gm.y * ig * sn);
+            }
+          }
+          rp[t] = p;
+          rq[t] = q;
+          rc[t] = cs;
+          rs[t] = se;
+        }
+        gbar(3, JT);
+        // H <- J^H H J by disjoint 2 x 2 blocks (rows of pair t1, columns of pair t2),
+        // X <- X J by (row, pair) items; no two items touch the same entry.
+        // J = [cs se; -conj(se) cs] acts on the (p, q) columns.
+        for (int e = tid; e < np * np + n * np; e += JT) {
+          if (e < np * np) {
+            const int t1 = e % np, t2 = e / np;
+            const int a0 = rp[t1], a1 = rq[t1], b0 = rp[t2], b1 = rq[t2];
+            const bool va0 = a0 < n, va1 = a1 < n, vb0 = b0 < n, vb1 = b1 < n;
+            const double c1 = rc[t1], c2 = rc[t2];
+            const zc s1 = rs[t1], s2 = rs[t2];
+            const zc z0 = zmk(0.0, 0.0);
+            const zc hpp = va0 && vb0 ? H[b0 * n + a0] : z0, hpq = va0 && vb1 ? H[b1 * n + a0] : z0;
+            const zc hqp = va1 && vb0 ? H[b0 * n + a1] : z0, hqq = va1 && vb1 ? H[b1 * n + a1] : z0;
+            const zc cpp = zsub(zscale(hpp, c2), zmul(zconj(s2), hpq));
+            const zc cpq = zadd(zmul(s2, hpp), zscale(hpq, c2));
+            const zc cqp = zsub(zscale(hqp, c2), zmul(zconj(s2), hqq));
+            const zc cqq = zadd(zmul(s2, hqp), zscale(hqq, c2));
+            if (va0 && vb0) H[b0 * n + a0] = zsub(zscale(cpp, c1), zmul(s1, cqp));
+            if (va0 && vb1) H[b1 * n + a0] = zsub(zscale(cpq, c1), zmul(s1, cqq));
+            if (va1 && vb0) H[b0 * n + a1] = zadd(zmul(zconj(s1), cpp), zscale(cqp, c1));
+            if (va1 && vb1) H[b1 * n + a1] = zadd(zmul(zconj(s1), cpq), zscale(cqq, c1));
+          } else {
+            const int f = e - np * np;
+            const int i = f % n, t = f / n;
+            const int p = rp[t], q = rq[t];
+            if (p >= n || q >= n) continue;
+            const double cs = rc[t];
+            const zc se = rs[t];
+            const zc xi = X[p * n + i], yi = X[q * n + i];
+            X[p * n + i] = zsub(zscale(xi, cs), zmul(zconj(se), yi));
+            X[q * n + i] = zadd(zmul(se, xi), zscale(yi, cs));
           }
         }
-        rp[t] = p;
-        rq[t] = q;
-        rc[t] = cs;
-        rs[t] = se;
+        gbar(3, JT);
       }
-      __syncthreads();
-      // H <- J^H H J by disjoint 2 x 2 blocks (rows of pair t1, columns of pair t2),
-      // X <- X J by (row, pair) items; no two items touch the same entry.
-      // J = [cs se; -conj(se) cs] acts on the (p, q) columns.
-      for (int e = threadIdx.x; e < np * np + n * np; e += NT) {
-        if (e < np * np) {
-          const int t1 = e % np, t2 = e / np;
-          const int a0 = rp[t1], a1 = rq[t1], b0 = rp[t2], b1 = rq[t2];
-          const bool va0 = a0 < n, va1 = a1 < n, vb0 = b0 < n, vb1 = b1 < n;
-          const double c1 = rc[t1], c2 = rc[t2];
-          const zc s1 = rs[t1], s2 = rs[t2];
-          const zc z0 = zmk(0.0, 0.0);
-          const zc hpp = va0 && vb0 ? H[b0 * n + a0] : z0, hpq = va0 && vb1 ? H[b1 * n + a0] : z0;
-          const zc hqp = va1 && vb0 ? H[b0 * n + a1] : z0, hqq = va1 && vb1 ? H[b1 * n + a1] : z0;
-          const zc cpp = zsub(zscale(hpp, c2), zmul(zconj(s2), hpq));
-          const zc cpq = zadd(zmul(s2, hpp), zscale(hpq, c2));
-          const zc cqp = zsub(zscale(hqp, c2), zmul(zconj(s2), hqq));
-          const zc cqq = zadd(zmul(s2, hqp), zscale(hqq, c2));
-          if (va0 && vb0) H[b0 * n + a0] = zsub(zscale(cpp, c1), zmul(s1, cqp));
-          if (va0 && vb1) H[b1 * n + a0] = zsub(zscale(cpq, c1), zmul(s1, cqq));
-          if (va1 && vb0) H[b0 * n + a1] = zadd(zmul(zconj(s1), cpp), zscale(cqp, c1));
-          if (va1 && vb1) H[b1 * n + a1] = zadd(zmul(zconj(s1), cpq), zscale(cqq, c1));
-        } else {
-          const int f = e - np * np;
-          const int i = f % n, t = f / n;
-          const int p = rp[t], q = rq[t];
-          if (p >= n || q >= n) continue;
-          const double cs = rc[t];
-          const zc se = rs[t];
-          const zc xi = X[p * n + i], yi = X[q * n + i];
-          X[p * n + i] = zsub(zscale(xi, cs), zmul(zconj(se), yi));
-          X[q * n + i] = zadd(zmul(se, xi), zscale(yi, cs));
-        }
-      }
-      __syncthreads();
     }
+    if (tid == 0) nsw = sweep;
   }
-  return sweep;
+  __syncthreads();
+  return nsw;
 }
 
 // Cluster execution (k_trunc_gram launched with clusters of csize CTAs per problem):
@@ -1163,21 +1184,45 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   stamp(6);
   const int kp = pchol_grp(H, kk1, S.perm, (GDELTA * tol) * (GDELTA * tol), true, NW, threadIdx.x >> 5, 1, X2, scu);
   stamp(7);
-  zc* Gp = Gv;   // R R^H (kp x kp)
-  zc* Z = X2;    // eigenvectors (kp x kp)
-  for (int e = threadIdx.x; e < kp * kp; e += NT) {
-    const int a = e % kp, b = e / kp;
-    zc s = zmk(0.0, 0.0);
-    for (int j = max(a, b); j < kk1; ++j) zfma(s, H[j * kk1 + a], zconj(H[j * kk1 + b]));
-    Gp[b * kp + a] = s;
-    Z[b * kp + a] = zmk(a == b ? 1.0 : 0.0, 0.0);
+  int sweeps = 0;
+  if (g_gram_onesided) {
+    // one-sided Jacobi on B = R^H (kk1 x kp, X2's region): rotating column pairs until
+    // they are orthogonal gives B Z = R^H Z = (left singular vectors) x Sigma directly --
+    // no R R^H product, no eigenvector accumulation, one barrier per round (jacobi_nw,
+    // half-warp per pair)
+    zc* B = X2;
+    for (int e = threadIdx.x; e < kk1 * kp; e += NT) {
+      const int a = e % kk1, c = e / kk1;
+      B[e] = a >= c ? zconj(H[a * kk1 + c]) : zmk(0.0, 0.0);   // conj(R(c, a))
+    }
+    __syncthreads();
+    stamp(8);
+    tc[2] = clock64();
+    sweeps = jacobi_nw(B, kk1, kp, kk1, S);
+    for (int c = threadIdx.x >> 5; c < kp; c += NW) {   // warp per column norm
+      double ns = 0.0;
+      for (int q = threadIdx.x & 31; q < kk1; q += 32) ns += zabs2(B[c * kk1 + q]);
+      ns = warp_sum(ns);
+      if ((threadIdx.x & 31) == 0) S.sig[c] = sqrt(ns);
+    }
+    __syncthreads();
+  } else {
+    zc* Gp = Gv;   // R R^H (kp x kp)
+    zc* Z = X2;    // eigenvectors (kp x kp)
+    for (int e = threadIdx.x; e < kp * kp; e += NT) {
+      const int a = e % kp, b = e / kp;
+      zc s = zmk(0.0, 0.0);
+      for (int j = max(a, b); j < kk1; ++j) zfma(s, H[j * kk1 + a], zconj(H[j * kk1 + b]));
+      Gp[b * kp + a] = s;
+      Z[b * kp + a] = zmk(a == b ? 1.0 : 0.0, 0.0);
+    }
+    __syncthreads();
+    stamp(8);
+    tc[2] = clock64();
+    sweeps = herm_jacobi(Gp, kp, Z, S);
+    for (int c = threadIdx.x; c < kp; c += NT) S.sig[c] = sqrt(fmax(Gp[c * kp + c].x, 0.0));
+    __syncthreads();
   }
-  __syncthreads();
-  stamp(8);
-  tc[2] = clock64();
-  const int sweeps = herm_jacobi(Gp, kp, Z, S);
-  for (int c = threadIdx.x; c < kp; c += NT) S.sig[c] = sqrt(fmax(Gp[c * kp + c].x, 0.0));
-  __syncthreads();
   for (int c = threadIdx.x; c < kp; c += NT) {
     int pos = 0;
     for (int o = 0; o < kp; ++o)
@@ -1200,12 +1245,20 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   // W = P R^H Z_r (kk1 x r) in Gv's region (G dead: S.sig holds its diagonal)
   __syncthreads();
   zc* W = Gv;
-  for (int e = threadIdx.x; e < kk1 * r; e += NT) {
-    const int j = e % kk1, l = e / kk1;
-    const int c = S.order[l];
-    zc s = zmk(0.0, 0.0);
-    for (int a = 0; a <= min(j, kp - 1); ++a) zfma(s, zconj(H[j * kk1 + a]), Z[c * kp + a]);
-    W[(int64_t)l * kk1 + S.perm[j]] = s;
+  if (g_gram_onesided) {
+    for (int e = threadIdx.x; e < kk1 * r; e += NT) {
+      const int j = e % kk1, l = e / kk1;
+      W[(int64_t)l * kk1 + S.perm[j]] = X2[S.order[l] * kk1 + j];
+    }
+  } else {
+    const zc* Z = X2;
+    for (int e = threadIdx.x; e < kk1 * r; e += NT) {
+      const int j = e % kk1, l = e / kk1;
+      const int c = S.order[l];
+      zc s = zmk(0.0, 0.0);
+      for (int a = 0; a <= min(j, kp - 1); ++a) zfma(s, zconj(H[j * kk1 + a]), Z[c * kp + a]);
+      W[(int64_t)l * kk1 + S.perm[j]] = s;
+    }
   }
   __syncthreads();
   // conj(Vhat) = conj(M^H W / S^2) (kk2 x r) to global
@@ -1358,6 +1411,14 @@ void launch_gram(zc* arena, zc* aout, int* ranks, const TruncDesc* d_desc, int n
   if (scratch.n < need) scratch.alloc(need);
   const int smem = (3 * GSQ + KG + 1) * (int)sizeof(zc);
   CK(cudaFuncSetAttribute(k_trunc_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  if (getenv("CBIE_ONESIDED_JACOBI")) {   // experiment knob (slower on configs 2 and 4: 4.7 sweeps)
+    const int z = 1;
+    CK(cudaMemcpyToSymbol(g_gram_onesided, &z, sizeof(int)));
+  }
+  if (getenv("CBIE_JACOBI_T")) {   // experiment knob: threads of the two-sided sweeps
+    const int jt = std::max(32, std::min(NT, atoi(getenv("CBIE_JACOBI_T")) / 32 * 32));
+    CK(cudaMemcpyToSymbol(g_jacobi_threads, &jt, sizeof(int)));
+  }
   for (int b0 = 0; b0 < nd; b0 += wave) {
     const int nb = std::min(wave, nd - b0);
     cudaLaunchConfig_t cfg = {};

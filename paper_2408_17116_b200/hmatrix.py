@@ -85,6 +85,13 @@ class HMatrix:
             self.dev.lib.cbie_hmatrix_destroy(h)
             self.h = None
 
+    def offload(self) -> None:
+        """Move the leaf data to pinned host memory mapped into the device address space
+        (cbie_hmatrix_offload): the H-LU and matvec still read it, over the host link, and
+        the device memory is free for the factorisation of problems too large for both
+        (config 5: 67 GB H-matrix + the factors)."""
+        self.dev.check(self.dev.lib.cbie_hmatrix_offload(self.h))
+
     # -- structure -------------------------------------------------------------------
     def tree(self):
         n = ct.c_int64()

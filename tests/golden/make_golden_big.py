@@ -240,7 +240,31 @@ def mie_currents(cfg, n_patch=None, seed=41):
          pos=np.concatenate(pts), n_terms=spec.n_terms)
 
 
+def thread_sweep(cfg):
+    """The reference's config run under the two other thread settings of BASELINE.md 3
+    (setting 1, workers=1 / BLAS=1, is cfgN_solve): workers=cores with BLAS=1, and
+    workers=1 with BLAS=cores.  Timings only (JSON)."""
+    from threadpoolctl import threadpool_limits
+    cores = os.cpu_count() or 1
+    out = {"cores": cores}
+    for name, workers, blas in (("workers=cores,BLAS=1", cores, 1), ("workers=1,BLAS=cores", 1, cores)):
+        prob = ref_problem(cfg, workers=workers)
+        with threadpool_limits(blas):
+            t0 = time.perf_counter()
+            r = rsolver.solve_direct(prob)
+            wall = time.perf_counter() - t0
+        out[name] = {"fill_s": r.metrics["fill_s"], "factor_s": r.metrics["factor_s"], "wall_s": wall,
+                     "residual": r.residual}
+        print(name, out[name], flush=True)
+    path = os.path.join(HERE, f"cfg{cfg}_thread_sweep.json")
+    json.dump(out, open(path, "w"), indent=1)
+    print("wrote", path)
+
+
 def main(job):
+    if job.endswith("_sweep"):
+        thread_sweep(int(job[3]))
+        return
     if job == "mie":
         mie_currents(2)
         mie_currents(5, n_patch=64)

@@ -18,17 +18,23 @@ hs = H.stats()
 print(json.dumps({"stage": "fill", "wall_s": time.perf_counter() - t0, "N": prob.n_dofs,
                   **{k: hs[k] for k in ("fill_ms", "aca_ms", "arena_bytes", "stored_scalars", "compression_rate",
                                         "n_leaves", "demoted") if k in hs}}), flush=True)
+if os.environ.get("CFG5_OFFLOAD", "1") == "1":
+    t = time.perf_counter()
+    H.offload()          # the 67 GB H-matrix to mapped host memory: HBM for the factors
+    print(json.dumps({"stage": "offload", "wall_s": time.perf_counter() - t}), flush=True)
 t1 = time.perf_counter()
 F = hm.hlu_factor(H, prob.effective_trunc_tol)
 fs = F.stats()
 print(json.dumps({"stage": "hlu", "wall_s": time.perf_counter() - t1,
                   **{k: fs[k] for k in ("factor_device_ms", "record_ms", "tasks", "levels", "launches", "temp_bytes",
-                                        "pool_budget_gb", "trunc_overflow", "flops", "stored_scalars")
+                                        "pool_budget_gb", "trunc_overflow", "flops", "stored_scalars",
+                                        "lean_capacity", "cap_boost", "cap_retries")
                      if k in fs}}), flush=True)
 b = gen.rhs(prob.excitation) * gen.row_scale
 t2 = time.perf_counter()
 x = F.solve(b)
+sol_s = time.perf_counter() - t2
+del F                    # the matvec of the residual reads the H-matrix from host memory
 res = float(np.linalg.norm(H.matvec(x) - b) / np.linalg.norm(b))
-print(json.dumps({"stage": "solve", "wall_s": time.perf_counter() - t2, "residual": res,
-                  "solve_device_ms": F.stats().get("solve_device_ms")}), flush=True)
+print(json.dumps({"stage": "solve", "solve_wall_s": sol_s, "residual": res}), flush=True)
 np.save(os.path.join("gpurun_out", f"cfg{cfg}_x.npy"), x * gen.col_scale)
