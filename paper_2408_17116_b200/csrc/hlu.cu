@@ -1784,6 +1784,7 @@ static int64_t hlu_layout(cbie_hlu* F, std::vector<CopySeg>& segs) {
     F->lean = getenv("CBIE_LEAN_CAP") != nullptr || (double)wide * sizeof(zc) > 0.5 * (double)fr;
   }
   F->stat["lean_capacity"] = F->lean ? 1 : 0;
+  g_ws_tight = F->lean;   // workspaces capped at 1 GiB per launch beside a crowded arena
   for (int li = 0; li < nleaf; ++li) {
     auto& L = T.leaves[li];
     const auto& L0 = H->tree.leaves[li];
@@ -1827,6 +1828,9 @@ static int64_t hlu_pool_budget(int64_t leaf_end, int share) {
   // scratch (up to ~24 GB on the largest configurations)
   const double reserve = std::max(8.0, std::min(24.0, 0.15 * (double)fr / (double)(1ll << 30))) * (double)(1ll << 30);
   double gb = 0.6 * ((double)fr / share - 1.0 * (double)leaf_end * sizeof(zc) - reserve) / (double)(1ll << 30) - 4.0;
+  // tight memory (lean capacities): the size-class pool can overshoot its budget by ~80 %
+  // (config 5: 32 GB budget, 58 GB top), so aim lower
+  if (g_ws_tight) gb *= 0.5;
   gb = std::max(4.0, std::min(gb, 120.0));
   if (getenv("CBIE_POOL_GB")) gb = atof(getenv("CBIE_POOL_GB"));
   return (int64_t)(gb * (double)(1ll << 30)) / (int64_t)sizeof(zc);

@@ -4,6 +4,7 @@
 // Restates hmatrix.py:31-89 (ClusterTree, admissible), 96-204 (block kinds,
 // block tree) with flat arrays so the device kernels can address leaves by index.
 #pragma once
+#include <algorithm>
 #include <memory>
 #include <vector>
 
@@ -144,6 +145,13 @@ void launch_truncate_gram(zc* arena, int* ranks, const TruncDesc* d_desc, int nd
 bool launch_truncate_blocked(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, double tol,
                              unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, int kc_max,
                              int mn_max, zc* arena_out, int* defer, const int* idx = nullptr);
+
+// Per-launch workspace cap of the recompression kernels: `gb` GiB normally, 1 GiB in
+// tight-memory mode (lean factor capacities, hlu.cu), so that the per-lane workspaces fit
+// beside a factor arena that fills most of HBM (config 5).
+extern bool g_ws_tight;
+inline bool ws_tight() { return g_ws_tight; }
+inline size_t ws_cap(int gb) { return (size_t)(g_ws_tight ? std::min(gb, 1) : gb) << 30; }
 
 // contiguous segment copies src[src + i] -> dst[dst + i] (aca.cu)
 struct CopySeg {

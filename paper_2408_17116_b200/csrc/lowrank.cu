@@ -407,7 +407,8 @@ __global__ void __launch_bounds__(LR_NT) k_truncate(zc* arena, zc* aout, int* ra
 
 }  // namespace
 
-unsigned long long* g_trunc_prof = nullptr;   // debug cycle counters (CBIE_PROFILE)
+unsigned long long* g_trunc_prof = nullptr;
+bool g_ws_tight = false;   // debug cycle counters (CBIE_PROFILE)
 
 void trunc_prof_enable(bool on, int onesided) {
   if (on && !g_trunc_prof) {
@@ -426,7 +427,7 @@ static void launch_unblocked_list(zc* arena, zc* arena_out, int* ranks, const Tr
                                   TruncWork& work, cudaStream_t s, const int* list) {
   DBuf<zc>& dscratch = work.dscratch;
   // one CTA per SM (grid-stride over the list) unless the scratch would exceed 4 GB
-  const int64_t cap_mem = std::max<int64_t>(74, ((int64_t)4 << 30) / std::max<int64_t>(per * (int64_t)sizeof(zc), 1));
+  const int64_t cap_mem = std::max<int64_t>(ws_tight() ? 1 : 74, (int64_t)ws_cap(4) / std::max<int64_t>(per * (int64_t)sizeof(zc), 1));
   const int grid = (int)std::min<int64_t>(nd, std::min<int64_t>(148, cap_mem));
   if (dscratch.n < (size_t)grid * per) dscratch.alloc((size_t)grid * per);
   const size_t smem = std::max((size_t)SMEM_J * SMEM_J * 3 * sizeof(zc) + SMEM_J * (sizeof(zc) + sizeof(double)),
@@ -601,7 +602,7 @@ void launch_truncate(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, int
     launch_unblocked_list(arena, arena_out, ranks, d_desc, nd, kmax, per, tol, overflow, work, s, dfr);
     return;
   }
-  const int wave = (int)std::max<int64_t>(1, ((int64_t)1 << 30) / (per * (int64_t)sizeof(zc)));
+  const int wave = (int)std::max<int64_t>(1, (int64_t)ws_cap(1) / (per * (int64_t)sizeof(zc)));
   const size_t need = (size_t)std::min(wave, nd) * per;
   if (scratch.n < need) scratch.alloc(need);
   // exact path: Ms, Bs, Js (3 x 64^2) + rdM/kapM; randomized path: Ms, Ws + GEMM tiles
@@ -865,7 +866,7 @@ void launch_dense_lr(zc* arena, int* ranks, const DenseLRDesc* d_desc, int nd, i
                      int max_cap, DBuf<zc>& scratch, cudaStream_t s) {
   if (nd == 0) return;
   const int64_t per = (int64_t)(max_m + max_n) * max_cap;
-  const int wave = (int)std::max<int64_t>(1, ((int64_t)1 << 30) / (per * (int64_t)sizeof(zc)));
+  const int wave = (int)std::max<int64_t>(1, (int64_t)ws_cap(1) / (per * (int64_t)sizeof(zc)));
   const size_t need = (size_t)std::min(wave, nd) * per;
   if (scratch.n < need) scratch.alloc(need);
   const size_t smem = (size_t)max_cap * (sizeof(zc) + sizeof(double)) + 32 +

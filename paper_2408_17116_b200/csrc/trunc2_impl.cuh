@@ -599,7 +599,7 @@ void launch_rpl(zc* arena, zc* aout, int* ranks, const TruncDesc* d_desc, int nd
                 unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, unsigned long long* prof,
                 int* defer, const int* idx = nullptr) {
   const int64_t per = scratch_per(kc);
-  const int wave = (int)std::max<int64_t>(1, ((int64_t)2 << 30) / (per * (int64_t)sizeof(zc)));
+  const int wave = (int)std::max<int64_t>(1, (int64_t)ws_cap(2) / (per * (int64_t)sizeof(zc)));
   const size_t need = (size_t)std::min(wave, nd) * per;
   if (scratch.n < need) scratch.alloc(need);
   const int smem = ELEMS * (int)sizeof(zc);
@@ -1406,7 +1406,7 @@ void launch_gram(zc* arena, zc* aout, int* ranks, const TruncDesc* d_desc, int n
   csize = std::max(1, std::min(csize, 8));
   // one launch per group whenever 2 GB of scratch allow it (a second launch of the tail
   // would wait for the whole first one on the stream)
-  const int wave = (int)std::max<int64_t>(1, ((int64_t)2 << 30) / (per * csize * (int64_t)sizeof(zc)));
+  const int wave = (int)std::max<int64_t>(1, (int64_t)ws_cap(2) / (per * csize * (int64_t)sizeof(zc)));
   const size_t need = (size_t)std::min(wave, nd) * csize * per;
   if (scratch.n < need) scratch.alloc(need);
   const int smem = (3 * GSQ + KG + 1) * (int)sizeof(zc);
