@@ -43,6 +43,29 @@ __host__ __device__ __forceinline__ void zfma(zc& acc, zc a, zc b) {
   acc.x = fma(a.x, b.x, fma(-a.y, b.y, acc.x));
   acc.y = fma(a.x, b.y, fma(a.y, b.x, acc.y));
 }
+// FP64 tensor-core MMA (DMMA, mma.sync.m8n8k4.f64): D(8x8) += A(8x4) B(4x8) per warp.
+// Fragments: a = A[lane / 4][lane % 4], b = B[lane % 4][lane / 4],
+// (c0, c1) = C[lane / 4][2 (lane % 4) + {0, 1}].  512 flops per instruction (DFMA: 64).
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+// complex 8x8x4 step: C += A B (4 DMMA; c = {Cr0, Cr1, Ci0, Ci1})
+__device__ __forceinline__ void zdmma(double* c, zc a, zc b) {
+  dmma(c[0], c[1], a.x, b.x);
+  dmma(c[0], c[1], -a.y, b.y);
+  dmma(c[2], c[3], a.x, b.y);
+  dmma(c[2], c[3], a.y, b.x);
+}
+// complex 8x8x4 step with the A operand conjugated: C += conj(A) B
+__device__ __forceinline__ void zdmma_ca(double* c, zc a, zc b) {
+  dmma(c[0], c[1], a.x, b.x);
+  dmma(c[0], c[1], a.y, b.y);
+  dmma(c[2], c[3], a.x, b.y);
+  dmma(c[2], c[3], -a.y, b.x);
+}
+
 // Executed FP64 work of the H-LU kernels (SURVEY 8(d) flop convention): every task
 // adds its own algorithmic count once, with the ranks it actually saw on the device.
 // One counter per translation unit (static), read / reset by CBIE_FLOP_API below.

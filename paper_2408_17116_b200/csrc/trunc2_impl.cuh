@@ -725,6 +725,98 @@ __device__ void gram_acc(const zc* __restrict__ X, int r_lo, int r_hi, int k, in
   }
 }
 
+// DMMA form of gram_acc (same contract, but G is WRITTEN, not accumulated): the
+// products run on the FP64 tensor pipe (mma.sync.m8n8k4.f64, 4 DMMA per complex 8x8x4
+// step).  The upper 8 x 8 tiles (a-block <= b-block) are dealt to the warps of a row
+// group, the 4-row steps of each 32-row chunk round-robin to RS row groups.  Chunks are
+// double-buffered in Xs (2 x KG x GSLD shared zc; may overlap G, which is stored after
+// the last staging read) by cp.async, column-major with a stride that makes the fragment
+// loads conflict-free.  Row-group partials are added in group order (deterministic).
+constexpr int GTPW = 9;     // upper tiles per warp (36 tiles of k = 64 over 4 warps)
+constexpr int GMCH = 32;    // rows per staged chunk
+constexpr int GSLD = 36;    // staging column stride (zc)
+__device__ int g_gram_mma = 1;   // 0: DFMA gram_acc / apply_sel (CBIE_NO_DMMA)
+
+__device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gsrc), "r"(valid ? 16 : 0)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
+
+__device__ __noinline__ void gram_acc_mma(const zc* __restrict__ X, int r_lo, int r_hi, int k, int ldx, zc* G,
+                                          zc* Xs) {
+  const int nb = (k + 7) >> 3, nt = nb * (nb + 1) / 2;
+  int RS = min(NW, GMCH / 4);
+  while (RS > 1 && (nt + NW / RS - 1) / (NW / RS) > GTPW) RS >>= 1;
+  const int wpr = NW / RS;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int g = w / wpr, wi = w % wpr;
+  const int fr = lane & 3, fc = lane >> 2;
+  double acc[GTPW][4];
+#pragma unroll
+  for (int q = 0; q < GTPW; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.0;
+  const int nch = (r_hi - r_lo + GMCH - 1) / GMCH;
+  auto issue = [&](int c) {
+    if (c < nch) {
+      const int r0 = r_lo + c * GMCH;
+      zc* buf = Xs + (c & 1) * (KG * GSLD);
+      for (int e = threadIdx.x; e < GMCH * k; e += NT) {
+        const int r = e % GMCH, col = e / GMCH;
+        const bool ok = r0 + r < r_hi;
+        cp_async16(buf + col * GSLD + r, ok ? X + (int64_t)col * ldx + r0 + r : X, ok);
+      }
+    }
+    cp_async_commit();
+  };
+  issue(0);
+  for (int c = 0; c < nch; ++c) {
+    issue(c + 1);
+    cp_async_wait1();
+    __syncthreads();
+    const zc* buf = Xs + (c & 1) * (KG * GSLD);
+    const int nst = (min(GMCH, r_hi - r_lo - c * GMCH) + 3) >> 2;
+    for (int st = g; st < nst; st += RS) {
+      const int row = 4 * st + fr;
+#pragma unroll
+      for (int q = 0; q < GTPW; ++q) {
+        const int t = wi + q * wpr;
+        if (t >= nt) break;   // warp-uniform
+        int b = 0;
+        while ((b + 1) * (b + 2) / 2 <= t) ++b;
+        const int ca = (t - b * (b + 1) / 2) * 8 + fc, cb = b * 8 + fc;
+        const zc xa = ca < k ? buf[ca * GSLD + row] : zmk(0.0, 0.0);
+        const zc xb = cb < k ? buf[cb * GSLD + row] : zmk(0.0, 0.0);
+        zdmma_ca(acc[q], xa, xb);
+      }
+    }
+    __syncthreads();   // buffer c & 1 is refilled by the next iteration's issue
+  }
+  for (int gg = 0; gg < RS; ++gg) {
+    if (g == gg) {
+#pragma unroll
+      for (int q = 0; q < GTPW; ++q) {
+        const int t = wi + q * wpr;
+        if (t >= nt) break;
+        int b = 0;
+        while ((b + 1) * (b + 2) / 2 <= t) ++b;
+        const int ta = t - b * (b + 1) / 2;
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          const int ea = ta * 8 + fc, eb = b * 8 + 2 * fr + j;
+          if (ea >= k || eb >= k || ea > eb) continue;
+          zc& gp = G[eb * k + ea];
+          const zc val = zmk(acc[q][j], acc[q][2 + j]);
+          gp = gg == 0 ? val : zadd(gp, val);
+          if (ea != eb) G[ea * k + eb] = zconj(gp);
+        }
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // pivoted Cholesky of the Hermitian G (k x k, ld k, shared) in place: row j < kk of G
 // holds row j of R (columns in pivoted order, entries >= j); perm[j] = original
 // column of pivot j.  Returns kk: stops when the largest remaining pivot is <= thr_rel *
@@ -949,6 +1041,43 @@ __device__ void apply_sel(const zc* __restrict__ X, int mo, int ldx, int i_lo, i
   }
 }
 
+// DMMA form of apply_sel: a warp per 8-row block of O; the A fragments of the whole
+// inner dimension (kk <= 64: 16 four-column steps) are loaded up front (gathered columns
+// perm[j] of X, 8 consecutive rows per column), then every 8-column block of O is one
+// chain of 4 DMMA per step against T's fragments in shared memory.
+__device__ __noinline__ void apply_sel_mma(const zc* __restrict__ X, int mo, int ldx, int i_lo, int i_hi, const int* perm,
+                              int kk, const zc* T, int r, zc* __restrict__ O) {
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int fr = lane >> 2, fk = lane & 3;
+  const int nrb = (i_hi - i_lo + 7) >> 3, nks = (kk + 3) >> 2, ncb = (r + 7) >> 3;
+  for (int rb = w; rb < nrb; rb += NW) {
+    const int i = i_lo + rb * 8 + fr;
+    zc a[KG / 4];
+#pragma unroll
+    for (int s = 0; s < KG / 4; ++s) {
+      const int j = 4 * s + fk;
+      a[s] = (s < nks && j < kk && i < i_hi) ? X[(int64_t)perm[j] * ldx + i] : zmk(0.0, 0.0);
+    }
+    for (int cb = 0; cb < ncb; ++cb) {
+      double c[4] = {0.0, 0.0, 0.0, 0.0};
+      const int l = cb * 8 + fr;
+#pragma unroll
+      for (int s = 0; s < KG / 4; ++s) {
+        if (s >= nks) break;
+        const int j = 4 * s + fk;
+        const zc b = (j < kk && l < r) ? T[l * kk + j] : zmk(0.0, 0.0);
+        zdmma(c, a[s], b);
+      }
+      const int row = i_lo + rb * 8 + fr;
+#pragma unroll
+      for (int jj = 0; jj < 2; ++jj) {
+        const int col = cb * 8 + 2 * fk + jj;
+        if (col < r && row < i_hi) O[(int64_t)col * mo + row] = zmk(c[jj], c[2 + jj]);
+      }
+    }
+  }
+}
+
 // Hermitian eigenproblem H (n x n, ld n, shared) = X diag(h) X^H by cyclic two-sided
 // Jacobi with the round-robin parallel ordering; X (ld n, shared) enters as I.  The
 // rotation of pair (p, q) is the one of jacobi_nw for the 2 x 2 Gram [h_pp h_pq; . h_qq].
@@ -1105,8 +1234,13 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   // 1. Gram matrices
   for (int e = threadIdx.x; e < 2 * GSQ; e += NT) sm[e] = zmk(0.0, 0.0);
   __syncthreads();
-  gram_acc(U, mu0, mu1, k, ldu, Gu, X2);
-  gram_acc(Vt, nv0, nv1, k, ldv, Gv, X2);
+  if (g_gram_mma) {   // staging in Gv's region (+ X2's head): free until G_v is stored
+    gram_acc_mma(U, mu0, mu1, k, ldu, Gu, Gv);
+    gram_acc_mma(Vt, nv0, nv1, k, ldv, Gv, Gv);
+  } else {
+    gram_acc(U, mu0, mu1, k, ldu, Gu, X2);
+    gram_acc(Vt, nv0, nv1, k, ldv, Gv, X2);
+  }
   cluster_gram_sum(Gu, k, X2);
   cluster_gram_sum(Gv, k, X2);
   // 2. balancing
@@ -1278,7 +1412,10 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   // 6a. U' = U_sel D R_u11^{-1} W
   tri_solve_cols(X2, k, kk1, W, r, scu);
   stamp(10);
-  if (r > 0) apply_sel(U, m, ldu, mu0, mu1, pu, kk1, W, r, Uo);
+  if (r > 0) {
+    if (g_gram_mma) apply_sel_mma(U, m, ldu, mu0, mu1, pu, kk1, W, r, Uo);
+    else apply_sel(U, m, ldu, mu0, mu1, pu, kk1, W, r, Uo);
+  }
   __syncthreads();
   stamp(11);
   // 6b. Vt' = Vt_sel D^{-1} R_v11^{-1} conj(Vhat)
@@ -1287,7 +1424,10 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   for (int e = threadIdx.x; e < kk2 * r; e += NT) W2[e] = Vhg[e];
   __syncthreads();
   tri_solve_cols(X2, k, kk2, W2, r, scv);
-  if (r > 0) apply_sel(Vt, n, ldv, nv0, nv1, pv, kk2, W2, r, Vo);
+  if (r > 0) {
+    if (g_gram_mma) apply_sel_mma(Vt, n, ldv, nv0, nv1, pv, kk2, W2, r, Vo);
+    else apply_sel(Vt, n, ldv, nv0, nv1, pv, kk2, W2, r, Vo);
+  }
   if (threadIdx.x == 0 && crank == 0)
     // applies, pivoted Choleskys, M and H products, Jacobi sweeps (Gram counted above)
     flop_add(8.0 * ((double)m * kk1 + (double)n * kk2) * r + 16.0 * k * (double)k * k / 3.0 +
@@ -1406,11 +1546,16 @@ void launch_gram(zc* arena, zc* aout, int* ranks, const TruncDesc* d_desc, int n
   csize = std::max(1, std::min(csize, 8));
   // one launch per group whenever 2 GB of scratch allow it (a second launch of the tail
   // would wait for the whole first one on the stream)
-  const int wave = (int)std::max<int64_t>(1, (int64_t)ws_cap(2) / (per * csize * (int64_t)sizeof(zc)));
+  static const int ws_gb = getenv("CBIE_GRAM_WS_GB") ? atoi(getenv("CBIE_GRAM_WS_GB")) : 2;
+  const int wave = (int)std::max<int64_t>(1, (int64_t)ws_cap(ws_gb) / (per * csize * (int64_t)sizeof(zc)));
   const size_t need = (size_t)std::min(wave, nd) * csize * per;
   if (scratch.n < need) scratch.alloc(need);
   const int smem = (3 * GSQ + KG + 1) * (int)sizeof(zc);
   CK(cudaFuncSetAttribute(k_trunc_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  if (getenv("CBIE_NO_DMMA")) {   // A/B knob: DFMA Gram accumulation and applies
+    const int z = 0;
+    CK(cudaMemcpyToSymbol(g_gram_mma, &z, sizeof(int)));
+  }
   if (getenv("CBIE_ONESIDED_JACOBI")) {   // experiment knob (slower on configs 2 and 4: 4.7 sweeps)
     const int z = 1;
     CK(cudaMemcpyToSymbol(g_gram_onesided, &z, sizeof(int)));

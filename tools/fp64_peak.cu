@@ -19,6 +19,24 @@ __global__ void dfma_chain(double* out, int iters, double a, double b) {
   if (s == 12345.678) out[0] = s;
 }
 
+// (3) DMMA (mma.sync.m8n8k4.f64) chain: 8 independent accumulators per warp
+__global__ void dmma_chain(double* out, int iters) {
+  double a = 1e-3 * (threadIdx.x & 31), b = 1.0 - a;
+  double c[8][2];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) c[q][0] = c[q][1] = q;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                   : "+d"(c[q][0]), "+d"(c[q][1]) : "d"(a), "d"(b));
+  }
+  double s = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s += c[q][0] + c[q][1];
+  if (s == 12345.678) out[0] = s;
+}
+
 int main() {
   int sms = 0; cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
   double* d; cudaMalloc(&d, 8);
@@ -35,6 +53,21 @@ int main() {
   }
   double flops = 2.0 * 8 * 16 * (double)iters * threads * blocks;
   printf("{\"probe\":\"dfma_chain\",\"tflops\":%.3f,\"ms\":%.3f,\"sms\":%d}\n", flops / best / 1e9, best, sms);
+
+  for (int wpb = 4; wpb <= 16; wpb *= 2) {
+    const int th = 32 * wpb, bl = sms * (wpb == 4 ? 8 : wpb == 8 ? 4 : 2);
+    dmma_chain<<<bl, th>>>(d, 16);
+    cudaDeviceSynchronize();
+    best = 1e30f;
+    for (int r = 0; r < 5; ++r) {
+      cudaEventRecord(e0);
+      dmma_chain<<<bl, th>>>(d, iters);
+      cudaEventRecord(e1); cudaEventSynchronize(e1);
+      float ms; cudaEventElapsedTime(&ms, e0, e1); if (ms < best) best = ms;
+    }
+    const double fl = 512.0 * 8 * (double)iters * (th / 32) * bl;
+    printf("{\"probe\":\"dmma_chain\",\"warps_per_sm\":%d,\"tflops\":%.3f,\"ms\":%.3f}\n", th / 32 * bl / sms, fl / best / 1e9, best);
+  }
 
   cublasHandle_t h; cublasCreate(&h);
   for (int z = 0; z < 2; ++z) {
