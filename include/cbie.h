@@ -216,6 +216,13 @@ int cbie_far_field_sums(cbie_ctx* ctx, const cbie_c128* tab, int ntab, const dou
 int cbie_lowrank_truncate(cbie_ctx* ctx, const cbie_c128* U, int m, int k, const cbie_c128* V,
                           int n, double tol, int* r, cbie_c128* Uo, cbie_c128* Vo);
 
+/* Development benchmark of the Gram-path recompression kernel (no reference
+ * counterpart; tools/trunc_bench.py): nprob synthetic problems U (m x k), Vt (n x k)
+ * of numerical rank ~r_true, recompressed reps times on clusters of csize CTAs.
+ * ms_out: mean launch time [1]; prof_out: cycle counters [32]; ranks_out [nprob]. */
+int cbie_trunc_bench(cbie_ctx* ctx, int m, int n, int k, int r_true, int nprob, double tol, int csize,
+                     int reps, float* ms_out, unsigned long long* prof_out, int* ranks_out);
+
 /* ---- multi-GPU fill (one process per GPU, NCCL over NVLink / NVSwitch) ----
  * The reference fills leaves with a thread pool over HMatrix._fill_leaf
  * (hmatrix.py:207-224, 243-264); here each process fills the leaves it owns and

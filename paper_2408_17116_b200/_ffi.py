@@ -65,6 +65,8 @@ _SIGS = {
     "cbie_hlu_solve": (ct.c_int, [P, P, P, ct.c_int]),
     "cbie_lowrank_truncate": (ct.c_int, [P, P, ct.c_int, ct.c_int, P, ct.c_int, ct.c_double,
                                          ct.POINTER(ct.c_int), P, P]),
+    "cbie_trunc_bench": (ct.c_int, [P, ct.c_int, ct.c_int, ct.c_int, ct.c_int, ct.c_int, ct.c_double,
+                                    ct.c_int, ct.c_int, P, P, P]),
     "cbie_stats_json": (ct.c_int, [P, ct.c_int, ct.c_char_p, ct.c_size_t]),
     "cbie_partition_lpt": (None, [P, ct.c_int64, ct.c_int, P]),
     "cbie_shard_layout_host": (ct.c_int, [ct.c_int, P, P, P, P, P, ct.c_int, P, P, I64P]),

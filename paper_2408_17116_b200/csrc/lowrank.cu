@@ -886,3 +886,89 @@ void launch_dense_lr(zc* arena, int* ranks, const DenseLRDesc* d_desc, int nd, i
 }
 
 CBIE_FLOP_API(lowrank)
+
+// Development benchmark of the Gram-path recompression kernel (tools/trunc_bench.py):
+// nprob independent problems U (m x k) Vt (n x k), Gaussian columns scaled by
+// 10^(-4 j / r_true) (numerical rank ~ r_true at tol 1e-4), recompressed reps times into
+// a separate output region (inputs unchanged).  ms_out: mean launch time; prof_out (32):
+// the CBIE_PROFILE cycle counters of the last launch; ranks_out (nprob): kept ranks.
+extern "C" int cbie_trunc_bench(cbie_ctx* c, int m, int n, int k, int r_true, int nprob, double tol, int csize,
+                                int reps, float* ms_out, unsigned long long* prof_out, int* ranks_out) {
+  try {
+    cudaSetDevice(c->device);
+    cudaStream_t s = c->stream;
+    const int64_t per_in = (int64_t)(m + n) * k, per_out = (int64_t)(m + n) * k;
+    std::vector<zc> h((size_t)per_in * nprob);
+    uint64_t st = 0x9E3779B97F4A7C15ull;
+    auto nrm = [&]() {   // Box-Muller on a 64-bit LCG
+      st = st * 6364136223846793005ull + 1442695040888963407ull;
+      const double u1 = ((st >> 11) + 1.0) / 9007199254740993.0;
+      st = st * 6364136223846793005ull + 1442695040888963407ull;
+      const double u2 = (st >> 11) / 9007199254740992.0;
+      return sqrt(-2.0 * log(u1)) * cos(6.283185307179586 * u2);
+    };
+    for (int p = 0; p < nprob; ++p)
+      for (int l = 0; l < k; ++l) {
+        const double sc = pow(10.0, -4.0 * l / std::max(1, r_true));
+        zc* U = h.data() + (size_t)p * per_in;
+        for (int i = 0; i < m; ++i) U[(size_t)l * m + i] = zmk(sc * nrm(), sc * nrm());
+        zc* V = U + (size_t)m * k;
+        for (int j = 0; j < n; ++j) V[(size_t)l * n + j] = zmk(nrm(), nrm());
+      }
+    DBuf<zc> ar, out;
+    ar.upload(h, s);
+    out.alloc((size_t)per_out * nprob);
+    std::vector<TruncDesc> ds(nprob);
+    for (int p = 0; p < nprob; ++p) {
+      TruncDesc& d = ds[p];
+      d.in_u = (int64_t)p * per_in;
+      d.in_v = d.in_u + (int64_t)m * k;
+      d.ldu = m;
+      d.ldv = n;
+      d.skip_slot = -1;
+      d.out_u = (int64_t)p * per_out;
+      d.out_v = d.out_u + (int64_t)m * k;
+      d.m = m;
+      d.n = n;
+      d.k = k;
+      d.k_slot = -1;
+      d.cap = k;
+      d.out_slot = p;
+    }
+    DBuf<TruncDesc> dd;
+    dd.upload(ds, s);
+    DBuf<int> ranks, defer;
+    ranks.alloc(nprob);
+    defer.alloc(nprob + 1);
+    DBuf<unsigned long long> ovf;
+    ovf.alloc(1);
+    CK(cudaMemsetAsync(ovf.p, 0, 8, s));
+    DBuf<zc> scratch;
+    trunc_prof_enable(true, 0);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    float tot = 0.0f;
+    for (int it = 0; it <= reps; ++it) {
+      CK(cudaMemsetAsync(defer.p, 0, sizeof(int), s));
+      CK(cudaMemsetAsync(g_trunc_prof, 0, 32 * sizeof(unsigned long long), s));
+      cudaEventRecord(e0, s);
+      launch_truncate_gram(ar.p, ranks.p, dd.p, nprob, tol, ovf.p, scratch, s, out.p, defer.p, nullptr,
+                           k > 64 ? std::max(m, n) : 0, csize);
+      cudaEventRecord(e1, s);
+      CK(cudaEventSynchronize(e1));
+      float ms = 0.0f;
+      cudaEventElapsedTime(&ms, e0, e1);
+      if (it > 0) tot += ms;   // the first launch is a warm-up
+    }
+    *ms_out = tot / std::max(1, reps);
+    CK(cudaMemcpy(prof_out, g_trunc_prof, 32 * sizeof(unsigned long long), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(ranks_out, ranks.p, sizeof(int) * nprob, cudaMemcpyDeviceToHost));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    return CBIE_OK;
+  } catch (const cbie_error& e) {
+    c->err = e.what();
+    return e.code;
+  }
+}

@@ -736,6 +736,9 @@ constexpr int GTPW = 9;     // upper tiles per warp (36 tiles of k = 64 over 4 w
 constexpr int GMCH = 32;    // rows per staged chunk
 constexpr int GSLD = 36;    // staging column stride (zc)
 __device__ int g_gram_mma = 1;   // 0: DFMA gram_acc / apply_sel (CBIE_NO_DMMA)
+__device__ int g_ms_min_add = 1;    // multi-stage: fewest new columns per stage (CBIE_MS_MIN_ADD)
+__device__ int g_pchol_w = NW / 2;   // warps per Gram pivoted Cholesky (CBIE_PCHOL_W)
+__device__ int g_pcholh_w = NW;      // warps of the core pivoted Cholesky (CBIE_PCHOLH_W)
 
 __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, bool valid) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
@@ -1268,11 +1271,13 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   //    gather space), the others G_v (gather through the global scratch Rvg, written later)
   __shared__ int kuv[2];
   {
-    const int w = threadIdx.x >> 5;
-    const bool ga = w < NW / 2;
-    const int kr = pchol_grp(ga ? Gu : Gv, k, ga ? pu : pv, CHOL_EPS, false, NW / 2, ga ? w : w - NW / 2,
-                             ga ? 1 : 2, ga ? X2 : Rvg, ga ? scu : scv);
-    if ((threadIdx.x & (NT / 2 - 1)) == 0) kuv[ga ? 0 : 1] = kr;
+    const int w = threadIdx.x >> 5, GW = g_pchol_w;   // warps per factorisation
+    const bool ga = w < GW, gb = w >= NW / 2 && w < NW / 2 + GW;
+    if (ga || gb) {
+      const int kr = pchol_grp(ga ? Gu : Gv, k, ga ? pu : pv, CHOL_EPS, false, GW, ga ? w : w - NW / 2,
+                               ga ? 1 : 2, ga ? X2 : Rvg, ga ? scu : scv);
+      if ((threadIdx.x & (NT / 2 - 1)) == 0) kuv[ga ? 0 : 1] = kr;
+    }
     __syncthreads();
   }
   const int ku = kuv[0], kv = kuv[1];
@@ -1316,7 +1321,14 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   for (int e = threadIdx.x; e < kk1 * kk2; e += NT) Mg[e] = X2[e];
   __syncthreads();
   stamp(6);
-  const int kp = pchol_grp(H, kk1, S.perm, (GDELTA * tol) * (GDELTA * tol), true, NW, threadIdx.x >> 5, 1, X2, scu);
+  __shared__ int kps;
+  if ((threadIdx.x >> 5) < g_pcholh_w) {
+    const int kq = pchol_grp(H, kk1, S.perm, (GDELTA * tol) * (GDELTA * tol), true, g_pcholh_w, threadIdx.x >> 5, 1,
+                             X2, scu);
+    if (threadIdx.x == 0) kps = kq;
+  }
+  __syncthreads();
+  const int kp = kps;
   stamp(7);
   int sweeps = 0;
   if (g_gram_onesided) {
@@ -1496,7 +1508,7 @@ __global__ void __launch_bounds__(NT, 1)
       const int add = min(KG - r, k - done);
       // too little room left for the remaining columns (each stage costs a full Gram
       // recompression): Householder kernels -- nothing was written to the output yet
-      if (add < min(16, k - done)) {
+      if (add < min(g_ms_min_add, k - done)) {
         if (threadIdx.x == 0 && crank == 0) defer[1 + atomicAdd(defer, 1)] = idx ? tix : base + pb;
         return;
       }
@@ -1552,6 +1564,18 @@ void launch_gram(zc* arena, zc* aout, int* ranks, const TruncDesc* d_desc, int n
   if (scratch.n < need) scratch.alloc(need);
   const int smem = (3 * GSQ + KG + 1) * (int)sizeof(zc);
   CK(cudaFuncSetAttribute(k_trunc_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  if (getenv("CBIE_MS_MIN_ADD")) {
+    const int z = std::max(1, atoi(getenv("CBIE_MS_MIN_ADD")));
+    CK(cudaMemcpyToSymbol(g_ms_min_add, &z, sizeof(int)));
+  }
+  if (getenv("CBIE_PCHOL_W")) {
+    const int z = std::max(1, std::min(NW / 2, atoi(getenv("CBIE_PCHOL_W"))));
+    CK(cudaMemcpyToSymbol(g_pchol_w, &z, sizeof(int)));
+  }
+  if (getenv("CBIE_PCHOLH_W")) {
+    const int z = std::max(1, std::min(NW, atoi(getenv("CBIE_PCHOLH_W"))));
+    CK(cudaMemcpyToSymbol(g_pcholh_w, &z, sizeof(int)));
+  }
   if (getenv("CBIE_NO_DMMA")) {   // A/B knob: DFMA Gram accumulation and applies
     const int z = 0;
     CK(cudaMemcpyToSymbol(g_gram_mma, &z, sizeof(int)));
