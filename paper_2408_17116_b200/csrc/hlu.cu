@@ -121,7 +121,11 @@ struct Recorder {
   int64_t pool_budget = 0;
   int nbuf = 0;
   // free lists per size class: (offset, buffer id)
-  std::map<int, std::vector<std::pair<int64_t, int>>> freel;
+  // (keyed by the level of the chunk's last access: reuse takes the chunk that was done
+  // EARLIEST in the schedule, so the new owner waits as little as possible)
+  std::map<int, std::multimap<int, std::pair<int64_t, int>>> freel;
+  bool reuse_oldest = getenv("CBIE_REUSE_OLDEST") != nullptr;   // A/B knob: tape order (round 1)
+  int64_t free_seq = 0;
   std::vector<int> init_ranks;   // initial values of every rank slot
   // dependency state per buffer: access rectangles with their levels
   struct Access {
@@ -134,12 +138,36 @@ struct Recorder {
     int kind;   // virtual kind (executor stream) of the access, -1: collapsed (see floor_w / floor_r)
   };
   std::vector<std::vector<Entry>> ent;
+  // fixed-capacity access list (no heap traffic on the recording path)
+  struct AccList {
+    Access a[80];
+    int n = 0;
+    AccList() {}
+    AccList(std::initializer_list<Access> l) {
+      for (const Access& x : l) push_back(x);
+    }
+    void push_back(const Access& x) {
+      if (n >= 80) throw cbie_error(CBIE_EINVALID, "H-LU recorder: too many accesses in one task");
+      a[n++] = x;
+    }
+    const Access* begin() const { return a; }
+    const Access* end() const { return a + n; }
+  };
   // per buffer: latest level per op kind among the accesses folded into its
   // collapsed entries; a task conflicting with a collapsed entry depends on all of them
   std::vector<std::array<int, NVK>> floor_w, floor_r;   // writes / reads folded
   // per launch group (level, kind): latest level of every kind it depends on (the
   // executor runs each kind on its own stream, so one event per kind suffices)
-  std::map<std::pair<int, int>, std::array<int, NVK>> gdep;
+  // (indexed level * NVK + kind; an untouched entry has has = false)
+  struct GDep {
+    std::array<int, NVK> d;
+    bool has = false;
+  };
+  std::vector<GDep> gdep;
+  const GDep* gdep_find(int level, int vk) const {
+    const size_t i = (size_t)level * NVK + vk;
+    return i < gdep.size() && gdep[i].has ? &gdep[i] : nullptr;
+  }
   std::vector<int> last_w, max_r;   // (kept for the whole-buffer fast path)
   // tapes
   std::vector<GemmD> gemm;
@@ -212,7 +240,7 @@ struct Recorder {
     ent[buf].clear();
     ent[buf].push_back(Entry{whole(buf), mx, true, -1});
   }
-  void addA(int kind, int idx, const std::vector<Access>& rd, const std::vector<Access>& wr) {
+  void addA(int kind, int idx, const AccList& rd, const AccList& wr) {
     int lvl = 0;
     int dk[NVK];
     for (int q = 0; q < NVK; ++q) dk[q] = -1;
@@ -239,13 +267,14 @@ struct Recorder {
     if (serial) lvl = (int)tasks.size() + 1;
     const int vk = vkind(kind, lvl);
     {
-      auto it = gdep.find({lvl, vk});
-      if (it == gdep.end()) {
-        std::array<int, NVK> a;
-        for (int q = 0; q < NVK; ++q) a[q] = dk[q];
-        gdep.emplace(std::make_pair(lvl, vk), a);
+      const size_t gi = (size_t)lvl * NVK + vk;
+      if (gi >= gdep.size()) gdep.resize(std::max(gi + 1, gdep.size() * 2));
+      GDep& g = gdep[gi];
+      if (!g.has) {
+        g.has = true;
+        for (int q = 0; q < NVK; ++q) g.d[q] = dk[q];
       } else {
-        for (int q = 0; q < NVK; ++q) it->second[q] = std::max(it->second[q], dk[q]);
+        for (int q = 0; q < NVK; ++q) g.d[q] = std::max(g.d[q], dk[q]);
       }
     }
     for (const Access& r : rd)
@@ -265,7 +294,7 @@ struct Recorder {
       acc_start.push_back((int64_t)acc_buf.size());
     }
   }
-  void accs_of(const Mat& m, std::vector<Access>& v) const {
+  void accs_of(const Mat& m, AccList& v) const {
     v.push_back(acc(m));
     if (m.rslot >= 0 && slot_owner[m.rslot] >= 0) v.push_back(whole(slot_owner[m.rslot]));
     if (m.cslot >= 0 && slot_owner[m.cslot] >= 0) v.push_back(whole(slot_owner[m.cslot]));
@@ -283,10 +312,15 @@ struct Recorder {
     if (a.cslot >= 0) v.push_back(slot_owner[a.cslot]);
   }
   void add(int kind, int idx, std::initializer_list<int> rd, std::initializer_list<int> wr) {
-    add(kind, idx, std::vector<int>(rd), std::vector<int>(wr));
+    AccList r, w;
+    for (int b : rd)
+      if (b >= 0) r.push_back(whole(b));
+    for (int b : wr)
+      if (b >= 0) w.push_back(whole(b));
+    addA(kind, idx, r, w);
   }
   void add(int kind, int idx, const std::vector<int>& rd, const std::vector<int>& wr) {
-    std::vector<Access> r, w;
+    AccList r, w;
     for (int b : rd)
       if (b >= 0) r.push_back(whole(b));
     for (int b : wr)
@@ -317,29 +351,51 @@ struct Recorder {
     int cls;
     int buf;
   };
-  std::map<int, int> refc;          // live temporaries: buffer id -> references
-  std::map<int, Tmp> live;
+  std::vector<int> refc;            // per buffer: references of a live temporary (0: not one)
+  std::vector<Tmp> live;
   void retain(int buf) {
-    auto it = refc.find(buf);
-    if (it != refc.end()) ++it->second;
+    if (buf >= 0 && buf < (int)refc.size() && refc[buf] > 0) ++refc[buf];
   }
+  int site = 0;                 // debug: allocation volume per call site (CBIE_MEMLOG)
+  int64_t site_elems[12] = {};
   Tmp alloc(int64_t elems) {
     Tmp t = alloc_raw(elems);
+    site_elems[site] += cls_size(t.cls);
+    if ((int)refc.size() <= t.buf) {
+      refc.resize((size_t)nbuf + 1024, 0);
+      live.resize((size_t)nbuf + 1024);
+    }
     refc[t.buf] = 1;
     live[t.buf] = t;
     return t;
   }
+  // size classes: (4 + j) 2^e elements, j = 0..3 (at most 25 % slack; powers of two
+  // wasted up to half of every chunk and the pool recycled twice as often)
+  static int64_t cls_size(int cls) { return (int64_t)(4 + (cls & 3)) << (cls >> 2); }
   Tmp alloc_raw(int64_t elems) {
-    int cls = 10;
-    while (((int64_t)1 << cls) < elems) ++cls;
-    auto& fl = freel[cls];
-    const int64_t sz = (int64_t)1 << cls;
-    if (!fl.empty() && pool_top + sz > pool_budget) {
-      auto pr = fl.front();   // oldest freed chunk first
-      fl.erase(fl.begin());
-      collapse_reuse(pr.second);   // new owner: every earlier access conflicts
-      if (track) reuse_at.push_back({(int)tasks.size(), pr.second});
-      return Tmp{pr.first, cls, pr.second};
+    int cls = 8 << 2;   // 4 * 2^8 = 1024 elements
+    while (cls_size(cls) < elems) ++cls;
+    const int64_t sz = cls_size(cls);
+    if (pool_top + sz > pool_budget) {
+      // free chunks of this class and of the next three (< 2x the size): the one whose last
+      // access has the lowest level
+      int best = -1, blvl = INT32_MAX;
+      for (int c = cls; c < cls + 4; ++c) {
+        auto it = freel.find(c);
+        if (it == freel.end() || it->second.empty()) continue;
+        if (it->second.begin()->first < blvl) {
+          blvl = it->second.begin()->first;
+          best = c;
+        }
+      }
+      if (best >= 0) {
+        auto& fl = freel[best];
+        auto pr = fl.begin()->second;
+        fl.erase(fl.begin());
+        collapse_reuse(pr.second);   // new owner: every earlier access conflicts
+        if (track) reuse_at.push_back({(int)tasks.size(), pr.second});
+        return Tmp{pr.first, best, pr.second};
+      }
     }
     Tmp t{leaf_end + pool_top, cls, new_buf()};
     buf_off[t.buf] = t.off;
@@ -349,13 +405,13 @@ struct Recorder {
   }
   void release(const Tmp& t) { release_buf(t.buf); }
   void release_buf(int buf) {
-    auto it = refc.find(buf);
-    if (it == refc.end()) return;        // not a temporary (leaf storage)
-    if (--it->second > 0) return;
+    if (buf < 0 || buf >= (int)refc.size() || refc[buf] <= 0) return;   // not a live temporary (leaf storage)
+    if (--refc[buf] > 0) return;
     const Tmp& t = live[buf];
-    freel[t.cls].push_back({t.off, t.buf});
-    refc.erase(it);
-    live.erase(buf);
+    int lvl = 0;
+    for (auto& e : ent[buf]) lvl = std::max(lvl, e.level);
+    freel[t.cls].emplace(reuse_oldest ? (int)std::min<int64_t>(free_seq++, INT32_MAX) : lvl,
+                         std::make_pair(t.off, t.buf));
   }
 
   Mat tmp_mat(int rows, int cols, int rslot, int cslot, std::vector<Tmp>& owned) {
@@ -404,11 +460,11 @@ struct Recorder {
     gemm.push_back(d);
     flops += 8.0 * A.rows * A.cols * B.cols;
     ++gemm_count;
-    std::vector<Access> rd;
+    AccList rd;
     accs_of(A, rd);
     accs_of(B, rd);
     accs_of(C, rd);   // C's dims (and data when beta != 0)
-    addA(OP_GEMM, (int)gemm.size() - 1, rd, {acc(C)});
+    addA(OP_GEMM, (int)gemm.size() - 1, rd, AccList{acc(C)});
   }
   // Y = a X + b Y
   void op_ew(const Mat* X, const Mat& Y, zc a, zc b) {
@@ -422,10 +478,10 @@ struct Recorder {
     d.b = b;
     d.hasX = X != nullptr;
     ew.push_back(d);
-    std::vector<Access> rd;
+    AccList rd;
     if (X) accs_of(*X, rd);
     accs_of(Y, rd);
-    addA(OP_EW, (int)ew.size() - 1, rd, {acc(Y)});
+    addA(OP_EW, (int)ew.size() - 1, rd, AccList{acc(Y)});
   }
   void op_trsm(const Mat& T, int64_t pivoff, int variant, const Mat& Y) {
     if (Y.cols == 0) return;
@@ -433,9 +489,9 @@ struct Recorder {
     trsm.push_back(d);
     flops += 4.0 * T.rows * T.rows * Y.cols;
     ++trsm_count;
-    std::vector<Access> rd{acc(T)};
+    AccList rd{acc(T)};
     accs_of(Y, rd);
-    addA(OP_TRSM, (int)trsm.size() - 1, rd, {acc(Y)});
+    addA(OP_TRSM, (int)trsm.size() - 1, rd, AccList{acc(Y)});
   }
   void op_getrf(const Mat& A, int64_t pivoff, int leaf) {
     getrf.push_back(GetrfD{A.off, pivoff, A.rows, leaf});
@@ -455,7 +511,7 @@ struct Recorder {
     d.np = (int)ps.size();
     for (int i = 0; i < d.np; ++i) d.p[i] = ps[i];
     cat.push_back(d);
-    std::vector<Access> rd;
+    AccList rd;
     if (srcmats) {
       for (const Mat& m : *srcmats) accs_of(m, rd);
     } else {
@@ -466,7 +522,7 @@ struct Recorder {
       if (p.cols.slot >= 0 && slot_owner[p.cols.slot] >= 0) rd.push_back(whole(slot_owner[p.cols.slot]));
     // the out-slot belongs to the destination buffer: writes of both halves share it
     Access w{dstbuf, dst_rid, 0, 1 << 30, 0, 1 << 30};
-    addA(OP_CONCAT, (int)cat.size() - 1, rd, {w});
+    addA(OP_CONCAT, (int)cat.size() - 1, rd, AccList{w});
   }
   void op_dlr(const Mat& P, const LR& o) {
     DenseLRDesc d;
@@ -490,10 +546,13 @@ struct Recorder {
     trunc.push_back(d);
     trunc_kmax.push_back(kmax);
     ++trunc_count;
-    std::vector<int> rd{rdbuf, rdbuf2, wrbuf};
-    if (d.k_slot >= 0) rd.push_back(slot_owner[d.k_slot]);
-    if (d.skip_slot >= 0) rd.push_back(slot_owner[d.skip_slot]);
-    add(OP_TRUNC, (int)trunc.size() - 1, rd, {rdbuf, wrbuf});
+    AccList rd, wr;
+    for (int b : {rdbuf, rdbuf2, wrbuf, d.k_slot >= 0 ? slot_owner[d.k_slot] : -1,
+                  d.skip_slot >= 0 ? slot_owner[d.skip_slot] : -1})
+      if (b >= 0) rd.push_back(whole(b));
+    for (int b : {rdbuf, wrbuf})
+      if (b >= 0) wr.push_back(whole(b));
+    addA(OP_TRUNC, (int)trunc.size() - 1, rd, wr);
   }
 };
 
@@ -537,7 +596,37 @@ struct Builder {
   cbie_hlu& F;
   const Tree& T;
   const int C;
-  Builder(Recorder& r, cbie_hlu& f) : R(r), F(f), T(f.tree), C(f.tree.C) {}
+  Builder(Recorder& r, cbie_hlu& f) : R(r), F(f), T(f.tree), C(f.tree.C) {
+    for (const auto& L : T.leaves)
+      if (L.kind == BLK_LR) {
+        int& c = capmax[std::max(L.m, L.n)];
+        c = std::max(c, L.cap);
+      }
+  }
+  // Capacity of a TEMPORARY low-rank block (the parts and the result of prod_lowrank): the
+  // products are sub-blocks of an admissible block, so their ranks are those of the
+  // low-rank factor leaves of that size -- tmp_cap_mult x the largest factor-leaf capacity
+  // (2 r + 48) of the size class, not min(m, n).  Smaller temporaries keep the pool from
+  // recycling chunks (every reuse orders the new owner after the old one and deepens the
+  // schedule).  A clipped truncation is counted like a leaf's and re-factored with larger
+  // capacities (cbie_hlu_factor).  CBIE_TMP_CAP_MULT=0: min(m, n) as before.
+  std::map<int, int> capmax;   // max(m, n) of the low-rank leaves -> largest factor capacity
+  double tmp_cap_mult = getenv("CBIE_TMP_CAP_MULT") ? atof(getenv("CBIE_TMP_CAP_MULT")) : 1.5;
+  int tcap(int m, int n) const {
+    const int full = std::min(m, n);
+    if (!(tmp_cap_mult > 0.0) || capmax.empty()) return full;
+    const int s = std::max(m, n);
+    auto it = capmax.lower_bound(s);
+    double c;
+    if (it != capmax.end()) {
+      c = it->second;
+    } else {   // larger than every low-rank leaf: the largest class, +25 % per doubling
+      auto last = std::prev(capmax.end());
+      c = last->second;
+      for (int z = last->first; z < s; z *= 2) c *= 1.25;
+    }
+    return std::max(1, std::min(full, (int)(tmp_cap_mult * c)));
+  }
 
   // Lazy low-rank updates: updates to a low-rank LEAF are queued and merged by ONE
   // concatenation + recompression when the leaf is next read (or the queue fills),
@@ -621,6 +710,61 @@ struct Builder {
   void flush_all() {
     while (!pend.empty()) flush(pend.begin()->first);
   }
+  // Collected products of a FRESH temporary target (prod_lowrank parts): the products are
+  // formed independently and merged by one concatenation + recompression, instead of one
+  // recompression per product (hmatrix.py:625-633 adds them one after the other).  Same
+  // sum, one truncation instead of two, and the two products no longer wait for each other.
+  bool par_prod = getenv("CBIE_NO_PARPROD") == nullptr;
+  void flush_into(const LR& Tg, Pend& p) {
+    if (p.U.empty()) return;
+    const int m = Tg.U.rows, n = Tg.Vt.rows;
+    const int kc = p.capsum;
+    R.site = 8;
+    Recorder::Tmp t = R.alloc((int64_t)(m + n) * kc);
+    R.site = 0;
+    const int ks = R.new_slot(0, t.buf);
+    std::vector<Piece> pu, pv;
+    std::vector<int> bu, bv;
+    for (size_t i = 0; i < p.U.size(); ++i) {
+      pu.push_back(Piece{p.U[i].view(), p.U[i].rows, 0, p.U[i].Cc(), p.sign[i]});
+      pv.push_back(Piece{p.Vt[i].view(), p.Vt[i].rows, 0, p.Vt[i].Cc(), zmk(1, 0)});
+      bu.push_back(p.U[i].buf);
+      bv.push_back(p.Vt[i].buf);
+    }
+    R.op_concat(t.off, m, ks, t.buf, pu, bu, 0, &p.U);
+    R.op_concat(t.off + (int64_t)m * kc, n, ks, t.buf, pv, bv, 1, &p.Vt);
+    TruncDesc d;
+    d.in_u = t.off;
+    d.in_v = t.off + (int64_t)m * kc;
+    d.ldu = m;
+    d.ldv = n;
+    d.out_u = Tg.U.off;
+    d.out_v = Tg.Vt.off;
+    d.m = m;
+    d.n = n;
+    d.k = kc;
+    d.k_slot = ks;
+    d.cap = Tg.cap;
+    d.out_slot = Tg.slot;
+    d.skip_slot = -1;
+    R.op_trunc(d, std::min(kc, std::max(m, n)), t.buf, -1, Tg.buf);
+    R.flops += trunc_flops(m, n, kc);
+    for (size_t i = 0; i < p.U.size(); ++i) {
+      R.release_buf(p.U[i].buf);
+      R.release_buf(p.Vt[i].buf);
+    }
+    R.release(t);
+    p = Pend();
+  }
+  void collect(Pend& p, const Mat& U, const Mat& Vt, zc sign) {
+    if (U.cols == 0) return;
+    R.retain(U.buf);
+    R.retain(Vt.buf);
+    p.U.push_back(U);
+    p.Vt.push_back(Vt);
+    p.sign.push_back(sign);
+    p.capsum += U.cols;
+  }
 
   const BNode& nd(int id) const { return T.nodes[id]; }
   int rows_of(int id) const { return T.dofs(nd(id).r); }
@@ -699,7 +843,9 @@ struct Builder {
     } else if (kind(id) == BLK_LR) {
       LR l = lr(id);
       std::vector<Recorder::Tmp> own;
+      R.site = 9;
       Mat W = R.tmp_mat(l.cap, X.cols, l.slot, X.cslot, own);
+      R.site = 0;
       R.op_gemm(l.V(), X, W, zmk(1, 0), zmk(0, 0));
       R.op_gemm(l.U, W, OUT, alpha, beta);
       for (auto& t : own) R.release(t);
@@ -720,7 +866,9 @@ struct Builder {
     } else if (kind(id) == BLK_LR) {
       LR l = lr(id);
       std::vector<Recorder::Tmp> own;
+      R.site = 9;
       Mat W = R.tmp_mat(X.rows, l.cap, X.rslot, l.slot, own);
+      R.site = 0;
       R.op_gemm(X, l.U, W, zmk(1, 0), zmk(0, 0));
       R.op_gemm(W, l.V(), OUT, alpha, beta);
       for (auto& t : own) R.release(t);
@@ -757,7 +905,9 @@ struct Builder {
     if (U.cols == 0) return;
     std::vector<Recorder::Tmp> own;
     const int kc = Tg.cap + U.cols;
+    R.site = 1;
     Recorder::Tmp t = R.alloc((int64_t)(m + n) * kc);
+    R.site = 0;
     own.push_back(t);
     const int ks = R.new_slot(0, t.buf);
     std::vector<Piece> pu{Piece{Tg.U.view(), m, 0, Tg.U.Cc(), zmk(1, 0)},
@@ -793,7 +943,9 @@ struct Builder {
   // dense P (m x n) -> truncated low rank temp (hmatrix.py:605-609)
   LR dense_to_lr(const Mat& P, std::vector<Recorder::Tmp>& own) {
     const int m = P.rows, n = P.cols;
+    R.site = 7;
     LR o = R.tmp_lr(m, n, std::min(m, n), own);
+    R.site = 0;
     R.op_dlr(P, o);
     return o;
   }
@@ -836,9 +988,11 @@ struct Builder {
     int id = -1;     // node id, or -1 for a temp LR
     LR tl;
     int rows = 0, cols = 0;
+    Pend* q = nullptr;   // temp LR: collect the products here (flush_into) instead of adding
   };
   void tgt_add_lr(const Tgt& t, const Mat& U, const Mat& Vt, zc sign) {
     if (t.id >= 0) add_lr(t.id, U, Vt, sign);
+    else if (t.q) collect(*t.q, U, Vt, sign);
     else add_lr_to(t.tl, U, Vt, sign);
   }
   void tgt_add_full(const Tgt& t, const Mat& P) {
@@ -847,7 +1001,8 @@ struct Builder {
     } else {
       std::vector<Recorder::Tmp> own;
       LR o = dense_to_lr(P, own);
-      add_lr_to(t.tl, o.U, o.Vt, zmk(1, 0));
+      if (t.q) collect(*t.q, o.U, o.Vt, zmk(1, 0));
+      else add_lr_to(t.tl, o.U, o.Vt, zmk(1, 0));
       for (auto& x : own) R.release(x);
     }
   }
@@ -857,24 +1012,34 @@ struct Builder {
     const int m = rows_of(A), n = cols_of(B);
     if (kind(A) == BLK_LR) {
       LR a = lr(A);
+      R.site = 5;
       Mat Wt = R.tmp_mat(n, a.cap, -1, a.slot, own);      // (A.V B)^T
+      R.site = 0;
       mul_left(a.V(), B, Wt.T(), zmk(1, 0), false);
       tgt_add_lr(t, a.U, Wt, sign);
     } else if (kind(B) == BLK_LR) {
       LR b = lr(B);
+      R.site = 5;
       Mat W = R.tmp_mat(m, b.cap, -1, b.slot, own);
+      R.site = 0;
       mul_right(A, b.U, W, zmk(1, 0), false);
       tgt_add_lr(t, W, b.Vt, sign);
     } else if (kind(A) == BLK_DENSE && kind(B) == BLK_DENSE) {
+      R.site = 6;
       Mat P = R.tmp_mat(m, n, -1, -1, own);
+      R.site = 0;
       R.op_gemm(D(A), D(B), P, sign, zmk(0, 0));
       tgt_add_full(t, P);
     } else if (kind(A) == BLK_DENSE) {
+      R.site = 6;
       Mat P = R.tmp_mat(m, n, -1, -1, own);
+      R.site = 0;
       mul_left(D(A), B, P, sign, false);
       tgt_add_full(t, P);
     } else if (kind(B) == BLK_DENSE) {
+      R.site = 6;
       Mat P = R.tmp_mat(m, n, -1, -1, own);
+      R.site = 0;
       mul_right(A, D(B), P, sign, false);
       tgt_add_full(t, P);
     } else if (t.id >= 0 && kind(t.id) == BLK_H) {
@@ -909,15 +1074,22 @@ struct Builder {
         const int ma = rsz(A, a), nb = csz(B, b);
         Tgt t;
         t.id = -1;
-        t.tl = R.tmp_lr(ma, nb, std::min(ma, nb), own2);
+        R.site = 2;
+        t.tl = R.tmp_lr(ma, nb, tcap(ma, nb), own2);
+        R.site = 0;
+        Pend q;
+        if (par_prod) t.q = &q;
         for (int k = 0; k < a_.nc; ++k) gemm_h(t, kid(A, a, k), kid(B, k, b), zmk(1, 0));
+        if (par_prod) flush_into(t.tl, q);
         parts.push_back(t.tl);
         pr.push_back(roff(A, a));
         pc.push_back(coff(B, b));
       }
     int kc = 0;
     for (auto& p : parts) kc += p.cap;
+    R.site = 3;
     Recorder::Tmp t = R.alloc((int64_t)(m + n) * kc);
+    R.site = 0;
     own2.push_back(t);
     const int ks = R.new_slot(0, t.buf);
     std::vector<Piece> pu, pv;
@@ -935,7 +1107,9 @@ struct Builder {
     }
     R.op_concat(t.off, m, ks, t.buf, pu, bu, 0, &mu);
     R.op_concat(t.off + (int64_t)m * kc, n, ks, t.buf, pv, bu, 1, &mv);
-    LR o = R.tmp_lr(m, n, std::min(m, n), own);
+    R.site = 4;
+    LR o = R.tmp_lr(m, n, tcap(m, n), own);
+    R.site = 0;
     TruncDesc d;
     d.in_u = t.off;
     d.in_v = t.off + (int64_t)m * kc;
@@ -1033,7 +1207,9 @@ struct Builder {
       for (int c = 0; c < nd(B).nc; ++c) lsolve_blk(L, kid(B, 0, c));
     } else if (nd(B).nr == 1) {
       std::vector<Recorder::Tmp> own;
+      R.site = 10;
       Mat X = R.tmp_mat(rows_of(B), cols_of(B), -1, -1, own);
+      R.site = 0;
       densify(B, X);
       lsolve(L, X);
       overwrite(B, X);
@@ -1056,7 +1232,9 @@ struct Builder {
       for (int a = 0; a < nd(B).nr; ++a) rsolve_blk(kid(B, a, 0), U);
     } else if (nd(B).nc == 1) {
       std::vector<Recorder::Tmp> own;
+      R.site = 10;
       Mat X = R.tmp_mat(rows_of(B), cols_of(B), -1, -1, own);
+      R.site = 0;
       densify(B, X);
       rsolve(X, U);
       overwrite(B, X);
@@ -1243,10 +1421,10 @@ void make_plan(Plan& P, cudaStream_t s, const Recorder* Rx = nullptr, const std:
     for (size_t i = 0; i < groups.size(); ++i) gid[{groups[i].level, vkind(groups[i].kind, groups[i].level)}] = (int)i;
     for (auto& gr : groups) {
       const int gvk = vkind(gr.kind, gr.level);
-      auto it = R.gdep.find({gr.level, gvk});
-      if (it == R.gdep.end()) continue;
+      const Recorder::GDep* it = R.gdep_find(gr.level, gvk);
+      if (!it) continue;
       for (int q = 0; q < NVK; ++q) {
-        const int L = it->second[q];
+        const int L = it->d[q];
         if (q == gvk || L < 0) continue;
         if (L >= gr.level) throw cbie_error(CBIE_EINVALID, "H-LU schedule: dependency not earlier than its task");
         auto jt = gid.find({L, q});
@@ -1341,6 +1519,8 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
   DBuf<zc>& dlr_scratch = P.dlr_scratch;
   const size_t trsm_smem = P.trsm_smem, getrf_smem = P.getrf_smem;
   CK(cudaFuncSetAttribute(k_trsm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)trsm_smem));
+  CK(cudaFuncSetAttribute(k_gemm_mma<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gm_smem_bytes(64)));
+  CK(cudaFuncSetAttribute(k_gemm_mma<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gm_smem_bytes(32)));
   // blocked diagonal-leaf kernels (dense_lu.cuh) unless a leaf exceeds LU_NMAX
   const bool blk_lu = getenv("CBIE_LU_UNBLOCKED") == nullptr && P.maxn_lu <= LU_NMAX;
   const size_t blk_smem = ((size_t)std::max(P.maxn_lu, 1) + LU_QC) * LU_NB * sizeof(zc);
@@ -1414,6 +1594,7 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
       case OP_GEMM: {
         // [start, start + split): dense x dense (64 x 64 tiles); the rest: 32 x 32 tiles
         const bool g64 = getenv("CBIE_GEMM32") == nullptr;
+        const bool dmma_gemm = getenv("CBIE_GEMM_DFMA") == nullptr;   // A/B knob: the DFMA tile kernels
         const int split = g64 ? gr.split : 0;
         auto launch = [&](int b, int e, bool wide) {
           if (e <= b) return;
@@ -1424,7 +1605,14 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
           }
           for (int b0 = b; b0 < e; b0 += 65535) {
             const int nb = std::min(65535, e - b0);
-            if (wide)
+            if (dmma_gemm) {   // FP64 tensor-core tiles (64 x 64, or 64 x 32 for the ragged products)
+              if (wide)
+                k_gemm_mma<64><<<dim3(ceil_div(mt, GM_BM), ceil_div(nt, 64), nb), 256, gm_smem_bytes(64), s>>>(arena, ranks,
+                                                                                            dg.p + gr.start + b0);
+              else
+                k_gemm_mma<32><<<dim3(ceil_div(mt, GM_BM), ceil_div(nt, 32), nb), 256, gm_smem_bytes(32), s>>>(arena, ranks,
+                                                                                            dg.p + gr.start + b0);
+            } else if (wide)
               k_gemm64<<<dim3(ceil_div(mt, GT64), ceil_div(nt, GT64), nb), 256, 0, s>>>(arena, ranks,
                                                                                        dg.p + gr.start + b0);
             else
@@ -1875,6 +2063,9 @@ static void hlu_factor_impl(cbie_hlu* F) {
   }
   key = fnv(key, (int64_t)(F->tol * 1e15));
   key = fnv(key, (int64_t)(getenv("CBIE_POOL_GB") ? atof(getenv("CBIE_POOL_GB")) * 1000 : -1));
+  key = fnv(key, (int64_t)(getenv("CBIE_TMP_CAP_MULT") ? atof(getenv("CBIE_TMP_CAP_MULT")) * 1000 : -1));
+  key = fnv(key, getenv("CBIE_NO_PARPROD") ? 1 : 0);
+  key = fnv(key, getenv("CBIE_LAZY") ? 1 + atoi(getenv("CBIE_LAZY")) : 0);
   const bool use_cache = getenv("CBIE_NO_PLAN_CACHE") == nullptr;
   auto& g_plan_cache = g_plan_caches[c->device];
   auto t0 = std::chrono::steady_clock::now();
@@ -2254,7 +2445,9 @@ int cbie_hlu_dist_plan_host(const double* pts, int64_t npts, int C, int n_leaf, 
           F.npiv += L.m;
         }
       } else {
-        const int r = std::max(1, std::min(L.m, L.n) / 8);
+        // assumed rank: 16 at 192, +8 per doubling of the block side
+        int r = 16;
+        for (int z = 192; z < std::min(L.m, L.n); z *= 2) r += 8;
         L.cap = std::max(1, std::min(std::max(1, std::min(L.m, L.n) / 2), 2 * r + 48));
         L.off_u = leaf_end;
         leaf_end += (int64_t)L.m * L.cap;
@@ -2263,7 +2456,24 @@ int cbie_hlu_dist_plan_host(const double* pts, int64_t npts, int C, int n_leaf, 
       }
     }
     Recorder R;
-    hlu_record(&F, R, leaf_end, (int64_t)1 << 40, true);
+    // debug: CBIE_PLAN_POOL_GB bounds the temporary pool like a device run would
+    const int64_t budget = getenv("CBIE_PLAN_POOL_GB")
+                               ? (int64_t)(atof(getenv("CBIE_PLAN_POOL_GB")) * (double)(1ll << 30)) / (int64_t)sizeof(zc)
+                               : (int64_t)1 << 40;
+    const auto tr0 = std::chrono::steady_clock::now();
+    hlu_record(&F, R, leaf_end, budget, getenv("CBIE_PLAN_NOTRACK") == nullptr);
+    if (getenv("CBIE_MEMLOG"))
+      fprintf(stderr, "[cbie] host plan: recording %.0f ms\n",
+              std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - tr0).count());
+    if (getenv("CBIE_MEMLOG"))
+      fprintf(stderr, "[cbie] host plan: tasks %zu, pool top %.2f GiB, leaf storage %.2f GiB\n", R.tasks.size(),
+              (double)R.pool_top * sizeof(zc) / (double)(1ll << 30), (double)leaf_end * sizeof(zc) / (double)(1ll << 30));
+    if (getenv("CBIE_MEMLOG")) {
+      const char* nm[12] = {"other", "add_concat", "prod_parts", "prod_concat", "prod_out", "gemm_W", "gemm_P",
+                            "dense_to_lr", "collect_concat", "mul_W", "solve_X", ""};
+      for (int i = 0; i < 11; ++i)
+        fprintf(stderr, "[cbie]   temps %-14s %.2f GiB\n", nm[i], (double)R.site_elems[i] * sizeof(zc) / (double)(1ll << 30));
+    }
     DistPlan D;
     dist_plan(R, F, world, D, nullptr, false);
     int64_t fe = 0;

@@ -135,6 +135,103 @@ __global__ void __launch_bounds__(256) k_gemm64(zc* __restrict__ ar, const int* 
     }
 }
 
+// FP64 tensor-core GEMM (mma.sync.m8n8k4.f64, common.cuh zdmma): one 64 x BN output tile
+// per CTA, 8 warps as 4 x 2, each warp a 16 x BN/2 sub-tile of 2 x BN/16 m8n8 blocks.
+// K runs in chunks of 16 through a double-buffered shared staging filled by cp.async (one
+// 16-byte complex per copy, so any view -- transposed or not, any ld -- stages the same
+// way; out-of-range elements are zero-filled by the copy).  The staging is k-major with a
+// row stride = 2 (mod 8) complex: the 8 lanes of a quarter-warp (4 k x 2 rows) then hit 8
+// distinct 16-byte bank groups, so every fragment load is conflict-free.
+constexpr int GM_BM = 64, GM_BK = 16;
+__device__ __forceinline__ void gm_cp16(void* sdst, const void* gsrc, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gsrc), "r"(valid ? 16 : 0) : "memory");
+}
+constexpr size_t gm_smem_bytes(int bn) { return (size_t)2 * GM_BK * (GM_BM + 2 + bn + 2) * sizeof(zc); }
+template <int BN>
+__global__ void __launch_bounds__(256, 2) k_gemm_mma(zc* __restrict__ ar, const int* __restrict__ ranks,
+                                                     const GemmD* __restrict__ ds) {
+  constexpr int LDA = GM_BM + 2, LDB = BN + 2;
+  constexpr int NB = BN / 16;   // m8n8 column blocks per warp
+  const GemmD d = ds[blockIdx.z];
+  const int m = dimv(d.m, ranks), n = dimv(d.n, ranks), k = dimv(d.k, ranks);
+  const int i0 = blockIdx.x * GM_BM, j0 = blockIdx.y * BN;
+  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) flop_add(8.0 * m * n * k);
+  if (i0 >= m || j0 >= n) return;
+  extern __shared__ __align__(16) unsigned char gm_smem[];
+  zc(*sA)[GM_BK * LDA] = reinterpret_cast<zc(*)[GM_BK * LDA]>(gm_smem);
+  zc(*sB)[GM_BK * LDB] = reinterpret_cast<zc(*)[GM_BK * LDB]>(gm_smem + 2 * GM_BK * LDA * sizeof(zc));
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int wm = w & 3, wn = w >> 2;
+  const int fr = lane & 3, fc = lane >> 2;
+  double acc[2][NB][4];
+#pragma unroll
+  for (int a = 0; a < 2; ++a)
+#pragma unroll
+    for (int b = 0; b < NB; ++b) acc[a][b][0] = acc[a][b][1] = acc[a][b][2] = acc[a][b][3] = 0.0;
+  const zc* __restrict__ Ag = ar + d.A.off;
+  const zc* __restrict__ Bg = ar + d.B.off;
+  const int lda = d.A.ld, ldb = d.B.ld, atr = d.A.tr, btr = d.B.tr;
+  const int nch = (k + GM_BK - 1) / GM_BK;
+  auto issue = [&](int c) {
+    if (c < nch) {
+      const int k0 = c * GM_BK;
+      zc* a_s = sA[c & 1];
+      zc* b_s = sB[c & 1];
+      // the index that is contiguous in global memory runs fastest over the threads
+      for (int e = threadIdx.x; e < GM_BK * GM_BM; e += 256) {
+        const int kk = atr ? e % GM_BK : e / GM_BM, ii = atr ? e / GM_BK : e % GM_BM;
+        const int gi = i0 + ii, gk = k0 + kk;
+        const bool ok = gi < m && gk < k;
+        gm_cp16(a_s + kk * LDA + ii, ok ? Ag + (atr ? (int64_t)gi * lda + gk : (int64_t)gk * lda + gi) : Ag, ok);
+      }
+      for (int e = threadIdx.x; e < GM_BK * BN; e += 256) {
+        const int kk = btr ? e / BN : e % GM_BK, jj = btr ? e % BN : e / GM_BK;
+        const int gj = j0 + jj, gk = k0 + kk;
+        const bool ok = gj < n && gk < k;
+        gm_cp16(b_s + kk * LDB + jj, ok ? Bg + (btr ? (int64_t)gk * ldb + gj : (int64_t)gj * ldb + gk) : Bg, ok);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  issue(0);
+  for (int c = 0; c < nch; ++c) {
+    issue(c + 1);
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    const zc* a_s = sA[c & 1] + wm * 16 + fc;
+    const zc* b_s = sB[c & 1] + wn * (BN / 2) + fc;
+#pragma unroll
+    for (int ks = 0; ks < GM_BK / 4; ++ks) {
+      zc a[2], b[NB];
+#pragma unroll
+      for (int q = 0; q < 2; ++q) a[q] = a_s[(ks * 4 + fr) * LDA + q * 8];
+#pragma unroll
+      for (int q = 0; q < NB; ++q) b[q] = b_s[(ks * 4 + fr) * LDB + q * 8];
+#pragma unroll
+      for (int qa = 0; qa < 2; ++qa)
+#pragma unroll
+        for (int qb = 0; qb < NB; ++qb) zdmma(acc[qa][qb], a[qa], b[qb]);
+    }
+    __syncthreads();   // buffer c & 1 is refilled by the next iteration's issue
+  }
+  const bool has_beta = d.beta.x != 0.0 || d.beta.y != 0.0;
+#pragma unroll
+  for (int qa = 0; qa < 2; ++qa)
+#pragma unroll
+    for (int qb = 0; qb < NB; ++qb)
+#pragma unroll
+      for (int j = 0; j < 2; ++j) {
+        const int gi = i0 + wm * 16 + qa * 8 + fc, gj = j0 + wn * (BN / 2) + qb * 8 + 2 * fr + j;
+        if (gi < m && gj < n) {
+          const int64_t o = vidx(d.C, gi, gj);
+          zc v = zmul(d.alpha, zmk(acc[qa][qb][j], acc[qa][qb][2 + j]));
+          if (has_beta) v = zadd(v, zmul(d.beta, ar[o]));
+          ar[o] = v;
+        }
+      }
+}
+
 // matrix x vector (n == 1, the triangular solves with one right-hand side): a CTA takes 32
 // rows, its 8 warps split the inner dimension (lanes = rows: coalesced over a column-major
 // A), partial sums reduced through shared memory in a fixed order

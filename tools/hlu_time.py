@@ -23,5 +23,8 @@ for cfg in [int(a) for a in sys.argv[1:]]:
     res = float(np.linalg.norm(H.matvec(F.solve(b)) - b) / np.linalg.norm(b))
     print(json.dumps({"cfg": cfg, "fill_ms": H.stats()["fill_ms"], "hlu_ms": ts, "residual": res,
                       "overflow": st["trunc_overflow"], "record_ms": st["record_ms"],
-                      "solve_ms": F.stats().get("solve_device_ms")}), flush=True)
+                      "solve_ms": F.stats().get("solve_device_ms"), "levels": st.get("levels"),
+                      "launches": st.get("launches"), "temp_gb": round(st.get("temp_bytes", 0) / 2 ** 30, 1),
+                      "pool_gb": round(st.get("pool_budget_gb", 0), 1),
+                      "tflops": round(st.get("flops", 0) / st["factor_device_ms"] / 1e9, 2)}), flush=True)
     del F, H, gen
