@@ -614,7 +614,8 @@ struct Builder {
   double tmp_cap_mult = getenv("CBIE_TMP_CAP_MULT") ? atof(getenv("CBIE_TMP_CAP_MULT")) : 1.5;
   int tcap(int m, int n) const {
     const int full = std::min(m, n);
-    if (!(tmp_cap_mult > 0.0) || capmax.empty()) return full;
+    // a re-factorisation after a clipped truncation (cap_boost > 1) takes no chances
+    if (!(tmp_cap_mult > 0.0) || capmax.empty() || F.cap_boost > 1) return full;
     const int s = std::max(m, n);
     auto it = capmax.lower_bound(s);
     double c;

@@ -737,6 +737,8 @@ constexpr int GMCH = 32;    // rows per staged chunk
 constexpr int GSLD = 36;    // staging column stride (zc)
 __device__ int g_gram_mma = 1;   // 0: DFMA gram_acc / apply_sel (CBIE_NO_DMMA)
 __device__ int g_ms_min_add = 1;    // multi-stage: fewest new columns per stage (CBIE_MS_MIN_ADD)
+__device__ int g_prof_mn = 0;       // CBIE_PROFILE: only problems with max(m, n) >= this (CBIE_PROF_MN)
+__device__ int g_prof_kmin = 0;     // ... and k >= this (CBIE_PROF_KMIN)
 __device__ int g_pchol_w = NW / 2;   // warps per Gram pivoted Cholesky (CBIE_PCHOL_W)
 __device__ int g_pcholh_w = NW;      // warps of the core pivoted Cholesky (CBIE_PCHOLH_W)
 
@@ -761,6 +763,18 @@ __device__ __noinline__ void gram_acc_mma(const zc* __restrict__ X, int r_lo, in
 #pragma unroll
   for (int q = 0; q < GTPW; ++q) acc[q][0] = acc[q][1] = acc[q][2] = acc[q][3] = 0.0;
   const int nch = (r_hi - r_lo + GMCH - 1) / GMCH;
+  // staging offsets of this warp's tiles (tile t = (ta, b), ta <= b), fixed for the whole
+  // accumulation: decoded once, not per 4-row step; -1: column beyond k (zero operand)
+  int oa[GTPW], ob[GTPW];
+#pragma unroll
+  for (int q = 0; q < GTPW; ++q) {
+    const int t = wi + q * wpr;
+    int b = 0;
+    while ((b + 1) * (b + 2) / 2 <= t) ++b;
+    const int ca = (t - b * (b + 1) / 2) * 8 + fc, cb = b * 8 + fc;
+    oa[q] = (t < nt && ca < k) ? ca * GSLD + fr : -1;
+    ob[q] = (t < nt && cb < k) ? cb * GSLD + fr : -1;
+  }
   auto issue = [&](int c) {
     if (c < nch) {
       const int r0 = r_lo + c * GMCH;
@@ -781,16 +795,12 @@ __device__ __noinline__ void gram_acc_mma(const zc* __restrict__ X, int r_lo, in
     const zc* buf = Xs + (c & 1) * (KG * GSLD);
     const int nst = (min(GMCH, r_hi - r_lo - c * GMCH) + 3) >> 2;
     for (int st = g; st < nst; st += RS) {
-      const int row = 4 * st + fr;
+      const zc* bs = buf + 4 * st;
 #pragma unroll
       for (int q = 0; q < GTPW; ++q) {
-        const int t = wi + q * wpr;
-        if (t >= nt) break;   // warp-uniform
-        int b = 0;
-        while ((b + 1) * (b + 2) / 2 <= t) ++b;
-        const int ca = (t - b * (b + 1) / 2) * 8 + fc, cb = b * 8 + fc;
-        const zc xa = ca < k ? buf[ca * GSLD + row] : zmk(0.0, 0.0);
-        const zc xb = cb < k ? buf[cb * GSLD + row] : zmk(0.0, 0.0);
+        if (wi + q * wpr >= nt) break;   // warp-uniform
+        const zc xa = oa[q] >= 0 ? bs[oa[q]] : zmk(0.0, 0.0);
+        const zc xb = ob[q] >= 0 ? bs[ob[q]] : zmk(0.0, 0.0);
         zdmma_ca(acc[q], xa, xb);
       }
     }
@@ -1535,7 +1545,7 @@ __global__ void __launch_bounds__(NT, 1)
   }
   if (threadIdx.x == 0 && crank == 0) {
     ranks[d.out_slot] = r;
-    if (prof) {
+    if (prof && max(m, n) >= g_prof_mn && k >= g_prof_kmin) {
       const long long tc4 = clock64();
       atomicAdd(prof + 0, (unsigned long long)(tc[1] - tc[0]));
       atomicAdd(prof + 1, (unsigned long long)(tc[2] - tc[1]));
@@ -1564,6 +1574,12 @@ void launch_gram(zc* arena, zc* aout, int* ranks, const TruncDesc* d_desc, int n
   if (scratch.n < need) scratch.alloc(need);
   const int smem = (3 * GSQ + KG + 1) * (int)sizeof(zc);
   CK(cudaFuncSetAttribute(k_trunc_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, smem));
+  if (getenv("CBIE_PROF_MN") || getenv("CBIE_PROF_KMIN")) {
+    const int z = getenv("CBIE_PROF_MN") ? atoi(getenv("CBIE_PROF_MN")) : 0;
+    const int y = getenv("CBIE_PROF_KMIN") ? atoi(getenv("CBIE_PROF_KMIN")) : 0;
+    CK(cudaMemcpyToSymbol(g_prof_mn, &z, sizeof(int)));
+    CK(cudaMemcpyToSymbol(g_prof_kmin, &y, sizeof(int)));
+  }
   if (getenv("CBIE_MS_MIN_ADD")) {
     const int z = std::max(1, atoi(getenv("CBIE_MS_MIN_ADD")));
     CK(cudaMemcpyToSymbol(g_ms_min_add, &z, sizeof(int)));
