@@ -1224,6 +1224,37 @@ __device__ void cluster_gram_sum(zc* G, int k, zc* tmp) {
   __syncthreads();
 }
 
+// Small complex product on the FP64 tensor pipe: C(i, j) = sum_{c < K} A(i, c) B(c, j),
+// i < M, j < N, for the k x k steps of the Gram path (operands in shared or L2-resident
+// global memory, read straight into the m8n8k4 fragments through the functors fa / fb; st
+// stores one entry).  All NW warps; a warp takes 8 x 16 strips (two tiles share the A
+// fragment).  Callers synchronise afterwards.
+template <class FA, class FB, class FS>
+__device__ __forceinline__ void kk_gemm_mma(int M, int N, int K, FA fa, FB fb, FS st) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, fr = lane & 3, fc = lane >> 2;
+  const int tm = (M + 7) >> 3, tn = (N + 15) >> 4;
+  for (int t = w; t < tm * tn; t += NW) {
+    const int i0 = (t % tm) * 8, j0 = (t / tm) * 16;
+    double c0[4] = {0.0, 0.0, 0.0, 0.0}, c1[4] = {0.0, 0.0, 0.0, 0.0};
+    const int i = i0 + fc, ja = j0 + fc, jb = j0 + 8 + fc;
+    for (int k0 = 0; k0 < K; k0 += 4) {
+      const int kk = k0 + fr;
+      const bool kv = kk < K;
+      const zc a = (kv && i < M) ? fa(i, kk) : zmk(0.0, 0.0);
+      const zc b0 = (kv && ja < N) ? fb(kk, ja) : zmk(0.0, 0.0);
+      const zc b1 = (kv && jb < N) ? fb(kk, jb) : zmk(0.0, 0.0);
+      zdmma(c0, a, b0);
+      zdmma(c1, a, b1);
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const int oj = j0 + 2 * fr + j;
+      if (i < M && oj < N) st(i, oj, zmk(c0[j], c0[2 + j]));
+      if (i < M && oj + 8 < N) st(i, oj + 8, zmk(c1[j], c1[2 + j]));
+    }
+  }
+}
+
 // One Gram-path recompression (steps 1-5 above) of U (m x k, ldu) Vt (n x k, ldv),
 // k <= KG: writes Uo (m x r, ld m), Vo (n x r, ld n) and returns r (0: zero product);
 // r is clipped at cap (counted in overflow).  sc: per-CTA scratch (4 GSQ).
@@ -1299,14 +1330,22 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   }
   __syncthreads();
   // 4. core M = (R_u P_u^T)(R_v P_v^T)^T  (ku x kv), kept in global for U' = M Vhat
-  for (int e = threadIdx.x; e < ku * kv; e += NT) {
-    const int a = e % ku, b = e / ku;
-    zc s = zmk(0.0, 0.0);
-    for (int c = 0; c < k; ++c) {
-      const int ju = posu[c], jv = posv[c];
-      if (ju >= a && jv >= b) zfma(s, Gu[ju * k + a], Gv[jv * k + b]);
+  if (g_gram_mma) {
+    kk_gemm_mma(
+        ku, kv, k,
+        [&](int a, int c) { const int ju = posu[c]; return ju >= a ? Gu[ju * k + a] : zmk(0.0, 0.0); },
+        [&](int c, int b) { const int jv = posv[c]; return jv >= b ? Gv[jv * k + b] : zmk(0.0, 0.0); },
+        [&](int a, int b, zc v) { X2[b * ku + a] = v; });
+  } else {
+    for (int e = threadIdx.x; e < ku * kv; e += NT) {
+      const int a = e % ku, b = e / ku;
+      zc s = zmk(0.0, 0.0);
+      for (int c = 0; c < k; ++c) {
+        const int ju = posu[c], jv = posv[c];
+        if (ju >= a && jv >= b) zfma(s, Gu[ju * k + a], Gv[jv * k + b]);
+      }
+      X2[e] = s;
     }
-    X2[e] = s;
   }
   for (int e = threadIdx.x; e < k * k; e += NT) {
     Rug[e] = Gu[e];
@@ -1322,11 +1361,17 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   //    singular vectors: Vhat = M^H W / S^2.  Singular values below ~sqrt(eps) s_0
   //    are not resolved, far below tol * s_0.
   zc* H = Gu;
-  for (int e = threadIdx.x; e < kk1 * kk1; e += NT) {
-    const int a = e % kk1, b = e / kk1;
-    zc s = zmk(0.0, 0.0);
-    for (int c = 0; c < kk2; ++c) zfma(s, X2[c * kk1 + a], zconj(X2[c * kk1 + b]));
-    H[b * kk1 + a] = s;
+  if (g_gram_mma) {
+    kk_gemm_mma(
+        kk1, kk1, kk2, [&](int a, int c) { return X2[c * kk1 + a]; },
+        [&](int c, int b) { return zconj(X2[c * kk1 + b]); }, [&](int a, int b, zc v) { H[b * kk1 + a] = v; });
+  } else {
+    for (int e = threadIdx.x; e < kk1 * kk1; e += NT) {
+      const int a = e % kk1, b = e / kk1;
+      zc s = zmk(0.0, 0.0);
+      for (int c = 0; c < kk2; ++c) zfma(s, X2[c * kk1 + a], zconj(X2[c * kk1 + b]));
+      H[b * kk1 + a] = s;
+    }
   }
   for (int e = threadIdx.x; e < kk1 * kk2; e += NT) Mg[e] = X2[e];
   __syncthreads();
@@ -1365,12 +1410,20 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   } else {
     zc* Gp = Gv;   // R R^H (kp x kp)
     zc* Z = X2;    // eigenvectors (kp x kp)
-    for (int e = threadIdx.x; e < kp * kp; e += NT) {
-      const int a = e % kp, b = e / kp;
-      zc s = zmk(0.0, 0.0);
-      for (int j = max(a, b); j < kk1; ++j) zfma(s, H[j * kk1 + a], zconj(H[j * kk1 + b]));
-      Gp[b * kp + a] = s;
-      Z[b * kp + a] = zmk(a == b ? 1.0 : 0.0, 0.0);
+    if (g_gram_mma) {
+      kk_gemm_mma(
+          kp, kp, kk1, [&](int a, int j) { return j >= a ? H[j * kk1 + a] : zmk(0.0, 0.0); },
+          [&](int j, int b) { return j >= b ? zconj(H[j * kk1 + b]) : zmk(0.0, 0.0); },
+          [&](int a, int b, zc v) { Gp[b * kp + a] = v; });
+      for (int e = threadIdx.x; e < kp * kp; e += NT) Z[e] = zmk(e % kp == e / kp ? 1.0 : 0.0, 0.0);
+    } else {
+      for (int e = threadIdx.x; e < kp * kp; e += NT) {
+        const int a = e % kp, b = e / kp;
+        zc s = zmk(0.0, 0.0);
+        for (int j = max(a, b); j < kk1; ++j) zfma(s, H[j * kk1 + a], zconj(H[j * kk1 + b]));
+        Gp[b * kp + a] = s;
+        Z[b * kp + a] = zmk(a == b ? 1.0 : 0.0, 0.0);
+      }
     }
     __syncthreads();
     stamp(8);
@@ -1408,22 +1461,39 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
     }
   } else {
     const zc* Z = X2;
-    for (int e = threadIdx.x; e < kk1 * r; e += NT) {
-      const int j = e % kk1, l = e / kk1;
-      const int c = S.order[l];
-      zc s = zmk(0.0, 0.0);
-      for (int a = 0; a <= min(j, kp - 1); ++a) zfma(s, zconj(H[j * kk1 + a]), Z[c * kp + a]);
-      W[(int64_t)l * kk1 + S.perm[j]] = s;
+    if (g_gram_mma) {
+      kk_gemm_mma(
+          kk1, r, kp, [&](int j, int a) { return a <= j ? zconj(H[j * kk1 + a]) : zmk(0.0, 0.0); },
+          [&](int a, int l) { return Z[S.order[l] * kp + a]; },
+          [&](int j, int l, zc v) { W[(int64_t)l * kk1 + S.perm[j]] = v; });
+    } else {
+      for (int e = threadIdx.x; e < kk1 * r; e += NT) {
+        const int j = e % kk1, l = e / kk1;
+        const int c = S.order[l];
+        zc s = zmk(0.0, 0.0);
+        for (int a = 0; a <= min(j, kp - 1); ++a) zfma(s, zconj(H[j * kk1 + a]), Z[c * kp + a]);
+        W[(int64_t)l * kk1 + S.perm[j]] = s;
+      }
     }
   }
   __syncthreads();
   // conj(Vhat) = conj(M^H W / S^2) (kk2 x r) to global
-  for (int e = threadIdx.x; e < kk2 * r; e += NT) {
-    const int b = e % kk2, l = e / kk2;
-    const double sg = S.sig[S.order[l]];
-    zc s = zmk(0.0, 0.0);
-    for (int a = 0; a < kk1; ++a) zfma(s, zconj(Mg[b * kk1 + a]), W[(int64_t)l * kk1 + a]);
-    Vhg[(int64_t)l * kk2 + b] = zconj(zscale(s, 1.0 / (sg * sg)));
+  if (g_gram_mma) {
+    kk_gemm_mma(
+        kk2, r, kk1, [&](int b, int a) { return zconj(Mg[b * kk1 + a]); },
+        [&](int a, int l) { return W[(int64_t)l * kk1 + a]; },
+        [&](int b, int l, zc v) {
+          const double sg = S.sig[S.order[l]];
+          Vhg[(int64_t)l * kk2 + b] = zconj(zscale(v, 1.0 / (sg * sg)));
+        });
+  } else {
+    for (int e = threadIdx.x; e < kk2 * r; e += NT) {
+      const int b = e % kk2, l = e / kk2;
+      const double sg = S.sig[S.order[l]];
+      zc s = zmk(0.0, 0.0);
+      for (int a = 0; a < kk1; ++a) zfma(s, zconj(Mg[b * kk1 + a]), W[(int64_t)l * kk1 + a]);
+      Vhg[(int64_t)l * kk2 + b] = zconj(zscale(s, 1.0 / (sg * sg)));
+    }
   }
   for (int j = threadIdx.x; j < kk1; j += NT) scu[j] = alpha[pu[j]];
   for (int j = threadIdx.x; j < kk2; j += NT) scv[j] = ainv[pv[j]];
