@@ -532,11 +532,14 @@ void launch_truncate_routed(zc* arena, int* ranks, const TruncDesc* d_desc, int 
   CK(cudaMemsetAsync(la, 0, sizeof(int) * (2 * nd + 2), s));   // counts of la and lf (and la's payload)
   CK(cudaMemsetAsync(lb, 0, sizeof(int), s));
   CK(cudaMemsetAsync(lg, 0, sizeof(int), s));
-  k_route<<<std::min((nd + 255) / 256, 148), 256, 0, s>>>(ranks, d_desc, nd, kg, la, lb, split ? lg : nullptr,
-                                                          split ? big->nsmall : nd);
+  // multi-stage on: the (rare) problems beyond its 256 columns join the Gram failures'
+  // list and run with them after the Gram launches -- one Householder pass per group
+  // instead of two mostly empty ones
+  k_route<<<std::min((nd + 255) / 256, 148), 256, 0, s>>>(ranks, d_desc, nd, kg, la, multi ? lf : lb,
+                                                          split ? lg : nullptr, split ? big->nsmall : nd);
   CKL();
   cudaEvent_t fork = nullptr, join = nullptr;
-  const bool two = sb != s && kc_max > kg;
+  const bool two = sb != s && kc_max > kg && !multi;
   if (two) {
     CK(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
     CK(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
@@ -549,7 +552,7 @@ void launch_truncate_routed(zc* arena, int* ranks, const TruncDesc* d_desc, int 
     launch_truncate_gram(arena, ranks, d_desc, nd - big->nsmall, tol, overflow, big->work3->scratch, big->s3, aout,
                          multi ? lf : nullptr, lg, multi ? mn_max : 0, big->cbig);
   }
-  if (kc_max > kg)
+  if (kc_max > kg && !multi)
     householder_list(arena, ranks, d_desc, nd, kmax, tol, overflow, two ? wb : work, two ? sb : s, kc_max, mn_max,
                      lb, aout);
   launch_truncate_gram(arena, ranks, d_desc, split ? big->nsmall : nd, tol, overflow, work.scratch, s, aout,

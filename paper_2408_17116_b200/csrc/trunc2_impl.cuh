@@ -1007,23 +1007,46 @@ __device__ int pchol_grp(zc* G, int k, int* perm, double thr_rel, bool trace_sto
 // Z (kk x r, ld kk, shared) <- R11^{-1} Z with R11 = rows/cols 0..kk-1 of R (ld k, upper),
 // then row j scaled by sc[j]; one warp per column, lanes hold rows lane, lane + 32
 __device__ void tri_solve_cols(const zc* R, int k, int kk, zc* Z, int r, const double* sc) {
+  // a warp carries three columns through the back substitution together (the row of R and
+  // the reciprocal pivot are loaded once per step, the three chains interleave)
+  __shared__ double dinv[KG];
+  constexpr int NC = 3;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int l = w; l < r; l += NW) {
-    zc* z = Z + (int64_t)l * kk;
-    zc x0 = lane < kk ? z[lane] : zmk(0.0, 0.0);
-    zc x1 = lane + 32 < kk ? z[lane + 32] : zmk(0.0, 0.0);
-    for (int a = kk - 1; a >= 0; --a) {
-      const zc own = a >= 32 ? x1 : x0;
-      const zc xa = zscale(zshfl(own, a & 31), 1.0 / R[a * k + a].x);
-      if (lane == (a & 31)) {
-        if (a >= 32) x1 = xa;
-        else x0 = xa;
-      }
-      if (lane < a) x0 = zsub(x0, zmul(R[a * k + lane], xa));
-      if (lane + 32 < a) x1 = zsub(x1, zmul(R[a * k + lane + 32], xa));
+  for (int a = threadIdx.x; a < kk; a += NT) dinv[a] = 1.0 / R[a * k + a].x;
+  __syncthreads();
+  for (int l0 = w; l0 < r; l0 += NW * NC) {
+    zc x0[NC], x1[NC];
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int l = l0 + c * NW;
+      const zc* z = Z + (int64_t)l * kk;
+      x0[c] = (l < r && lane < kk) ? z[lane] : zmk(0.0, 0.0);
+      x1[c] = (l < r && lane + 32 < kk) ? z[lane + 32] : zmk(0.0, 0.0);
     }
-    if (lane < kk) z[lane] = zscale(x0, sc[lane]);
-    if (lane + 32 < kk) z[lane + 32] = zscale(x1, sc[lane + 32]);
+    for (int a = kk - 1; a >= 0; --a) {
+      const zc ra0 = lane < a ? R[a * k + lane] : zmk(0.0, 0.0);
+      const zc ra1 = lane + 32 < a ? R[a * k + lane + 32] : zmk(0.0, 0.0);
+      const double di = dinv[a];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) {
+        const zc own = a >= 32 ? x1[c] : x0[c];
+        const zc xa = zscale(zshfl(own, a & 31), di);
+        if (lane == (a & 31)) {
+          if (a >= 32) x1[c] = xa;
+          else x0[c] = xa;
+        }
+        x0[c] = zsub(x0[c], zmul(ra0, xa));
+        x1[c] = zsub(x1[c], zmul(ra1, xa));
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < NC; ++c) {
+      const int l = l0 + c * NW;
+      if (l >= r) continue;
+      zc* z = Z + (int64_t)l * kk;
+      if (lane < kk) z[lane] = zscale(x0[c], sc[lane]);
+      if (lane + 32 < kk) z[lane + 32] = zscale(x1[c], sc[lane + 32]);
+    }
   }
   __syncthreads();
 }
