@@ -123,7 +123,15 @@ struct Recorder {
   // free lists per size class: (offset, buffer id)
   // (keyed by the level of the chunk's last access: reuse takes the chunk that was done
   // EARLIEST in the schedule, so the new owner waits as little as possible)
-  std::map<int, std::multimap<int, std::pair<int64_t, int>>> freel;
+  struct FreeChunk {
+    int level;
+    int64_t seq, off;
+    int buf;
+    bool operator<(const FreeChunk& o) const {   // min-heap on (level, seq) through std::push_heap
+      return level != o.level ? level > o.level : seq > o.seq;
+    }
+  };
+  std::vector<std::vector<FreeChunk>> freel;   // indexed by size class
   bool reuse_oldest = getenv("CBIE_REUSE_OLDEST") != nullptr;   // A/B knob: tape order (round 1)
   int64_t free_seq = 0;
   std::vector<int> init_ranks;   // initial values of every rank slot
@@ -173,6 +181,7 @@ struct Recorder {
   std::vector<GemmD> gemm;
   std::vector<EwD> ew;
   std::vector<ConcatD> cat;
+  std::vector<Piece> cat_pieces;   // piece pool of the concatenations (ConcatD::p0)
   std::vector<TrsmD> trsm;
   std::vector<GetrfD> getrf;
   std::vector<TruncDesc> trunc;
@@ -295,9 +304,15 @@ struct Recorder {
     }
   }
   void accs_of(const Mat& m, AccList& v) const {
-    v.push_back(acc(m));
-    if (m.rslot >= 0 && slot_owner[m.rslot] >= 0) v.push_back(whole(slot_owner[m.rslot]));
-    if (m.cslot >= 0 && slot_owner[m.cslot] >= 0) v.push_back(whole(slot_owner[m.cslot]));
+    // data rectangle + the buffers owning its dynamic dimensions; a whole-buffer access of
+    // the matrix's own buffer already covers the rectangle (same dependencies, half the
+    // entries to scan and to keep)
+    const int o1 = m.rslot >= 0 ? slot_owner[m.rslot] : -1;
+    const int o2 = m.cslot >= 0 ? slot_owner[m.cslot] : -1;
+    if (o1 == m.buf || o2 == m.buf) v.push_back(whole(m.buf));
+    else v.push_back(acc(m));
+    if (o1 >= 0 && o1 != m.buf) v.push_back(whole(o1));
+    if (o2 >= 0 && o2 != m.buf && o2 != o1) v.push_back(whole(o2));
   }
   std::vector<int> slot_owner;
   int new_slot(int v0, int owner = -1) {
@@ -380,21 +395,21 @@ struct Recorder {
       // free chunks of this class and of the next three (< 2x the size): the one whose last
       // access has the lowest level
       int best = -1, blvl = INT32_MAX;
-      for (int c = cls; c < cls + 4; ++c) {
-        auto it = freel.find(c);
-        if (it == freel.end() || it->second.empty()) continue;
-        if (it->second.begin()->first < blvl) {
-          blvl = it->second.begin()->first;
+      for (int c = cls; c < cls + 4 && c < (int)freel.size(); ++c) {
+        if (freel[c].empty()) continue;
+        if (freel[c].front().level < blvl) {
+          blvl = freel[c].front().level;
           best = c;
         }
       }
       if (best >= 0) {
         auto& fl = freel[best];
-        auto pr = fl.begin()->second;
-        fl.erase(fl.begin());
-        collapse_reuse(pr.second);   // new owner: every earlier access conflicts
-        if (track) reuse_at.push_back({(int)tasks.size(), pr.second});
-        return Tmp{pr.first, best, pr.second};
+        std::pop_heap(fl.begin(), fl.end());
+        const FreeChunk pr = fl.back();
+        fl.pop_back();
+        collapse_reuse(pr.buf);   // new owner: every earlier access conflicts
+        if (track) reuse_at.push_back({(int)tasks.size(), pr.buf});
+        return Tmp{pr.off, best, pr.buf};
       }
     }
     Tmp t{leaf_end + pool_top, cls, new_buf()};
@@ -410,8 +425,10 @@ struct Recorder {
     const Tmp& t = live[buf];
     int lvl = 0;
     for (auto& e : ent[buf]) lvl = std::max(lvl, e.level);
-    freel[t.cls].emplace(reuse_oldest ? (int)std::min<int64_t>(free_seq++, INT32_MAX) : lvl,
-                         std::make_pair(t.off, t.buf));
+    if ((int)freel.size() <= t.cls) freel.resize(t.cls + 1);
+    auto& fl = freel[t.cls];
+    fl.push_back(FreeChunk{reuse_oldest ? 0 : lvl, free_seq++, t.off, t.buf});
+    std::push_heap(fl.begin(), fl.end());
   }
 
   Mat tmp_mat(int rows, int cols, int rslot, int cslot, std::vector<Tmp>& owned) {
@@ -509,7 +526,8 @@ struct Recorder {
     d.rows = rows;
     d.out_slot = out_slot;
     d.np = (int)ps.size();
-    for (int i = 0; i < d.np; ++i) d.p[i] = ps[i];
+    d.p0 = (int)cat_pieces.size();
+    cat_pieces.insert(cat_pieces.end(), ps.begin(), ps.end());
     cat.push_back(d);
     AccList rd;
     if (srcmats) {
@@ -1308,6 +1326,7 @@ struct Plan {
   DBuf<GemmD> dg;
   DBuf<EwD> de;
   DBuf<ConcatD> dc;
+  DBuf<Piece> dcp;   // piece pool of the concatenations
   DBuf<TrsmD> dt;
   DBuf<GetrfD> df;
   DBuf<TruncDesc> dtr;
@@ -1444,6 +1463,7 @@ void make_plan(Plan& P, cudaStream_t s, const Recorder* Rx = nullptr, const std:
   P.dg.upload(g, s);
   P.de.upload(e, s);
   P.dc.upload(c, s);
+  P.dcp.upload(R.cat_pieces, s);
   P.dt.upload(t, s);
   P.df.upload(f, s);
   P.dtr.upload(tr, s);
@@ -1648,7 +1668,7 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
       case OP_CONCAT: {
         for (int b0 = 0; b0 < gr.count; b0 += 65535) {
           int nb = std::min(65535, gr.count - b0);
-          k_concat<<<dim3(8, nb), 256, 0, s>>>(arena, ranks, dc.p + gr.start + b0);
+          k_concat<<<dim3(8, nb), 256, 0, s>>>(arena, ranks, dc.p + gr.start + b0, P.dcp.p);
         }
         break;
       }

@@ -295,12 +295,13 @@ struct Piece {
   zc scale;
 };
 constexpr int MAX_PIECES = 16;
-struct ConcatD {
+struct ConcatD {   // the pieces live in one pool shared by all concatenations of a plan
   int64_t dst;
   int rows, out_slot, np;
-  Piece p[MAX_PIECES];
+  int p0;          // first piece in the pool
 };
-__global__ void k_concat(zc* __restrict__ ar, int* __restrict__ ranks, const ConcatD* __restrict__ ds) {
+__global__ void k_concat(zc* __restrict__ ar, int* __restrict__ ranks, const ConcatD* __restrict__ ds,
+                         const Piece* __restrict__ pool) {
   // descriptor and column offsets staged once per CTA in shared memory (a per-thread
   // copy of the 800-byte descriptor, indexed by piece, went to local memory)
   __shared__ Piece sp[MAX_PIECES];
@@ -316,7 +317,7 @@ __global__ void k_concat(zc* __restrict__ ar, int* __restrict__ ranks, const Con
   }
   __syncthreads();
   const int np = snp, rows = srows;
-  for (int q = threadIdx.x; q < np; q += blockDim.x) sp[q] = dp->p[q];
+  for (int q = threadIdx.x; q < np; q += blockDim.x) sp[q] = pool[dp->p0 + q];
   __syncthreads();
   if (threadIdx.x == 0) {
     c0[0] = 0;
