@@ -560,6 +560,22 @@ struct Recorder {
     reads_of(P, rd);
     add(OP_DLR, (int)dlr.size() - 1, rd, {o.buf});
   }
+  // two-source recompression: reads the pieces (A1, B1), (A2, B2) in place, writes wr
+  void op_trunc2(const TruncDesc& d, int kmax, const Mat& A1, const Mat& B1, const Mat& A2, const Mat& B2,
+                 int wrbuf) {
+    trunc.push_back(d);
+    trunc_kmax.push_back(kmax);
+    ++trunc_count;
+    AccList rd, wr;
+    accs_of(A1, rd);
+    accs_of(B1, rd);
+    accs_of(A2, rd);
+    accs_of(B2, rd);
+    rd.push_back(whole(wrbuf));
+    if (d.skip_slot >= 0 && slot_owner[d.skip_slot] >= 0) rd.push_back(whole(slot_owner[d.skip_slot]));
+    wr.push_back(whole(wrbuf));
+    addA(OP_TRUNC, (int)trunc.size() - 1, rd, wr);
+  }
   void op_trunc(const TruncDesc& d, int kmax, int rdbuf, int rdbuf2, int wrbuf) {
     trunc.push_back(d);
     trunc_kmax.push_back(kmax);
@@ -737,6 +753,16 @@ struct Builder {
   void flush_into(const LR& Tg, Pend& p) {
     if (p.U.empty()) return;
     const int m = Tg.U.rows, n = Tg.Vt.rows;
+    if (p.U.size() == 2 && p.sign[0].x == 1.0 && p.sign[0].y == 0.0 &&
+        two_ok(p.U[0], p.Vt[0], p.U[1], p.Vt[1], m, n, p.sign[1])) {
+      trunc_two(Tg, p.U[0], p.Vt[0], p.U[1], p.Vt[1], p.sign[1], -1);
+      for (size_t i = 0; i < p.U.size(); ++i) {
+        R.release_buf(p.U[i].buf);
+        R.release_buf(p.Vt[i].buf);
+      }
+      p = Pend();
+      return;
+    }
     const int kc = p.capsum;
     R.site = 8;
     Recorder::Tmp t = R.alloc((int64_t)(m + n) * kc);
@@ -919,9 +945,59 @@ struct Builder {
   // ---- low-rank targets ----------------------------------------------------------------
   // target = generic low-rank storage (leaf or temporary)
   // T += sign U V^T-form (U m x r, Vt n x r) with truncation (hmatrix.py:535-554)
+  // Two-source recompression (TruncDesc::in_u2, CBIE_TWO_SOURCE=1): the target and the update
+  // are read in place by the Gram kernel, no concatenation is materialised -- the
+  // concatenation buffers are more than half of the temporaries the pool has to recycle
+  // (config 2: 34 GB of temporaries instead of 75 GB; config 4: 1,771 levels instead of
+  // 2,270, 8.4k launches instead of 12.2k).  Off by default: on config 4 the shallower
+  // schedule is SLOWER (3.02 s vs 2.78 s) -- its recompression groups are larger and more
+  // uneven, and fewer independent groups of neighbouring levels overlap on the three lanes.
+  // Only on the Gram path (tol >= 1e-5, tensor-pipe staging) and on the first attempt: a
+  // problem the Gram path would hand to the Householder kernels is counted as a clipped
+  // truncation and the factorisation is redone with concatenations (cap_boost > 1).
+  bool two_src = getenv("CBIE_TWO_SOURCE") != nullptr && getenv("CBIE_NO_GRAM") == nullptr &&
+                 getenv("CBIE_NO_DMMA") == nullptr && getenv("CBIE_NO_MULTISTAGE") == nullptr;
+  static bool plain(const Mat& a, int rows) { return a.tr == 0 && a.rows == rows; }
+  bool two_ok(const Mat& A1, const Mat& B1, const Mat& A2, const Mat& B2, int m, int n, zc sign) const {
+    return two_src && R.tol >= 1e-5 && F.cap_boost == 1 && plain(A1, m) && plain(A2, m) && plain(B1, n) &&
+           plain(B2, n) && sign.y == 0.0;
+  }
+  // (A1, B1) + sign (A2, B2) -> truncated into Tg (which may be piece 1 itself)
+  void trunc_two(const LR& Tg, const Mat& A1, const Mat& B1, const Mat& A2, const Mat& B2, zc sign, int skip_slot) {
+    const int m = Tg.U.rows, n = Tg.Vt.rows;
+    TruncDesc d;
+    d.in_u = A1.off;
+    d.in_v = B1.off;
+    d.ldu = A1.ld;
+    d.ldv = B1.ld;
+    d.in_u2 = A2.off;
+    d.in_v2 = B2.off;
+    d.ldu2 = A2.ld;
+    d.ldv2 = B2.ld;
+    d.k1 = A1.cols;
+    d.k1_slot = A1.cslot;
+    d.k2 = A2.cols;
+    d.k2_slot = A2.cslot;
+    d.sgn2 = sign.x;
+    d.out_u = Tg.U.off;
+    d.out_v = Tg.Vt.off;
+    d.m = m;
+    d.n = n;
+    d.k = A1.cols + A2.cols;
+    d.k_slot = -1;
+    d.cap = Tg.cap;
+    d.out_slot = Tg.slot;
+    d.skip_slot = skip_slot;
+    R.op_trunc2(d, std::min(d.k, std::max(m, n)), A1, B1, A2, B2, Tg.buf);
+    R.flops += trunc_flops(m, n, d.k);
+  }
   void add_lr_to(const LR& Tg, const Mat& U, const Mat& Vt, zc sign) {
     const int m = Tg.U.rows, n = Tg.Vt.rows;
     if (U.cols == 0) return;
+    if (two_ok(Tg.U, Tg.Vt, U, Vt, m, n, sign)) {
+      trunc_two(Tg, Tg.U, Tg.Vt, U, Vt, sign, U.cslot);
+      return;
+    }
     std::vector<Recorder::Tmp> own;
     const int kc = Tg.cap + U.cols;
     R.site = 1;
@@ -1421,13 +1497,30 @@ void make_plan(Plan& P, cudaStream_t s, const Recorder* Rx = nullptr, const std:
           if (mn > TRUNC_MN_SMALL) mnb = std::max(mnb, mn);
           else mns = std::max(mns, mn);
         }
+        // the largest cluster size whose nb clusters are co-resident (the occupancy query
+        // knows the GPC limits: 32 clusters of 4, not 37) beside up to 74 small problems
         int cb = 1;
         const int useful = std::min(8, (mnb + 191) / 192);
-        while (nb > 0 && 2 * cb <= useful && 2 * cb * nb + std::min(ns, 74) <= 148) cb *= 2;
+        auto fits = [&](int c) {
+          const int cap = truncate_gram_max_clusters(c);
+          const int room = cap > 0 ? cap - (std::min(ns, 74) + c - 1) / c : (148 - std::min(ns, 74)) / c;
+          return nb <= room;
+        };
+        while (nb > 0 && 2 * cb <= useful && fits(2 * cb)) cb *= 2;
         if (nb > 0 && cb > 1) {
           gr.nsmall = ns;
           gr.cbig = cb;
           gr.mn_small = mns;
+        }
+        // launch order = descriptor order: largest blocks first within each launch (the
+        // long problems start first, the short ones fill the SMs behind them); the routed
+        // launches reorder again by the device-side ranks (k_route)
+        auto heavier = [](const TruncDesc& x, const TruncDesc& y) { return x.m + x.n > y.m + y.n; };
+        if (gr.nsmall >= 0) {
+          std::stable_sort(b, b + ns, heavier);
+          std::stable_sort(b + ns, e, heavier);
+        } else {
+          std::stable_sort(b, e, heavier);
         }
       }
     }
@@ -2086,6 +2179,8 @@ static void hlu_factor_impl(cbie_hlu* F) {
   key = fnv(key, (int64_t)(getenv("CBIE_POOL_GB") ? atof(getenv("CBIE_POOL_GB")) * 1000 : -1));
   key = fnv(key, (int64_t)(getenv("CBIE_TMP_CAP_MULT") ? atof(getenv("CBIE_TMP_CAP_MULT")) * 1000 : -1));
   key = fnv(key, getenv("CBIE_NO_PARPROD") ? 1 : 0);
+  key = fnv(key, getenv("CBIE_TWO_SOURCE") ? 1 : 0);
+  key = fnv(key, F->cap_boost);
   key = fnv(key, getenv("CBIE_LAZY") ? 1 + atoi(getenv("CBIE_LAZY")) : 0);
   const bool use_cache = getenv("CBIE_NO_PLAN_CACHE") == nullptr;
   auto& g_plan_cache = g_plan_caches[c->device];
@@ -2189,8 +2284,10 @@ static void hlu_factor_impl(cbie_hlu* F) {
     int nexec = 0;
     for (auto& d : R.trunc) {
       if (d.skip_slot >= 0 && rk[d.skip_slot] == 0) continue;
-      const double k = d.k_slot >= 0 ? rk[d.k_slot] : d.k;
       const double r = rk[d.out_slot];
+      // (two-source: piece 1's slot is the output's, overwritten by r -- its rank is taken as r)
+      const double k = d.in_u2 >= 0 ? r + (d.k2_slot >= 0 ? rk[d.k2_slot] : d.k2)
+                                    : (d.k_slot >= 0 ? rk[d.k_slot] : d.k);
       bytes += 16.0 * (d.m + d.n) * (4.0 * k + r);
       const int kb = k <= 16 ? 0 : k <= 32 ? 1 : k <= 64 ? 2 : k <= 128 ? 3 : k <= 256 ? 4 : 5;
       hist[kb]++;

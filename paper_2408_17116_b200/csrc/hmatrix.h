@@ -99,7 +99,25 @@ struct TruncDesc {
   int k_slot;                  // >= 0: k = ranks[k_slot] (device-resident)
   int cap;                     // output capacity (columns)
   int out_slot;                // ranks[out_slot] <- r
+  // Two-source form (in_u2 >= 0; Gram path only): the input is [piece 1 | sgn2 * piece 2]
+  // read in place -- columns [0, k1) from in_u / in_v, columns [k1, k1 + k2) from in_u2 /
+  // in_v2 -- instead of a materialised concatenation; k = k1 + k2 with k1 = ranks[k1_slot]
+  // (k1 if the slot is < 0), k2 likewise.  The output may overwrite piece 1 (T += s U V^H).
+  int64_t in_u2 = -1, in_v2 = -1;
+  int ldu2 = 0, ldv2 = 0;
+  int k1 = 0, k1_slot = -1, k2 = 0, k2_slot = -1;
+  double sgn2 = 1.0;
 };
+// concatenated rank of a descriptor on the device
+#ifdef __CUDACC__
+__device__ __forceinline__ int trunc_k1(const TruncDesc& d, const int* ranks) {
+  return d.k1_slot >= 0 ? ranks[d.k1_slot] : d.k1;
+}
+__device__ __forceinline__ int trunc_k(const TruncDesc& d, const int* ranks) {
+  if (d.in_u2 >= 0) return trunc_k1(d, ranks) + (d.k2_slot >= 0 ? ranks[d.k2_slot] : d.k2);
+  return d.k_slot >= 0 ? ranks[d.k_slot] : d.k;
+}
+#endif
 // kmax >= every min(m,k), min(n,k) (dense mode: min(m,n) and n) in the batch
 // kc_max / mn_max: largest concatenated capacity and max(m, n) (randomized-path scratch);
 // arena_out (if non-null) receives the outputs (out_u / out_v offsets are relative to it)
@@ -139,6 +157,7 @@ void launch_truncate_routed(zc* arena, int* ranks, const TruncDesc* d_desc, int 
                             unsigned long long* overflow, TruncWork& work, cudaStream_t s, int kc_max,
                             int mn_max, TruncWork* work2 = nullptr, cudaStream_t s2 = nullptr,
                             zc* arena_out = nullptr, const TruncBig* big = nullptr);
+int truncate_gram_max_clusters(int csize);
 void launch_truncate_gram(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, double tol,
                           unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, zc* arena_out,
                           int* defer, const int* idx = nullptr, int mn_multi = 0, int csize = 1);

@@ -442,15 +442,57 @@ static void launch_unblocked_list(zc* arena, zc* arena_out, int* ranks, const Tr
 namespace {
 // split problems by device-side rank: k <= kg (and no-ops) -> la (Gram kernel), the rest -> lb
 // (i >= nsmall: Gram problems of the large blocks -> lg, when lg != nullptr)
-__global__ void k_route(const int* __restrict__ ranks, const TruncDesc* __restrict__ ds, int nd, int kg, int* la,
-                        int* lb, int* lg, int nsmall) {
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < nd; i += gridDim.x * blockDim.x) {
+// One CTA: the Gram lists (la, lg) come out ordered by estimated cost, heaviest first
+// (counting sort over RB cost buckets), so the long problems of a launch start first and
+// the short ones fill the SMs behind them; with arrival order a multi-stage 1536-row
+// problem could start in the last wave and the whole group waited for it.
+constexpr int RB = 16;
+__global__ void __launch_bounds__(256) k_route(const int* __restrict__ ranks, const TruncDesc* __restrict__ ds, int nd,
+                                               int kg, int* la, int* lb, int* lg, int nsmall,
+                                               unsigned long long* overflow) {
+  __shared__ int cnt[2][RB], pos[2][RB];
+  for (int e = threadIdx.x; e < 2 * RB; e += blockDim.x) (&cnt[0][0])[e] = 0;
+  __syncthreads();
+  auto classify = [&](int i, int& list, int& bucket) {
     const TruncDesc& d = ds[i];
-    const int k = d.k_slot >= 0 ? ranks[d.k_slot] : d.k;
+    const int k = trunc_k(d, ranks);
     const bool skip = d.skip_slot >= 0 && ranks[d.skip_slot] == 0;
     if (skip || k <= kg) {
-      int* l = (lg && i >= nsmall) ? lg : la;
-      l[1 + atomicAdd(l, 1)] = i;
+      list = (lg && i >= nsmall) ? 1 : 0;
+      // ~ stages x (k x k work + row streams): k = 64, m + n = 3072 -> 128
+      const int cost = skip ? 0 : ((k + 15) / 16) * ((d.m + d.n) / 128 + 8);
+      bucket = RB - 1 - min(RB - 1, cost / 16);
+    } else {
+      list = d.in_u2 >= 0 ? 3 : 2;
+      bucket = 0;
+    }
+  };
+  for (int i = threadIdx.x; i < nd; i += blockDim.x) {
+    int l, b;
+    classify(i, l, b);
+    if (l < 2) atomicAdd(&cnt[l][b], 1);
+  }
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    int acc = 0;
+    for (int b = 0; b < RB; ++b) {
+      pos[threadIdx.x][b] = acc;
+      acc += cnt[threadIdx.x][b];
+    }
+    int* l = threadIdx.x == 0 ? la : lg;
+    if (l) l[0] = acc;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < nd; i += blockDim.x) {
+    int l, b;
+    classify(i, l, b);
+    if (l < 2) {
+      int* dst = l == 0 ? la : lg;
+      dst[1 + atomicAdd(&pos[l][b], 1)] = i;
+    } else if (l == 3) {
+      // two-source inputs exist only for the Gram path: counted as a clipped truncation, the
+      // factorisation is redone with materialised concatenations (cbie_hlu_factor)
+      atomicAdd(overflow, 1ull);
     } else {
       lb[1 + atomicAdd(lb, 1)] = i;
     }
@@ -535,8 +577,8 @@ void launch_truncate_routed(zc* arena, int* ranks, const TruncDesc* d_desc, int 
   // multi-stage on: the (rare) problems beyond its 256 columns join the Gram failures'
   // list and run with them after the Gram launches -- one Householder pass per group
   // instead of two mostly empty ones
-  k_route<<<std::min((nd + 255) / 256, 148), 256, 0, s>>>(ranks, d_desc, nd, kg, la, multi ? lf : lb,
-                                                          split ? lg : nullptr, split ? big->nsmall : nd);
+  k_route<<<1, 256, 0, s>>>(ranks, d_desc, nd, kg, la, multi ? lf : lb,
+                                                          split ? lg : nullptr, split ? big->nsmall : nd, overflow);
   CKL();
   cudaEvent_t fork = nullptr, join = nullptr;
   const bool two = sb != s && kc_max > kg && !multi;

@@ -60,6 +60,14 @@ void launch_truncate_gram(zc* arena, int* ranks, const TruncDesc* d_desc, int nd
                    g_trunc_prof, defer, idx, mn_multi, csize);
 }
 
+// co-resident clusters of the Gram kernel per cluster size (cached per process; 0 = unknown)
+int truncate_gram_max_clusters(int csize) {
+  static int cache[9] = {-1, -1, -1, -1, -1, -1, -1, -1, -1};
+  if (csize < 1 || csize > 8) return 0;
+  if (cache[csize] < 0) cache[csize] = csize == 1 ? 148 : t2b::gram_max_clusters(csize);
+  return cache[csize];
+}
+
 bool launch_truncate_blocked(zc* arena, int* ranks, const TruncDesc* d_desc, int nd, double tol,
                              unsigned long long* overflow, DBuf<zc>& scratch, cudaStream_t s, int kc_max,
                              int mn_max, zc* arena_out, int* defer, const int* idx) {

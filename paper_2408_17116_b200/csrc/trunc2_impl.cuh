@@ -450,7 +450,7 @@ __global__ void __launch_bounds__(NT, T2_MINB)
   const TruncDesc d = descs[tix];
   const long long tc0 = clock64();
   if (d.skip_slot >= 0 && ranks[d.skip_slot] == 0) return;
-  const int k = d.k_slot >= 0 ? ranks[d.k_slot] : d.k;
+  const int k = trunc_k(d, ranks);
   const int m = d.m, n = d.n;
   if (k <= 0 || m == 0 || n == 0) {
     if (threadIdx.x == 0) ranks[d.out_slot] = 0;
@@ -750,8 +750,19 @@ __device__ __forceinline__ void cp_async16(void* sdst, const void* gsrc, bool va
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait1() { asm volatile("cp.async.wait_group 1;" ::: "memory"); }
 
-__device__ __noinline__ void gram_acc_mma(const zc* __restrict__ X, int r_lo, int r_hi, int k, int ldx, zc* G,
-                                          zc* Xs) {
+// A factor read in place from up to two pieces: columns [0, k1) from p1 (ld1), the
+// columns from k1 on from p2 (ld2) -- TruncDesc's two-source form; one piece: k1 = INT_MAX
+struct Src2 {
+  const zc* p1;
+  const zc* p2;
+  int ld1, ld2, k1;
+  __device__ __forceinline__ const zc* col(int c) const {
+    return c < k1 ? p1 + (int64_t)c * ld1 : p2 + (int64_t)(c - k1) * ld2;
+  }
+};
+__device__ __forceinline__ Src2 src1(const zc* p, int ld) { return Src2{p, p, ld, ld, 0x7fffffff}; }
+
+__device__ __noinline__ void gram_acc_mma(const Src2 X, int r_lo, int r_hi, int k, zc* G, zc* Xs) {
   const int nb = (k + 7) >> 3, nt = nb * (nb + 1) / 2;
   int RS = min(NW, GMCH / 4);
   while (RS > 1 && (nt + NW / RS - 1) / (NW / RS) > GTPW) RS >>= 1;
@@ -775,15 +786,25 @@ __device__ __noinline__ void gram_acc_mma(const zc* __restrict__ X, int r_lo, in
     oa[q] = (t < nt && ca < k) ? ca * GSLD + fr : -1;
     ob[q] = (t < nt && cb < k) ? cb * GSLD + fr : -1;
   }
+  // staging: a thread copies row (tid % GMCH) of columns tid / GMCH + i NT / GMCH of every
+  // chunk -- the column pointers (either piece) are resolved once
+  constexpr int NI = KG * GMCH / NT;
+  static_assert(NT % GMCH == 0 && NI * NT == KG * GMCH, "staging layout");
+  const int sr = threadIdx.x % GMCH;
+  const zc* cp[NI];
+#pragma unroll
+  for (int i = 0; i < NI; ++i) {
+    const int col = threadIdx.x / GMCH + i * (NT / GMCH);
+    cp[i] = col < k ? X.col(col) + sr : nullptr;
+  }
   auto issue = [&](int c) {
     if (c < nch) {
       const int r0 = r_lo + c * GMCH;
-      zc* buf = Xs + (c & 1) * (KG * GSLD);
-      for (int e = threadIdx.x; e < GMCH * k; e += NT) {
-        const int r = e % GMCH, col = e / GMCH;
-        const bool ok = r0 + r < r_hi;
-        cp_async16(buf + col * GSLD + r, ok ? X + (int64_t)col * ldx + r0 + r : X, ok);
-      }
+      zc* buf = Xs + (c & 1) * (KG * GSLD) + (threadIdx.x / GMCH) * GSLD + sr;
+      const bool ok = r0 + sr < r_hi;
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+        if (cp[i]) cp_async16(buf + i * (NT / GMCH) * GSLD, ok ? cp[i] + r0 : X.p1, ok);
     }
     cp_async_commit();
   };
@@ -1081,8 +1102,8 @@ __device__ void apply_sel(const zc* __restrict__ X, int mo, int ldx, int i_lo, i
 // inner dimension (kk <= 64: 16 four-column steps) are loaded up front (gathered columns
 // perm[j] of X, 8 consecutive rows per column), then every 8-column block of O is one
 // chain of 4 DMMA per step against T's fragments in shared memory.
-__device__ __noinline__ void apply_sel_mma(const zc* __restrict__ X, int mo, int ldx, int i_lo, int i_hi, const int* perm,
-                              int kk, const zc* T, int r, zc* __restrict__ O) {
+__device__ __noinline__ void apply_sel_mma(const Src2 X, int mo, int i_lo, int i_hi, const int* perm, int kk,
+                                           const zc* T, int r, zc* O) {
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int fr = lane >> 2, fk = lane & 3;
   const int nrb = (i_hi - i_lo + 7) >> 3, nks = (kk + 3) >> 2, ncb = (r + 7) >> 3;
@@ -1092,7 +1113,7 @@ __device__ __noinline__ void apply_sel_mma(const zc* __restrict__ X, int mo, int
 #pragma unroll
     for (int s = 0; s < KG / 4; ++s) {
       const int j = 4 * s + fk;
-      a[s] = (s < nks && j < kk && i < i_hi) ? X[(int64_t)perm[j] * ldx + i] : zmk(0.0, 0.0);
+      a[s] = (s < nks && j < kk && i < i_hi) ? X.col(perm[j])[i] : zmk(0.0, 0.0);
     }
     for (int cb = 0; cb < ncb; ++cb) {
       double c[4] = {0.0, 0.0, 0.0, 0.0};
@@ -1281,9 +1302,15 @@ __device__ __forceinline__ void kk_gemm_mma(int M, int N, int K, FA fa, FB fb, F
 // One Gram-path recompression (steps 1-5 above) of U (m x k, ldu) Vt (n x k, ldv),
 // k <= KG: writes Uo (m x r, ld m), Vo (n x r, ld n) and returns r (0: zero product);
 // r is clipped at cap (counted in overflow).  sc: per-CTA scratch (4 GSQ).
-__device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restrict__ Vt, int ldv, int m, int n,
-                          int k, zc* __restrict__ Uo, zc* __restrict__ Vo, int cap, double tol, zc* sc,
-                          unsigned long long* overflow, Smem& S, zc* sm, long long* tc, int* sweeps_out) {
+// su / sv: the factors (possibly two pieces each, read in place; Uo / Vo may overwrite the
+// first pieces: every row block is loaded completely before its output rows are stored);
+// the U columns from ksgn on carry the factor sgn (folded into the column balancing).
+__device__ int gram_stage(const Src2 su, const Src2 sv, int ksgn, double sgn, int m, int n, int k, zc* Uo, zc* Vo,
+                          int cap, double tol, zc* sc, unsigned long long* overflow, Smem& S, zc* sm,
+                          long long* tc, int* sweeps_out) {
+  const zc* U = su.p1;
+  const zc* Vt = sv.p1;
+  const int ldu = su.ld1, ldv = sv.ld1;
   __shared__ double alpha[KG], ainv[KG], scu[KG], scv[KG];
   __shared__ int pu[KG], pv[KG], posu[KG], posv[KG];
   zc* Gu = sm;
@@ -1302,8 +1329,8 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   for (int e = threadIdx.x; e < 2 * GSQ; e += NT) sm[e] = zmk(0.0, 0.0);
   __syncthreads();
   if (g_gram_mma) {   // staging in Gv's region (+ X2's head): free until G_v is stored
-    gram_acc_mma(U, mu0, mu1, k, ldu, Gu, Gv);
-    gram_acc_mma(Vt, nv0, nv1, k, ldv, Gv, Gv);
+    gram_acc_mma(su, mu0, mu1, k, Gu, Gv);
+    gram_acc_mma(sv, nv0, nv1, k, Gv, Gv);
   } else {
     gram_acc(U, mu0, mu1, k, ldu, Gu, X2);
     gram_acc(Vt, nv0, nv1, k, ldv, Gv, X2);
@@ -1314,7 +1341,7 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   for (int c = threadIdx.x; c < k; c += NT) {
     const double du = Gu[c * k + c].x, dv = Gv[c * k + c].x;
     const double a = (du > 0.0 && dv > 0.0) ? sqrt(sqrt(dv / du)) : 0.0;
-    alpha[c] = a;
+    alpha[c] = c >= ksgn ? sgn * a : a;   // the sign of the second U piece rides on its scale
     ainv[c] = a > 0.0 ? 1.0 / a : 0.0;
   }
   __syncthreads();
@@ -1528,7 +1555,7 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   tri_solve_cols(X2, k, kk1, W, r, scu);
   stamp(10);
   if (r > 0) {
-    if (g_gram_mma) apply_sel_mma(U, m, ldu, mu0, mu1, pu, kk1, W, r, Uo);
+    if (g_gram_mma) apply_sel_mma(su, m, mu0, mu1, pu, kk1, W, r, Uo);
     else apply_sel(U, m, ldu, mu0, mu1, pu, kk1, W, r, Uo);
   }
   __syncthreads();
@@ -1540,7 +1567,7 @@ __device__ int gram_stage(const zc* __restrict__ U, int ldu, const zc* __restric
   __syncthreads();
   tri_solve_cols(X2, k, kk2, W2, r, scv);
   if (r > 0) {
-    if (g_gram_mma) apply_sel_mma(Vt, n, ldv, nv0, nv1, pv, kk2, W2, r, Vo);
+    if (g_gram_mma) apply_sel_mma(sv, n, nv0, nv1, pv, kk2, W2, r, Vo);
     else apply_sel(Vt, n, ldv, nv0, nv1, pv, kk2, W2, r, Vo);
   }
   if (threadIdx.x == 0 && crank == 0)
@@ -1580,19 +1607,32 @@ __global__ void __launch_bounds__(NT, 1)
   long long tc[12] = {};
   tc[0] = clock64();
   if (d.skip_slot >= 0 && ranks[d.skip_slot] == 0) return;
-  const int k = d.k_slot >= 0 ? ranks[d.k_slot] : d.k;
+  const int k = trunc_k(d, ranks);
+  const bool two = d.in_u2 >= 0;
+  const int k1 = two ? trunc_k1(d, ranks) : 0x7fffffff;
   const int m = d.m, n = d.n;
   if (k <= 0 || m == 0 || n == 0) {
     if (threadIdx.x == 0 && crank == 0) ranks[d.out_slot] = 0;
     return;
   }
   const bool multi = k > KG && k <= KMS && max(m, n) <= mn_max;
-  if (k > KG && !multi) {   // handed to the Householder kernels
-    if (threadIdx.x == 0 && crank == 0) defer[1 + atomicAdd(defer, 1)] = idx ? tix : base + pb;
+  // hand-off to the Householder kernels; a two-source problem has no materialised input for
+  // them: counted as a clipped truncation (re-factorisation with concatenations)
+  auto hand_off = [&]() {
+    if (threadIdx.x == 0 && crank == 0) {
+      if (two) atomicAdd(overflow, 1ull);
+      else defer[1 + atomicAdd(defer, 1)] = idx ? tix : base + pb;
+    }
+  };
+  if (k > KG && !multi) {
+    hand_off();
     return;
   }
   const zc* U = arena + d.in_u;
   const zc* Vt = arena + d.in_v;
+  const Src2 su = two ? Src2{U, arena + d.in_u2, d.ldu, d.ldu2, k1} : src1(U, d.ldu);
+  const Src2 sv = two ? Src2{Vt, arena + d.in_v2, d.ldv, d.ldv2, k1} : src1(Vt, d.ldv);
+  const double sgn = two ? d.sgn2 : 1.0;
   zc* sc = scratch + (int64_t)blockIdx.x * per;                  // private k x k scratch
   zc* sc0 = scratch + (int64_t)(blockIdx.x - crank) * per;      // the cluster's shared bases
   const int mu0 = slice_lo(m, crank, csize), mu1 = slice_lo(m, crank + 1, csize);
@@ -1601,18 +1641,18 @@ __global__ void __launch_bounds__(NT, 1)
   zc* Vo = aout + d.out_v;
   int sweeps = 0, r = 0;
   if (!multi) {
-    r = gram_stage(U, d.ldu, Vt, d.ldv, m, n, k, Uo, Vo, d.cap, tol, sc, overflow, S, sm, tc, &sweeps);
+    r = gram_stage(su, sv, k1, sgn, m, n, k, Uo, Vo, d.cap, tol, sc, overflow, S, sm, tc, &sweeps);
   } else {
     zc* bu[2] = {sc0 + 4 * GSQ, sc0 + 4 * GSQ + (int64_t)2 * mn_max * KG};
     zc* bv[2] = {bu[0] + (int64_t)mn_max * KG, bu[1] + (int64_t)mn_max * KG};
     int cur = 0, done = KG;
-    r = gram_stage(U, d.ldu, Vt, d.ldv, m, n, KG, bu[0], bv[0], KG, tol, sc, overflow, S, sm, tc, &sweeps);
+    r = gram_stage(su, sv, k1, sgn, m, n, KG, bu[0], bv[0], KG, tol, sc, overflow, S, sm, tc, &sweeps);
     while (done < k) {
       const int add = min(KG - r, k - done);
       // too little room left for the remaining columns (each stage costs a full Gram
       // recompression): Householder kernels -- nothing was written to the output yet
       if (add < min(g_ms_min_add, k - done)) {
-        if (threadIdx.x == 0 && crank == 0) defer[1 + atomicAdd(defer, 1)] = idx ? tix : base + pb;
+        hand_off();
         return;
       }
       // append the next columns behind the kept basis (this CTA's rows; the next Gram
@@ -1620,17 +1660,19 @@ __global__ void __launch_bounds__(NT, 1)
       const int mr = mu1 - mu0, nr = nv1 - nv0;
       for (int e = threadIdx.x; e < add * mr; e += NT) {
         const int c = e / mr, i = mu0 + e % mr;
-        bu[cur][(int64_t)(r + c) * m + i] = U[(int64_t)(done + c) * d.ldu + i];
+        const zc v = su.col(done + c)[i];
+        bu[cur][(int64_t)(r + c) * m + i] = done + c >= k1 ? zscale(v, sgn) : v;
       }
       for (int e = threadIdx.x; e < add * nr; e += NT) {
         const int c = e / nr, i = nv0 + e % nr;
-        bv[cur][(int64_t)(r + c) * n + i] = Vt[(int64_t)(done + c) * d.ldv + i];
+        bv[cur][(int64_t)(r + c) * n + i] = sv.col(done + c)[i];
       }
       __syncthreads();
       done += add;
       const bool last = done == k;
       int sw = 0;
-      r = gram_stage(bu[cur], m, bv[cur], n, m, n, r + add, last ? Uo : bu[cur ^ 1], last ? Vo : bv[cur ^ 1],
+      r = gram_stage(src1(bu[cur], m), src1(bv[cur], n), 0x7fffffff, 1.0, m, n, r + add, last ? Uo : bu[cur ^ 1],
+                     last ? Vo : bv[cur ^ 1],
                      last ? d.cap : KG, tol, sc, overflow, S, sm, tc, &sw);
       sweeps += sw;
       cur ^= 1;
@@ -1651,6 +1693,33 @@ __global__ void __launch_bounds__(NT, 1)
       for (int q = 5; q < 12; ++q) atomicAdd(prof + 11 + q, (unsigned long long)tc[q]);
     }
   }
+}
+
+// clusters of csize CTAs of k_trunc_gram the device can hold at once (a cluster needs csize
+// free SMs inside ONE GPC, so this is below 148 / csize: 32 clusters of 4 on a B200)
+int gram_max_clusters(int csize) {
+  const int smem = (3 * GSQ + KG + 1) * (int)sizeof(zc);
+  if (cudaFuncSetAttribute(k_trunc_gram, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)(148 * csize));
+  cfg.blockDim = dim3(NT);
+  cfg.dynamicSmemBytes = (size_t)smem;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = (unsigned)csize;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  int n = 0;
+  if (cudaOccupancyMaxActiveClusters(&n, k_trunc_gram, &cfg) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  return n;
 }
 
 void launch_gram(zc* arena, zc* aout, int* ranks, const TruncDesc* d_desc, int nd, double tol,

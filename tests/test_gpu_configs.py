@@ -156,3 +156,18 @@ def test_clipped_temporary_rank_refactors(monkeypatch):
     assert st.get("cap_retries", 0) >= 1 and st.get("trunc_overflow", 0) == 0, st
     rel = np.linalg.norm(r.solution - g["x"]) / np.linalg.norm(g["x"])
     assert rel <= 10 * prob.aca_tol, rel
+
+
+def test_two_source_recompression_matches_reference(monkeypatch):
+    """CBIE_TWO_SOURCE=1: T + s U V^H is recompressed from its two pieces read in place
+    (no materialised concatenation, output over the target).  Same solution as the
+    concatenating default, within the reference bar."""
+    from paper_2408_17116_b200.solver import solve_direct
+    monkeypatch.setenv("CBIE_TWO_SOURCE", "1")
+    g = golden("cfg2_solve.npz")
+    prob, gen = _gen(2)
+    r = solve_direct(prob)
+    st = r.metrics["device"]["hlu"]
+    assert st.get("trunc_overflow", 0) == 0 and st.get("tasks_concat", 1) < 0.6 * st.get("tasks_trunc", 0), st
+    rel = np.linalg.norm(r.solution - g["x"]) / np.linalg.norm(g["x"])
+    assert rel <= 10 * prob.aca_tol, rel
