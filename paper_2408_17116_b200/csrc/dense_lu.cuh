@@ -464,13 +464,16 @@ __global__ void __launch_bounds__(LU_NT) k_rcond_blk(const zc* __restrict__ ar, 
 // TRSM with a factored diagonal leaf (variants as k_trsm), blocked:
 // one 512-thread CTA per (descriptor, 32-column chunk of Y), chunk in shared memory
 // ---------------------------------------------------------------------------
+// grid = tile list of the group (x: solve, y: 32-column chunk over its static width), as for
+// k_gemm_mma: the widths of a group run from one rank to a whole 1536-column block
 __global__ void __launch_bounds__(LU_NT, 2) k_trsm_blk(zc* __restrict__ ar, const int* __restrict__ ranks,
                                                     const int* __restrict__ pivs,
-                                                    const TrsmD* __restrict__ ds) {
-  const TrsmD d = ds[blockIdx.y];
+                                                    const TrsmD* __restrict__ ds, const uint2* __restrict__ tiles) {
+  const uint2 tl = tiles[blockIdx.x];
+  const TrsmD d = ds[tl.x];
   const int p = dimv(d.p, ranks), n = d.n;
-  if (blockIdx.x == 0 && threadIdx.x == 0) flop_add(4.0 * n * n * p);
-  const int c0 = blockIdx.x * LU_NB;
+  if (tl.y == 0 && threadIdx.x == 0) flop_add(4.0 * n * n * p);
+  const int c0 = (int)tl.y * LU_NB;
   if (c0 >= p) return;
   const int nc = min(LU_NB, p - c0);
   extern __shared__ __align__(16) unsigned char smem_raw[];

@@ -1384,6 +1384,9 @@ struct Grp {
   // OP_TRUNC, Gram path: [start, start + nsmall) small blocks, [nsmall, split) large blocks
   // recompressed by clusters of cbig CTAs per problem (mn_small: largest small side)
   int nsmall = -1, cbig = 1, mn_small = 0;
+  // OP_GEMM: tile lists of the two parts (64-wide tiles for [0, split), 32-wide for the rest)
+  int64_t tile0[2] = {0, 0};
+  int ntile[2] = {0, 0};
   std::vector<int> deps;   // groups of OTHER kinds this group waits for (multi-stream executor)
 };
 
@@ -1400,6 +1403,8 @@ struct Plan {
   std::vector<TruncDesc> tr;
   std::vector<DenseLRDesc> dl;
   DBuf<GemmD> dg;
+  std::vector<uint2> gt;   // tile lists of the GEMM groups (k_gemm_mma)
+  DBuf<uint2> dgt;
   DBuf<EwD> de;
   DBuf<ConcatD> dc;
   DBuf<Piece> dcp;   // piece pool of the concatenations
@@ -1474,6 +1479,25 @@ void make_plan(Plan& P, cudaStream_t s, const Recorder* Rx = nullptr, const std:
       };
       std::stable_partition(g.begin() + gr.start, g.end(), big);
       gr.split = (int)std::count_if(g.begin() + gr.start, g.end(), big);
+      for (int part = 0; part < 2; ++part) {
+        const int b = part == 0 ? 0 : gr.split, e = part == 0 ? gr.split : gr.count, bn = part == 0 ? 64 : 32;
+        gr.tile0[part] = (int64_t)P.gt.size();
+        for (int q = b; q < e; ++q) {
+          const GemmD& x = g[gr.start + q];
+          const int tm = ceil_div(std::max(x.m.v, 1), GM_BM), tn = ceil_div(std::max(x.n.v, 1), bn);
+          for (int tj = 0; tj < tn; ++tj)
+            for (int ti = 0; ti < tm; ++ti) P.gt.push_back(make_uint2((unsigned)q, (unsigned)ti | (unsigned)tj << 16));
+        }
+        gr.ntile[part] = (int)((int64_t)P.gt.size() - gr.tile0[part]);
+      }
+    }
+    if (kind == OP_TRSM) {   // tile list: (solve, 32-column chunk)
+      gr.tile0[0] = (int64_t)P.gt.size();
+      for (int q = 0; q < gr.count; ++q) {
+        const int nc = ceil_div(std::max(t[gr.start + q].p.v, 1), LU_NB);
+        for (int c = 0; c < nc; ++c) P.gt.push_back(make_uint2((unsigned)q, (unsigned)c));
+      }
+      gr.ntile[0] = (int)((int64_t)P.gt.size() - gr.tile0[0]);
     }
     if (kind == OP_TRUNC) {
       // factor-form problems (Gram path + hand-offs) first, dense-mode ones after; the
@@ -1554,6 +1578,7 @@ void make_plan(Plan& P, cudaStream_t s, const Recorder* Rx = nullptr, const std:
   }
   P.ddl.upload(dl, s);
   P.dg.upload(g, s);
+  P.dgt.upload(P.gt, s);
   P.de.upload(e, s);
   P.dc.upload(c, s);
   P.dcp.upload(R.cat_pieces, s);
@@ -1712,6 +1737,17 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
         const int split = g64 ? gr.split : 0;
         auto launch = [&](int b, int e, bool wide) {
           if (e <= b) return;
+          if (dmma_gemm && g64) {   // FP64 tensor-core tiles over the part's tile list
+            const int part = wide ? 0 : 1;
+            if (gr.ntile[part] == 0) return;
+            if (wide)
+              k_gemm_mma<64><<<gr.ntile[part], 256, gm_smem_bytes(64), s>>>(arena, ranks, dg.p + gr.start,
+                                                                           P.dgt.p + gr.tile0[part]);
+            else
+              k_gemm_mma<32><<<gr.ntile[part], 256, gm_smem_bytes(32), s>>>(arena, ranks, dg.p + gr.start,
+                                                                           P.dgt.p + gr.tile0[part]);
+            return;
+          }
           int mt = 1, nt = 1;
           for (int i = b; i < e; ++i) {
             mt = std::max(mt, g[gr.start + i].m.v);
@@ -1719,14 +1755,7 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
           }
           for (int b0 = b; b0 < e; b0 += 65535) {
             const int nb = std::min(65535, e - b0);
-            if (dmma_gemm) {   // FP64 tensor-core tiles (64 x 64, or 64 x 32 for the ragged products)
-              if (wide)
-                k_gemm_mma<64><<<dim3(ceil_div(mt, GM_BM), ceil_div(nt, 64), nb), 256, gm_smem_bytes(64), s>>>(arena, ranks,
-                                                                                            dg.p + gr.start + b0);
-              else
-                k_gemm_mma<32><<<dim3(ceil_div(mt, GM_BM), ceil_div(nt, 32), nb), 256, gm_smem_bytes(32), s>>>(arena, ranks,
-                                                                                            dg.p + gr.start + b0);
-            } else if (wide)
+            if (wide)
               k_gemm64<<<dim3(ceil_div(mt, GT64), ceil_div(nt, GT64), nb), 256, 0, s>>>(arena, ranks,
                                                                                        dg.p + gr.start + b0);
             else
@@ -1768,13 +1797,15 @@ Exec run_plan(Plan& P, zc* arena, int* ranks, int* piv, double* rcond, int* flag
       case OP_TRSM: {
         int cmax = 1;
         for (int i = 0; i < gr.count; ++i) cmax = std::max(cmax, ceil_div(t[gr.start + i].p.v, TS_COLS));
-        for (int b0 = 0; b0 < gr.count; b0 += 65535) {
-          int nb = std::min(65535, gr.count - b0);
-          if (blk_lu)
-            k_trsm_blk<<<dim3(ceil_div((int64_t)cmax * TS_COLS, LU_NB), nb), LU_NT, trsm_blk_smem, s>>>(
-                arena, ranks, piv, dt.p + gr.start + b0);
-          else
+        if (blk_lu) {
+          if (gr.ntile[0] > 0)
+            k_trsm_blk<<<gr.ntile[0], LU_NT, trsm_blk_smem, s>>>(arena, ranks, piv, dt.p + gr.start,
+                                                                 P.dgt.p + gr.tile0[0]);
+        } else {
+          for (int b0 = 0; b0 < gr.count; b0 += 65535) {
+            int nb = std::min(65535, gr.count - b0);
             k_trsm<<<dim3(cmax, nb), 256, trsm_smem, s>>>(arena, ranks, piv, dt.p + gr.start + b0);
+          }
         }
         break;
       }

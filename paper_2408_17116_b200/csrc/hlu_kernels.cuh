@@ -148,15 +148,20 @@ __device__ __forceinline__ void gm_cp16(void* sdst, const void* gsrc, bool valid
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gsrc), "r"(valid ? 16 : 0) : "memory");
 }
 constexpr size_t gm_smem_bytes(int bn) { return (size_t)2 * GM_BK * (GM_BM + 2 + bn + 2) * sizeof(zc); }
+// The grid is a TILE LIST built with the plan (x: product of the group, y: tile row |
+// tile column << 16, over the products' static sizes): a group mixes products from 100 x 76
+// to 192 x 1536, and a (max rows, max columns, products) grid launched ~10 x more CTAs than
+// there are tiles, every one of them fetching its descriptor before leaving.
 template <int BN>
 __global__ void __launch_bounds__(256, 2) k_gemm_mma(zc* __restrict__ ar, const int* __restrict__ ranks,
-                                                     const GemmD* __restrict__ ds) {
+                                                     const GemmD* __restrict__ ds, const uint2* __restrict__ tiles) {
   constexpr int LDA = GM_BM + 2, LDB = BN + 2;
   constexpr int NB = BN / 16;   // m8n8 column blocks per warp
-  const GemmD d = ds[blockIdx.z];
+  const uint2 tl = tiles[blockIdx.x];
+  const GemmD d = ds[tl.x];
   const int m = dimv(d.m, ranks), n = dimv(d.n, ranks), k = dimv(d.k, ranks);
-  const int i0 = blockIdx.x * GM_BM, j0 = blockIdx.y * BN;
-  if (blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0) flop_add(8.0 * m * n * k);
+  const int i0 = (int)(tl.y & 0xffffu) * GM_BM, j0 = (int)(tl.y >> 16) * BN;
+  if (tl.y == 0 && threadIdx.x == 0) flop_add(8.0 * m * n * k);
   if (i0 >= m || j0 >= n) return;
   extern __shared__ __align__(16) unsigned char gm_smem[];
   zc(*sA)[GM_BK * LDA] = reinterpret_cast<zc(*)[GM_BK * LDA]>(gm_smem);
