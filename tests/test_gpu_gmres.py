@@ -37,3 +37,18 @@ def test_gmres_restart_and_iteration_cap():
     assert r.iterations == 12 and not r.converged and r.residual > 1e-10
     r2 = solve_gmres(prob, restart=5, max_iters=400)
     assert r2.converged and r2.residual <= 1e-10
+
+
+def test_small_problem_iterates_on_the_dense_operator():
+    """N <= 600: the reference's solve_gmres uses the dense equilibrated matrix
+    (solver.py:278-287); here one dense leaf covers the matrix and the metrics say so."""
+    from paper_2408_17116_b200 import geometry as geo, kernels as ker
+    from paper_2408_17116_b200.solver import Problem, solve_gmres
+    vac = ker.Medium.from_relative(1.0, 1.0, 1.0)
+    prob = Problem(geo.unit_sphere_patches(0.5, 0, (4, 4)), ker.FormulationSpec(ker.MFIE_PEC, vac),
+                   ker.PlaneWave([0, 0, 1], [1, 0, 0], 1.0), gmres_tol=1e-10)
+    r = solve_gmres(prob)
+    assert r.metrics["operator"] == "dense" and r.converged
+    assert r.metrics["compression_rate"] <= 1e-12          # nothing compressed: one dense leaf
+    g = golden("small_solve.npz")
+    assert np.linalg.norm(r.solution - g["x_dense"]) / np.linalg.norm(g["x_dense"]) <= 1e-8

@@ -120,3 +120,36 @@ def test_hlu_singular_diagonal():
     H = hm.HMatrix.from_generator(pts, 1, 4, 2.0, ZeroGen(), 1e-8)
     with pytest.raises(SingularDiagonal):
         hm.hlu_factor(H, 1e-8)
+
+
+class RandGen:
+    """Dense random complex matrix (no diagonal dominance: the LU really pivots)."""
+
+    def __init__(self, n, seed):
+        rng = np.random.default_rng(seed)
+        self.A = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+
+    def block(self, rows, cols):
+        return self.A[np.ix_(np.asarray(rows), np.asarray(cols))]
+
+
+@pytest.mark.parametrize("n", [5, 37, 100, 192, 256, 384])
+def test_diagonal_leaf_lu_matches_lapack_pivot_for_pivot(n):
+    """One dense diagonal leaf factored by k_getrf_blk (zgetrf at hmatrix.py:835): the row
+    interchanges equal LAPACK's (scipy.linalg.lu_factor) and the factors agree to rounding."""
+    import scipy.linalg as sla
+    hm = _hm()
+    rng = np.random.default_rng(n)
+    pts = rng.standard_normal((n, 3))
+    gen = RandGen(n, 100 + n)
+    H = hm.HMatrix.from_generator(pts, 1, n, 1.0, gen, 1e-12)
+    perm = H.dof_perm
+    Ap = gen.A[np.ix_(perm, perm)]
+    F = hm.hlu_factor(H, 1e-12)
+    kind, LU, piv = F.leaf(0)
+    lu_ref, piv_ref = sla.lu_factor(Ap)
+    assert kind == "lu" and np.array_equal(piv, piv_ref)
+    assert np.abs(LU - lu_ref).max() <= 1e-11 * np.abs(lu_ref).max()
+    b = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    x = F.solve(b)
+    assert np.linalg.norm(gen.A @ x - b) <= 1e-10 * np.linalg.norm(b)
