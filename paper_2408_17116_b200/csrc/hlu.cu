@@ -2128,7 +2128,13 @@ static int64_t hlu_layout(cbie_hlu* F, std::vector<CopySeg>& segs) {
     } else {
       const int r = H->h_rank[li];
       const int want = F->lean ? r + F->cap_boost * std::max(16, r / 2) : F->cap_boost * (2 * r + 48);
-      L.cap = std::max(1, std::min(std::max(1, std::min(L.m, L.n) / 2), want));
+      // first attempt: at most the demotion budget min(m, n) / 2 (beyond it a low-rank leaf
+      // stores more than the dense block); a re-factorisation after a clipped truncation may
+      // use the full min(m, n), where no truncation can be clipped any more -- config 3
+      // (Mueller, eps_r = 16, tol 1e-5) has 664 fill-in ranks above the budget, which the
+      // reference, whose truncate_lowrank has no cap, simply keeps
+      const int budget = F->cap_boost > 1 ? std::min(L.m, L.n) : std::max(1, std::min(L.m, L.n) / 2);
+      L.cap = std::max(1, std::min(budget, want));
       L.off_u = leaf_end;
       leaf_end += (int64_t)L.m * L.cap;
       L.off_v = leaf_end;
@@ -2517,12 +2523,27 @@ int cbie_hlu_factor(cbie_hmat* h, double trunc_tol, cbie_hlu** out) {
     F = new cbie_hlu();
     F->H = h;
     F->tol = trunc_tol;
-    // a recompression whose kept rank exceeds its leaf's factor capacity (2 r + 48) is
-    // clipped and counted; re-factor with larger capacities until none is clipped (the
-    // reference keeps every singular value above tol * s_0).  At the demotion budget
-    // min(m, n) / 2 everywhere a clipped truncation is a RankOverflow.
+    // a recompression whose kept rank exceeds its leaf's factor capacity (2 r + 48, at most
+    // min(m, n) / 2) is clipped and counted; re-factor with larger capacities (up to the full
+    // min(m, n), where nothing can be clipped) until none is clipped -- the reference keeps
+    // every singular value above tol * s_0.
+    // the boost a block structure needed is remembered (per process): the next
+    // factorisation of the same mesh / tolerance starts there instead of failing first
+    static std::map<uint64_t, int> learned;
+    uint64_t skey = 1469598103934665603ull;
+    for (const auto& L : h->tree.leaves) skey = fnv(skey, L.kind * 1000003ll + L.m * 1009ll + L.n);
+    skey = fnv(skey, (int64_t)(trunc_tol * 1e15));
+    skey = fnv(skey, (int64_t)(getenv("CBIE_TMP_CAP_MULT") ? atof(getenv("CBIE_TMP_CAP_MULT")) * 1000 : -1));
+    skey = fnv(skey, getenv("CBIE_TWO_SOURCE") ? 1 : 0);
+    {
+      auto it = learned.find(skey);
+      if (it != learned.end()) F->cap_boost = it->second;
+    }
     for (int attempt = 0;; ++attempt) {
       hlu_factor_impl(F);
+      if (getenv("CBIE_MEMLOG"))
+        fprintf(stderr, "[cbie] H-LU attempt %d (capacity boost %d): %.0f clipped truncations, %.0f ms\n", attempt,
+                F->cap_boost, F->stat["trunc_overflow"], F->stat["factor_device_ms"]);
       if (F->stat["trunc_overflow"] == 0) break;
       if (F->cap_boost >= (1 << 12))
         throw cbie_error(CBIE_ERANK_OVERFLOW, "H-LU recompression rank exceeds the leaf budget");
@@ -2530,6 +2551,7 @@ int cbie_hlu_factor(cbie_hmat* h, double trunc_tol, cbie_hlu** out) {
       F->stat["cap_retries"] = attempt + 1;
     }
     F->stat["cap_boost"] = F->cap_boost;
+    if (F->cap_boost > 1) learned[skey] = F->cap_boost;
     *out = F;
   } catch (const cbie_error& e) {
     h->ctx->err = e.what();

@@ -171,3 +171,21 @@ def test_two_source_recompression_matches_reference(monkeypatch):
     assert st.get("trunc_overflow", 0) == 0 and st.get("tasks_concat", 1) < 0.6 * st.get("tasks_trunc", 0), st
     rel = np.linalg.norm(r.solution - g["x"]) / np.linalg.norm(g["x"])
     assert rel <= 10 * prob.aca_tol, rel
+
+
+@pytest.mark.slow
+def test_cfg3_hlu_completes_beyond_the_demotion_budget():
+    """Config 3 (Mueller, eps_r = 16, tol 1e-5): 664 fill-in ranks exceed min(m, n) / 2.  The
+    reference's truncate_lowrank has no cap (hmatrix.py:412-426); here the first attempt counts
+    the clipped truncations and the re-factorisation with full-size capacities keeps every
+    singular value, so the solve meets the residual bar instead of raising RankOverflow."""
+    from paper_2408_17116_b200 import hmatrix as hm
+    prob, gen = _gen(3)
+    H = hm.HMatrix(gen, prob.n_leaf, prob.eta, prob.aca_tol)
+    F = hm.hlu_factor(H, prob.effective_trunc_tol)
+    st = F.stats()
+    assert st["trunc_overflow"] == 0 and st.get("cap_boost", 1) > 1, st
+    b = gen.rhs(prob.excitation) * gen.row_scale
+    x = F.solve(b)
+    res = np.linalg.norm(H.matvec(x) - b) / np.linalg.norm(b)
+    assert res <= 100 * prob.aca_tol, res
