@@ -141,14 +141,21 @@ __device__ __forceinline__ int lu_block_argmax(double bv, int bi, double* sv, in
     si[threadIdx.x >> 5] = bi;
   }
   __syncthreads();
-  double B = sv[0];
-  int I = si[0];
+  // every warp reduces the NWARP partials by shuffles (a serial loop over them in every
+  // thread was 13 % of k_getrf_blk's stall samples)
+  static_assert(NWARP <= 32, "one lane per partial");
+  const int l = threadIdx.x & 31;
+  double B = l < NWARP ? sv[l] : -1.0;
+  int I = l < NWARP ? si[l] : 0x7fffffff;
 #pragma unroll
-  for (int w = 1; w < NWARP; ++w)
-    if (sv[w] > B || (sv[w] == B && si[w] < I)) {
-      B = sv[w];
-      I = si[w];
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, B, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, I, o);
+    if (ov > B || (ov == B && oi < I)) {
+      B = ov;
+      I = oi;
     }
+  }
   return I;
 }
 
@@ -244,8 +251,12 @@ __global__ void __launch_bounds__(GF_NT) k_getrf_blk(zc* __restrict__ ar, int* _
       // (independent read-modify-writes instead of a per-row chain over the columns)
       {
         const int rows = n - col - 1, cols = jb - c - 1;
+        // e -> (e % rows, e / rows) through a float reciprocal: exact here (e + 0.5 is never
+        // within rounding of a multiple of rows for e < 2^14), no integer division
+        const float rrec = rows > 0 ? 1.0f / (float)rows : 0.0f;
         for (int e = tid; e < rows * cols; e += GF_NT) {
-          const int i = col + 1 + e % rows, cc = c + 1 + e / rows;
+          const int q = (int)(((float)e + 0.5f) * rrec);
+          const int i = col + 1 + e - q * rows, cc = c + 1 + q;
           P[cc * n + i] = zsub(P[cc * n + i], zmul(P[c * n + i], P[cc * n + col]));
         }
       }
