@@ -1203,9 +1203,12 @@ __device__ int herm_jacobi(zc* H, int n, zc* X, Smem& S) {
         // H <- J^H H J by disjoint 2 x 2 blocks (rows of pair t1, columns of pair t2),
         // X <- X J by (row, pair) items; no two items touch the same entry.
         // J = [cs se; -conj(se) cs] acts on the (p, q) columns.
+        // item -> (index, pair) through float reciprocals: exact for these sizes (e + 0.5 is
+        // never within rounding of a multiple of np / n), no integer division per item
+        const float rnp = 1.0f / (float)np, rn = 1.0f / (float)n;
         for (int e = tid; e < np * np + n * np; e += JT) {
           if (e < np * np) {
-            const int t1 = e % np, t2 = e / np;
+            const int t2 = (int)(((float)e + 0.5f) * rnp), t1 = e - t2 * np;
             const int a0 = rp[t1], a1 = rq[t1], b0 = rp[t2], b1 = rq[t2];
             const bool va0 = a0 < n, va1 = a1 < n, vb0 = b0 < n, vb1 = b1 < n;
             const double c1 = rc[t1], c2 = rc[t2];
@@ -1223,7 +1226,7 @@ __device__ int herm_jacobi(zc* H, int n, zc* X, Smem& S) {
             if (va1 && vb1) H[b1 * n + a1] = zadd(zmul(zconj(s1), cpq), zscale(cqq, c1));
           } else {
             const int f = e - np * np;
-            const int i = f % n, t = f / n;
+            const int t = (int)(((float)f + 0.5f) * rn), i = f - t * n;
             const int p = rp[t], q = rq[t];
             if (p >= n || q >= n) continue;
             const double cs = rc[t];
