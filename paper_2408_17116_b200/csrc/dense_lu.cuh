@@ -18,6 +18,7 @@
 // done as a shared-memory-panel GEMM.  rcond uses the same zlacn2 iteration
 // as before on top of the blocked solves.
 #pragma once
+#include <cuda/barrier>
 
 constexpr int LU_NT = 256;          // threads of the blocked LU / solve kernels
 constexpr int LU_NW = LU_NT / 32;
@@ -490,11 +491,30 @@ __global__ void __launch_bounds__(LU_NT, 2) k_trsm_blk(zc* __restrict__ ar, cons
   extern __shared__ __align__(16) unsigned char smem_raw[];
   zc* S = reinterpret_cast<zc*>(smem_raw);   // [nc][n]
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
-  for (int e = tid; e < n * nc; e += LU_NT) {
-    const int i = e % n, j = e / n;
-    S[j * n + i] = ar[vidx(d.Y, i, c0 + j)];
+  if (!d.Y.tr) {
+    // untransposed right-hand side: every column of the chunk is one contiguous run of n
+    // complex numbers -- staged by the bulk-copy engine (TMA, cp.async.bulk through
+    // cuda::memcpy_async on a shared-memory barrier), one copy per column issued by one
+    // thread, instead of a load / store round trip through every thread's registers
+#pragma nv_diag_suppress static_var_with_dynamic_init
+    __shared__ cuda::barrier<cuda::thread_scope_block> bar;
+    if (tid == 0) {
+      init(&bar, LU_NT);
+      cuda::device::experimental::fence_proxy_async_shared_cta();
+    }
+    __syncthreads();
+    if (tid == 0)
+      for (int j = 0; j < nc; ++j)
+        cuda::memcpy_async(S + (size_t)j * n, ar + d.Y.off + (int64_t)(c0 + j) * d.Y.ld,
+                           cuda::aligned_size_t<16>((size_t)n * sizeof(zc)), bar);
+    bar.arrive_and_wait();
+  } else {
+    for (int e = tid; e < n * nc; e += LU_NT) {
+      const int i = e % n, j = e / n;
+      S[j * n + i] = ar[vidx(d.Y, i, c0 + j)];
+    }
+    __syncthreads();
   }
-  __syncthreads();
   const zc* A = ar + d.T;
   // variant 0: P^T L  -> row swaps then mode 0;  1: U -> mode 1;  2: U^T (lower, no conj)
   if (d.variant == 0) {
