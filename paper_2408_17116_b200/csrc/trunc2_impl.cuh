@@ -1185,12 +1185,16 @@ __device__ int herm_jacobi(zc* H, int n, zc* X, Smem& S) {
           if (p < n && q < n) {
             const double al = H[p * n + p].x, be = H[q * n + q].x;
             const zc gm = H[q * n + p];   // h_pq
-            const double g = sqrt(zabs2(gm));
-            if (g > 1e-300 && g > 1e-17 * sqrt(fabs(al * be))) {
-              const double zeta = (be - al) / (2.0 * g);
+            // same rotation as before (|h_pq| > 1e-17 sqrt(|h_pp h_qq|), tan from zeta) with
+            // half the dependent sqrt / divide chain: this single warp's latency is what the
+            // other fifteen wait for at the barrier below
+            const double g2 = zabs2(gm);
+            if (g2 > 1e-290 && g2 > 1e-34 * fabs(al * be)) {
+              const double ig = rsqrt(g2);
+              const double zeta = (be - al) * 0.5 * ig;
               const double tt = (zeta >= 0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-              cs = 1.0 / sqrt(1.0 + tt * tt);
-              const double sn = cs * tt, ig = 1.0 / g;
+              cs = rsqrt(1.0 + tt * tt);
+              const double sn = cs * tt;
               se = zmk(gm.x * ig * sn, gm.y * ig * sn);
             }
           }
